@@ -1,0 +1,209 @@
+/*
+ * pipespec.h — C ABI of the B200-native PipeSpec verify hot path.
+ *
+ * PipeSpec (arXiv 2505.01572) states the problem as
+ *   "Require: Input prompt, Models [M_0...M_K];  Ensure: Generated sequence O_K"
+ *   (Alg.1), greedy decoding.
+ * Each model M_i is a *stage* that owns its token buffer O_i ("Let O_i be token
+ * buffer for model i") and a paged KV cache.  The hot path is the
+ * per-stage verification pass (Alg.1): one bf16 forward of M_i over
+ * [pending token, d_0 .. d_{w-1}], greedy argmax per row, the longest matching
+ * prefix a, append d[0:a] + correction/bonus token (reading R1 of DESIGN.md),
+ * KV truncation (rollback) and the rejection signal to earlier stages.
+ *
+ * Conventions for every call:
+ *  - All sizes are int32/int64; all structs are plain C.
+ *  - Device pointers are CUDA device addresses on the stage's device; "host"
+ *    pointers are ordinary (pageable or pinned) host memory.  A pointer that
+ *    may be either is classified with cudaPointerGetAttributes.
+ *  - Weights and the KV pool are BORROWED: the caller (e.g. PyTorch) owns them
+ *    and keeps them alive until ps_stage_destroy.  The stage owns its token
+ *    buffer, page table, scratch activations and CUDA graphs.
+ *  - Errors: every call returns a ps_status; on error nothing observable
+ *    changed (out-params untouched, buffer unchanged) and ps_last_error()
+ *    returns a thread-local message.  No C++ exception crosses the ABI.
+ *  - Threading: a stage is single-owner: one thread drives it;
+ *    different stages may be driven concurrently from different threads.
+ *  - Determinism: identical inputs give bit-identical results; the
+ *    kernels are row-bucket invariant (fixed split order, absolute-position KV
+ *    chunking, no floating-point atomics), so a verify over w drafts yields the
+ *    same per-row logits as w+1 single-token steps.
+ *  - There is no CPU fallback: without a usable sm_100a device every compute
+ *    call returns PS_E_CUDA.
+ */
+#ifndef PIPESPEC_H_
+#define PIPESPEC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ps_status;
+#define PS_OK          0
+#define PS_E_INVALID  -1  /* bad argument / config (SPEC exit 2)              */
+#define PS_E_CONTRACT -2  /* engine contract violated, e.g. rollback keep > len*/
+#define PS_E_CAPACITY -3  /* out of KV pages or beyond max_seq                        */
+#define PS_E_CUDA     -4  /* CUDA error or no sm_100a device                          */
+#define PS_E_NCCL     -5  /* collective failure (tensor-parallel stages)              */
+#define PS_E_STALE    -6  /* operation discarded by an epoch change (runtime)         */
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* ps_last_error(void);
+
+/* Library/ABI version (major*10000 + minor*100 + patch). */
+int32_t ps_version(void);
+
+/* Model shape (public HF LLaMA configs; reading R19).
+ * Validated by ps_stage_create: n_heads % n_kv_heads == 0,
+ * head_dim in {64,128}, d_model % 64 == 0, d_ffn % 64 == 0, vocab >= 2. */
+typedef struct ps_model_shape {
+  int32_t vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, d_ffn;
+  float rms_eps, rope_theta;
+  int32_t rope_kind;        /* 0 plain rotate-half, 1 llama3 frequency scaling */
+  float rope_factor, lo_ff, hi_ff;
+  int32_t rope_orig_max;
+  int32_t tied_lm_head;     /* 1: lm_head == embed */
+} ps_model_shape;
+
+/* Per-layer weight slots, in this order (PyTorch nn.Linear layout [out,in]). */
+enum { PS_WQ = 0, PS_WK, PS_WV, PS_WO, PS_WG, PS_WU, PS_WD, PS_N_ATTN, PS_N_MLP, PS_LAYER_SLOTS };
+
+/* bf16 device pointers, row-major, 16-byte aligned.  `layers` is a HOST array
+ * of n_layers*PS_LAYER_SLOTS device pointers.  Borrowed. */
+typedef struct ps_weights {
+  const void* embed;        /* [vocab, d_model]                       */
+  const void* lm_head;      /* [vocab, d_model] (== embed when tied)  */
+  const void* final_norm;   /* [d_model]                              */
+  const void* const* layers;
+} ps_weights;
+
+/* Device placement.  Tensor parallelism (tp_size > 1) is reserved for the
+ * multi-GPU build; this build accepts tp_size == 1 only (else PS_E_INVALID). */
+typedef struct ps_placement {
+  int32_t device;           /* CUDA ordinal */
+  void* nccl_comm;          /* NULL, or a torch ProcessGroupNCCL _comm_ptr */
+  int32_t tp_rank, tp_size;
+} ps_placement;
+
+/* Stage options.  kv_pool: device buffer of kv_pool_bytes (>= the value of
+ * ps_kv_pool_bytes for max_seq), borrowed; its layout is private to the
+ * library ([page][layer][K|V][kv_head][page_size][head_dim] bf16).
+ * stream: a cudaStream_t the stage enqueues all work on (NULL = a stream the
+ * stage creates). */
+typedef struct ps_stage_opts {
+  int32_t max_seq;          /* max tokens in O_i (prompt + generated), >= 2   */
+  int32_t max_window;       /* max w accepted by ps_verify, 0..31             */
+  int32_t page_size;        /* tokens per KV page, power of two in [16,256]   */
+  void* kv_pool;
+  int64_t kv_pool_bytes;
+  void* stream;
+  int32_t use_graphs;       /* 1: capture one CUDA graph per rows bucket      */
+} ps_stage_opts;
+
+typedef struct ps_stage ps_stage;
+
+/* Bytes of KV pool a stage of this shape needs for max_seq tokens. */
+int64_t ps_kv_pool_bytes(const ps_model_shape* shape, int32_t max_seq, int32_t page_size);
+
+/* Create a stage: validates the shape, builds TMA descriptors over the
+ * borrowed weights, allocates scratch, and (optionally) captures graphs.
+ * O_i starts empty; call ps_prefill before ps_draft / ps_verify. */
+ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* weights,
+                          const ps_placement* placement, const ps_stage_opts* opts,
+                          ps_stage** out);
+ps_status ps_stage_destroy(ps_stage* stage);
+
+/* O_i := tokens[0:n] (host, n >= 1, every token < vocab, n <= max_seq).
+ * Keeps the KV of the longest common prefix with the current O_i, then runs
+ * the forward over the remaining positions so KV covers 0..n-2 and tokens[n-1]
+ * is pending.  Serves as prefill, as catch-up after a resync, and as the
+ * extend half of "rollback O_i to match O_j". */
+ps_status ps_prefill(ps_stage* stage, const int32_t* tokens, int32_t n);
+
+/* n_steps greedy autoregressive steps (rows = 1 each; Alg.1
+ * "Generate next token, append to O_0"), appended to O_i; the tokens are
+ * written to out_tokens[0:n_steps] (host).  Equals ps_verify with w = 0,
+ * repeated.  With a synthetic-alpha override set (ps_set_synthetic), the
+ * emitted token is the override's on-path token. */
+ps_status ps_draft(ps_stage* stage, int32_t n_steps, int32_t* out_tokens);
+
+/* Verification pass (Alg.1).  With len(O_i) = n, window[j] (host or
+ * device, int32) is the draft for position n+j, 0 <= w <= max_window.  Rows
+ * [x[n-1], d_0..d_{w-1}] at positions n-1..n-1+w are forwarded; pred_j is the
+ * argmax of row j's fp32 logits (lowest index on ties, reading R12);
+ *   a    = max{ j <= w : pred_t == d_t for all t < j }   -> *accepted_len
+ *   next = pred_a  (correction if a < w, bonus if a == w)  -> *next_token
+ * O_i becomes x ++ d[0:a] ++ [next], kv_len = n + a, and KV pages wholly at
+ * or beyond kv_len are freed.  A rejection (a < w) means the caller must
+ * resync stages j < i to O_i (keep = n + a + 1).
+ * opt_logits: NULL, or host/device float [w+1][vocab] receiving the rows'
+ * logits.  Errors: w > max_window or token >= vocab -> PS_E_INVALID;
+ * n + w > max_seq or no page -> PS_E_CAPACITY; empty O_i -> PS_E_CONTRACT. */
+ps_status ps_verify(ps_stage* stage, const int32_t* window, int32_t w,
+                    int32_t* accepted_len, int32_t* next_token, float* opt_logits);
+
+/* Rollback: requires 1 <= keep_len <= len(O_i) else PS_E_CONTRACT.
+ * O_i := O_i[0:keep_len], kv_len := min(kv_len, keep_len-1), pending :=
+ * O_i[keep_len-1]; frees pages wholly beyond kv_len (O(#freed pages)).
+ * keep_len == len(O_i) is a no-op. */
+ps_status ps_kv_rollback(ps_stage* stage, int64_t keep_len);
+
+/* Read O_i into out[0:min(cap,len)] (host); *len = len(O_i). */
+ps_status ps_stage_tokens(const ps_stage* stage, int32_t* out, int64_t cap, int64_t* len);
+
+typedef struct ps_stage_info {
+  int64_t n_tokens, kv_len, pages_in_use, pages_total;
+  int64_t launches_per_verify;  /* kernels one verify pass enqueues */
+  int32_t rows_buckets[4];      /* padded row counts with captured graphs */
+} ps_stage_info;
+ps_status ps_stage_get_info(const ps_stage* stage, ps_stage_info* info);
+
+/* Synthetic-alpha override (SURVEY §8(c)
+ * c.1 #8).  S: device or host int32 target stream (the real M_K greedy stream
+ * after the prompt), len_S entries; n_prompt: prompt length; level i and top K
+ * (this stage is M_i of a K+1 model chain); alphas[j] = alpha_{j,j+1} for
+ * j = i..K-1; seed: counter-generator seed.  While the stage's context is
+ * on-path (generated tokens == S prefix) every predicted token is replaced by
+ * the chained synthetic token; off-path predictions are the model's own.
+ * The forward still runs in full.  len_S == 0 disables the override. */
+ps_status ps_set_synthetic(ps_stage* stage, const int32_t* S, int32_t len_S, int32_t n_prompt,
+                           int32_t level, int32_t top, const double* alphas, uint64_t seed);
+
+/* Pipeline modes. */
+enum { PS_MODE_AR = 0, PS_MODE_SYNC_SD = 1, PS_MODE_PIPESPEC = 2 };
+
+typedef struct ps_run_opts {
+  int32_t mode;
+  int32_t max_new_tokens;
+  int32_t eos_id;                 /* -1 = none */
+  const int32_t* gamma;           /* host [k]: window cap per stage (stage 0 unused) */
+  const int32_t* lookahead;       /* host [k]: 0 = verify whenever >= 1 draft */
+  int32_t max_lead;               /* draft ring depth per stage pair (>= max gamma + 1) */
+} ps_run_opts;
+
+typedef struct ps_run_stats {
+  int64_t tokens;                 /* generated tokens (== *out_len)            */
+  int64_t wall_ns;                /* from first decode step to the last token  */
+  int64_t steps[8], verify_steps[8], rollbacks[8], busy_ns[8];
+  int64_t accept_hist[64];        /* tokens appended per stage-K verify step   */
+} ps_run_stats;
+
+/* Alg.1 end to end: prefill every stage with the prompt, then run the k
+ * stages (k <= 8) in the given mode until max_new_tokens (or eos) are in O_K.
+ * out: host int32[max_new_tokens] receiving the generated tokens (prompt
+ * excluded); *out_len their count.  PS_MODE_PIPESPEC runs one host thread per
+ * stage with non-blocking draft rings and rollback mailboxes. */
+ps_status ps_pipeline_run(ps_stage* const* stages, int32_t k, const int32_t* prompt,
+                          int32_t n_prompt, const ps_run_opts* opts, int32_t* out,
+                          int32_t* out_len, ps_run_stats* stats);
+
+/* Device-side timing hook for benchmarks: number of kernels this library has
+ * launched (graph launches count their kernels) since process start. */
+int64_t ps_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPESPEC_H_ */

@@ -1,0 +1,22 @@
+/*
+ * pipespec_test.h — test hooks of the pipespec library (not part of the
+ * user-facing ABI; used by tests/ to check single kernels in isolation).
+ */
+#ifndef PIPESPEC_TEST_H_
+#define PIPESPEC_TEST_H_
+#include <stdint.h>
+#include "pipespec.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* out[r][n] = sum_k X[r][k] * W[n][k] for r < R, n < N (fp32), through the
+ * production tcgen05 stream-K GEMM with a plain-store epilogue.
+ * W: device bf16 [N, K]; X: device bf16 [32, K] (rows >= R ignored);
+ * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
+ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,110 @@
+"""ctypes mirror of include/pipespec.h (argument marshalling only).
+
+Loading never falls back to anything: if libpipespec.so is missing the import
+raises, and on a machine without an sm_100a GPU every compute call returns
+PS_E_CUDA, surfaced as PipeSpecError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libpipespec.so")
+
+PS_OK, PS_E_INVALID, PS_E_CONTRACT, PS_E_CAPACITY, PS_E_CUDA, PS_E_NCCL, PS_E_STALE = 0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "PS_OK", -1: "PS_E_INVALID", -2: "PS_E_CONTRACT", -3: "PS_E_CAPACITY", -4: "PS_E_CUDA",
+                -5: "PS_E_NCCL", -6: "PS_E_STALE"}
+PS_WQ, PS_WK, PS_WV, PS_WO, PS_WG, PS_WU, PS_WD, PS_N_ATTN, PS_N_MLP, PS_LAYER_SLOTS = range(10)
+PS_MODE_AR, PS_MODE_SYNC_SD, PS_MODE_PIPESPEC = 0, 1, 2
+
+
+class PipeSpecError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ModelShape(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("d_ffn", C.c_int32),
+                ("rms_eps", C.c_float), ("rope_theta", C.c_float), ("rope_kind", C.c_int32),
+                ("rope_factor", C.c_float), ("lo_ff", C.c_float), ("hi_ff", C.c_float),
+                ("rope_orig_max", C.c_int32), ("tied_lm_head", C.c_int32)]
+
+
+class Weights(C.Structure):
+    _fields_ = [("embed", C.c_void_p), ("lm_head", C.c_void_p), ("final_norm", C.c_void_p),
+                ("layers", C.POINTER(C.c_void_p))]
+
+
+class Placement(C.Structure):
+    _fields_ = [("device", C.c_int32), ("nccl_comm", C.c_void_p), ("tp_rank", C.c_int32), ("tp_size", C.c_int32)]
+
+
+class StageOpts(C.Structure):
+    _fields_ = [("max_seq", C.c_int32), ("max_window", C.c_int32), ("page_size", C.c_int32),
+                ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_int64), ("stream", C.c_void_p),
+                ("use_graphs", C.c_int32)]
+
+
+class StageInfo(C.Structure):
+    _fields_ = [("n_tokens", C.c_int64), ("kv_len", C.c_int64), ("pages_in_use", C.c_int64),
+                ("pages_total", C.c_int64), ("launches_per_verify", C.c_int64), ("rows_buckets", C.c_int32 * 4)]
+
+
+class RunOpts(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("max_new_tokens", C.c_int32), ("eos_id", C.c_int32),
+                ("gamma", C.POINTER(C.c_int32)), ("lookahead", C.POINTER(C.c_int32)), ("max_lead", C.c_int32)]
+
+
+class RunStats(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("wall_ns", C.c_int64), ("steps", C.c_int64 * 8),
+                ("verify_steps", C.c_int64 * 8), ("rollbacks", C.c_int64 * 8), ("busy_ns", C.c_int64 * 8),
+                ("accept_hist", C.c_int64 * 64)]
+
+
+_I32P = C.POINTER(C.c_int32)
+_PROTOS = {
+    "ps_last_error": (C.c_char_p, []),
+    "ps_version": (C.c_int32, []),
+    "ps_kernel_launch_count": (C.c_int64, []),
+    "ps_kv_pool_bytes": (C.c_int64, [C.POINTER(ModelShape), C.c_int32, C.c_int32]),
+    "ps_stage_create": (C.c_int32, [C.POINTER(ModelShape), C.POINTER(Weights), C.POINTER(Placement),
+                                    C.POINTER(StageOpts), C.POINTER(C.c_void_p)]),
+    "ps_stage_destroy": (C.c_int32, [C.c_void_p]),
+    "ps_prefill": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "ps_draft": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "ps_verify": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, _I32P, _I32P, C.c_void_p]),
+    "ps_kv_rollback": (C.c_int32, [C.c_void_p, C.c_int64]),
+    "ps_stage_tokens": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "ps_stage_get_info": (C.c_int32, [C.c_void_p, C.POINTER(StageInfo)]),
+    "ps_set_synthetic": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_double), C.c_uint64]),
+    "ps_pipeline_run": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.POINTER(RunOpts),
+                                    C.c_void_p, _I32P, C.POINTER(RunStats)]),
+    "ps_test_gemm": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                 C.c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libpipespec.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2505_01572_b200._build`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _PROTOS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != PS_OK:
+        raise PipeSpecError(status, lib().ps_last_error().decode(errors="replace"))

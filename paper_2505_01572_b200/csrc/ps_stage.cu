@@ -1,0 +1,853 @@
+// ps_stage.cu — host side of the verify hot path: stage state (token buffer O_i,
+// paged-KV page table and free list), TMA descriptors over the borrowed
+// weights, the per-forward kernel sequence (PDL-chained, captured into one CUDA
+// graph per rows bucket) and the C ABI of include/pipespec.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pipespec.h"
+#include "../../include/pipespec_test.h"
+#include "ps_kernels.cuh"
+
+using namespace ps;
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+static ps_status fail(ps_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU_TRY(expr)                                                                       \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(PS_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+// ============================================================================ TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static ps_status get_encoder() {
+  if (g_encode) return PS_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled not found");
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return PS_OK;
+}
+
+// Row-major bf16 [rows, cols] matrix; box = box_rows x 64 columns, SWIZZLE_128B
+// (128-byte rows, the canonical K-major UMMA layout).
+static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  if (((uintptr_t)ptr & 15) || (cols * 2) % 16) return fail(PS_E_INVALID, "tensor not 16-byte aligned");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PS_OK;
+}
+
+// ============================================================================ GEMM launch
+constexpr int kStages = 8;
+static int g_num_sms = 0;
+
+template <int RP, bool GU>
+static ps_status gemm_setup_attr() {
+  static bool done = false;
+  if (done) return PS_OK;
+  CU_TRY(cudaFuncSetAttribute(gemm_kernel<RP, kStages, GU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmSmem<RP, kStages, GU>::kBytes));
+  done = true;
+  return PS_OK;
+}
+
+struct GemmShape {
+  int n_tiles, kb_total, grid, maxseg;
+};
+
+static GemmShape gemm_shape(int n_tiles, int K, int num_sms) {
+  GemmShape g;
+  g.n_tiles = n_tiles;
+  g.kb_total = K / 64;
+  long long U = (long long)n_tiles * g.kb_total;
+  g.grid = (int)std::min<long long>(num_sms, U);
+  auto owner = [&](long long u) { return (int)(((u + 1) * g.grid - 1) / U); };
+  g.maxseg = 1;
+  for (int t = 0; t < n_tiles; ++t) {
+    int ns = owner((long long)t * g.kb_total + g.kb_total - 1) - owner((long long)t * g.kb_total) + 1;
+    g.maxseg = std::max(g.maxseg, ns);
+  }
+  return g;
+}
+
+static ps_status launch_gemm(int RP, bool GU, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& a2,
+                             const CUtensorMap& x, const GemmParams& p, int grid, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (RP == 16 && !GU) {
+    cfg.dynamicSmemBytes = GemmSmem<16, kStages, false>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, false>, a0, a1, a2, x, p);
+  } else if (RP == 16) {
+    cfg.dynamicSmemBytes = GemmSmem<16, kStages, true>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, true>, a0, a1, a2, x, p);
+  } else if (!GU) {
+    cfg.dynamicSmemBytes = GemmSmem<32, kStages, false>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, false>, a0, a1, a2, x, p);
+  } else {
+    cfg.dynamicSmemBytes = GemmSmem<32, kStages, true>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, true>, a0, a1, a2, x, p);
+  }
+  if (e != cudaSuccess) return fail(PS_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+  g_launches++;
+  return PS_OK;
+}
+
+template <typename K, typename P>
+static ps_status launch_simple(K kernel, dim3 grid, dim3 block, size_t smem, const P& params, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, params);
+  if (e != cudaSuccess) return fail(PS_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  g_launches++;
+  return PS_OK;
+}
+
+static ps_status init_device_globals(int device) {
+  CU_TRY(cudaSetDevice(device));
+  int major = 0, minor = 0;
+  CU_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  CU_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (major != 10 || minor != 0)
+    return fail(PS_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", device, major, minor);
+  CU_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device));
+  ps_status st;
+  if ((st = get_encoder()) != PS_OK) return st;
+  if ((st = gemm_setup_attr<16, false>()) != PS_OK) return st;
+  if ((st = gemm_setup_attr<16, true>()) != PS_OK) return st;
+  if ((st = gemm_setup_attr<32, false>()) != PS_OK) return st;
+  if ((st = gemm_setup_attr<32, true>()) != PS_OK) return st;
+  CU_TRY(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+  return PS_OK;
+}
+
+// ============================================================================ stage
+struct LayerMaps {
+  CUtensorMap q, k, v, o, g, u, d;
+};
+
+struct ps_stage {
+  ps_model_shape sh{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int max_seq = 0, max_window = 0, page_size = 0;
+  bool use_graphs = true;
+  // weights (borrowed)
+  const __nv_bfloat16* embed = nullptr;
+  const __nv_bfloat16* lm_head = nullptr;
+  const __nv_bfloat16* final_norm = nullptr;
+  std::vector<const __nv_bfloat16*> lw;   // [L][9]
+  std::vector<LayerMaps> maps;
+  CUtensorMap map_lm;
+  CUtensorMap map_xg[2], map_att[2], map_h[2];   // per rows bucket (16, 32)
+  // KV pool (borrowed) + paging
+  __nv_bfloat16* kv = nullptr;
+  long long page_elems = 0;
+  int pages_total = 0;
+  std::vector<int> page_of;     // logical page -> physical (-1 unmapped)
+  std::vector<int> free_pages;  // stack
+  int32_t* d_page_table = nullptr;
+  int32_t* h_page_table = nullptr;   // pinned mirror
+  // scratch (owned)
+  StepIn* d_in = nullptr;
+  StepIn* h_in = nullptr;            // pinned staging
+  StepOut* d_out = nullptr;
+  StepOut* h_out = nullptr;          // mapped pinned mirror
+  StepOut* h_out_dev = nullptr;      // its device alias
+  float *x = nullptr, *q = nullptr, *ss = nullptr, *logits = nullptr, *ws = nullptr;
+  __nv_bfloat16 *xg = nullptr, *att = nullptr, *h = nullptr;
+  unsigned long long* amax = nullptr;
+  unsigned *counters = nullptr, *attn_counters = nullptr;
+  float *attn_o = nullptr, *attn_ml = nullptr;
+  float2* rope_cs = nullptr;
+  SynthParams* d_syn = nullptr;
+  SynthParams h_syn{};
+  int32_t* d_S = nullptr;
+  int n_prompt = 0;
+  int ss_ld = 0, xg_ld = 0, max_chunks = 0, attn_grid = 0;
+  GemmShape gs_qkv, gs_o, gs_gu, gs_d, gs_lm;
+  int lm_tiles = 0;
+  // graphs per (bucket, with_head)
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int kernels_per_fwd[2] = {0, 0};
+  // token buffer O_i
+  std::vector<int32_t> tokens;
+  long long kv_len = 0;
+  int onpath = 0;                    // generated tokens matching the synthetic target S
+  std::vector<int32_t> S_host;
+};
+
+static int bucket_rp(int b) { return b == 0 ? 16 : 32; }
+static int bucket_of(int R) { return R <= 16 ? 0 : 1; }
+
+extern "C" int64_t ps_kv_pool_bytes(const ps_model_shape* s, int32_t max_seq, int32_t page_size) {
+  if (!s || page_size <= 0) return -1;
+  long long pages = (max_seq + page_size - 1) / page_size;
+  long long page_elems = (long long)s->n_layers * 2 * s->n_kv_heads * page_size * s->head_dim;
+  return pages * page_elems * 2;
+}
+
+static void rope_table(const ps_model_shape& s, int max_seq, std::vector<float2>& out) {
+  const int hd = s.head_dim, half = hd / 2;
+  std::vector<double> inv(half);
+  for (int i = 0; i < half; ++i) inv[i] = 1.0 / std::pow((double)s.rope_theta, (2.0 * i) / hd);
+  if (s.rope_kind == 1) {   // llama3 frequency scaling (HF convention, reading R19)
+    const double factor = s.rope_factor, lo = s.lo_ff, hi = s.hi_ff, old = s.rope_orig_max;
+    const double low_wl = old / lo, high_wl = old / hi;
+    for (int i = 0; i < half; ++i) {
+      const double wl = 2.0 * M_PI / inv[i];
+      double f = wl > low_wl ? inv[i] / factor : inv[i];
+      if (wl >= high_wl && wl <= low_wl) {
+        const double sm = (old / wl - lo) / (hi - lo);
+        f = (1.0 - sm) * f / factor + sm * f;
+      }
+      inv[i] = f;
+    }
+  }
+  out.resize((size_t)max_seq * half);
+  for (int p = 0; p < max_seq; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double a = (double)p * inv[i];
+      out[(size_t)p * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+}
+
+// ---------------------------------------------------------------- forward
+// Enqueue one forward over StepIn rows (already uploaded): embed, L x {QKV,
+// attention, O, gate/up, down}, then (with_head) lm_head + argmax/scan.
+static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
+  const ps_model_shape& sh = S->sh;
+  const int RP = bucket_rp(b);
+  const int d = sh.d_model, hq = sh.n_heads * sh.head_dim, hkv = sh.n_kv_heads * sh.head_dim;
+  ps_status st;
+  int nk = 0;
+  {
+    EmbedParams e{S->d_in, S->embed, d, S->lw[0 * 9 + PS_N_ATTN], S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
+    if (sh.n_layers == 0) e.gain = S->final_norm;
+    if ((st = launch_simple(embed_kernel, dim3(RP), dim3(128), 0, e, S->stream)) != PS_OK) return st;
+    ++nk;
+  }
+  const float inv_d = 1.0f / d;
+  const int ss_n = (d + 127) / 128;
+  for (int l = 0; l < sh.n_layers; ++l) {
+    const __nv_bfloat16* const* W = &S->lw[(size_t)l * 9];
+    const LayerMaps& M = S->maps[l];
+    GemmParams p = {};
+    p.step = S->d_in;
+    p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
+    p.ws = S->ws; p.counters = S->counters;
+    // --- QKV + RoPE + paged KV append
+    p.mode = EPI_QKV;
+    p.N = hq + 2 * hkv;
+    p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg;
+    p.t1 = (hq + 127) / 128; p.t2 = p.t1 + (hkv + 127) / 128;
+    p.nq = hq; p.nk = hkv;
+    p.q = S->q; p.ld_q = hq;
+    p.kv = S->kv; p.page_table = S->d_page_table; p.page_size = S->page_size; p.layer = l;
+    p.hkv = sh.n_kv_heads; p.hd = sh.head_dim; p.page_stride = S->page_elems; p.rope_cs = S->rope_cs;
+    if ((st = launch_gemm(RP, false, M.q, M.k, M.v, S->map_xg[b], p, S->gs_qkv.grid, S->stream)) != PS_OK) return st;
+    ++nk;
+    // --- attention
+    AttnParams a{};
+    a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
+    a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
+    a.H = sh.n_heads; a.hd = sh.head_dim; a.scale = 1.0f / std::sqrt((float)sh.head_dim);
+    a.max_chunks = S->max_chunks; a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
+    a.out = S->att; a.ld_out = hq;
+    if ((st = launch_simple(attn_kernel, dim3(S->attn_grid), dim3(128), kAttnSmem, a, S->stream)) != PS_OK) return st;
+    ++nk;
+    // --- O projection + residual; writes x∘g_mlp and sumsq
+    GemmParams o = {};
+    o.step = S->d_in; o.mode = EPI_RESID; o.N = d;
+    o.n_tiles = S->gs_o.n_tiles; o.kb_total = S->gs_o.kb_total; o.maxseg = S->gs_o.maxseg;
+    o.x = S->x; o.ld_x = d; o.xg = S->xg; o.ld_xg = S->xg_ld; o.gain = W[PS_N_MLP];
+    o.ss_out = S->ss; o.ss_out_ld = S->ss_ld; o.ws = S->ws; o.counters = S->counters;
+    if ((st = launch_gemm(RP, false, M.o, M.o, M.o, S->map_att[b], o, S->gs_o.grid, S->stream)) != PS_OK) return st;
+    ++nk;
+    // --- gate/up + SiLU*mul
+    GemmParams g = {};
+    g.step = S->d_in; g.mode = EPI_SWIGLU; g.N = sh.d_ffn;
+    g.n_tiles = S->gs_gu.n_tiles; g.kb_total = S->gs_gu.kb_total; g.maxseg = S->gs_gu.maxseg;
+    g.ss_in = S->ss; g.ss_n = ss_n; g.ss_ld = S->ss_ld; g.inv_d = inv_d; g.eps = sh.rms_eps;
+    g.h = S->h; g.ld_h = sh.d_ffn; g.ws = S->ws; g.counters = S->counters;
+    if ((st = launch_gemm(RP, true, M.g, M.u, M.u, S->map_xg[b], g, S->gs_gu.grid, S->stream)) != PS_OK) return st;
+    ++nk;
+    // --- down + residual; writes x∘g_next and sumsq
+    GemmParams dn = {};
+    dn.step = S->d_in; dn.mode = EPI_RESID; dn.N = d;
+    dn.n_tiles = S->gs_d.n_tiles; dn.kb_total = S->gs_d.kb_total; dn.maxseg = S->gs_d.maxseg;
+    dn.x = S->x; dn.ld_x = d; dn.xg = S->xg; dn.ld_xg = S->xg_ld;
+    dn.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
+    dn.ss_out = S->ss; dn.ss_out_ld = S->ss_ld; dn.ws = S->ws; dn.counters = S->counters;
+    if ((st = launch_gemm(RP, false, M.d, M.d, M.d, S->map_h[b], dn, S->gs_d.grid, S->stream)) != PS_OK) return st;
+    ++nk;
+  }
+  if (with_head) {
+    GemmParams p = {};
+    p.step = S->d_in; p.mode = EPI_LMHEAD; p.N = sh.vocab;
+    p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
+    p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
+    p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
+    p.ws = S->ws; p.counters = S->counters;
+    if ((st = launch_gemm(RP, false, S->map_lm, S->map_lm, S->map_lm, S->map_xg[b], p, S->gs_lm.grid, S->stream)) !=
+        PS_OK)
+      return st;
+    ++nk;
+    ArgmaxParams ap{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
+    if ((st = launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, ap, S->stream)) != PS_OK) return st;
+    ++nk;
+  }
+  S->kernels_per_fwd[with_head ? 1 : 0] = nk;
+  return PS_OK;
+}
+
+static ps_status run_forward(ps_stage* S, int R, bool with_head) {
+  const int b = bucket_of(R);
+  CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
+  if (!S->use_graphs) return enqueue_forward(S, b, with_head);
+  cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
+  if (!ge) {
+    cudaGraph_t g;
+    CU_TRY(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
+    long long before = g_launches.load();
+    ps_status st = enqueue_forward(S, b, with_head);
+    cudaError_t e = cudaStreamEndCapture(S->stream, &g);
+    g_launches.store(before);
+    if (st != PS_OK) return st;
+    if (e != cudaSuccess) return fail(PS_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    CU_TRY(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+  }
+  CU_TRY(cudaGraphLaunch(ge, S->stream));
+  g_launches += S->kernels_per_fwd[with_head ? 1 : 0];
+  return PS_OK;
+}
+
+// ---------------------------------------------------------------- paging
+static ps_status ensure_pages(ps_stage* S, long long last_pos) {
+  const int need = (int)(last_pos / S->page_size) + 1;
+  if (need > (int)S->page_of.size()) return fail(PS_E_CAPACITY, "position %lld beyond max_seq", last_pos);
+  int lo = -1, hi = -1;
+  for (int lp = 0; lp < need; ++lp) {
+    if (S->page_of[lp] >= 0) continue;
+    if (S->free_pages.empty()) return fail(PS_E_CAPACITY, "KV pool exhausted");
+    S->page_of[lp] = S->free_pages.back();
+    S->free_pages.pop_back();
+    S->h_page_table[lp] = S->page_of[lp];
+    if (lo < 0) lo = lp;
+    hi = lp;
+  }
+  if (lo >= 0)
+    CU_TRY(cudaMemcpyAsync(S->d_page_table + lo, S->h_page_table + lo, (size_t)(hi - lo + 1) * 4,
+                           cudaMemcpyHostToDevice, S->stream));
+  return PS_OK;
+}
+
+static void free_pages_from(ps_stage* S, long long kv_len) {
+  // free pages lying wholly at or beyond kv_len (O(#freed))
+  const long long first = (kv_len + S->page_size - 1) / S->page_size;
+  for (long long lp = (long long)S->page_of.size() - 1; lp >= first; --lp) {
+    if (S->page_of[lp] < 0) continue;
+    S->free_pages.push_back(S->page_of[lp]);
+    S->page_of[lp] = -1;
+    S->h_page_table[lp] = 0;
+  }
+}
+
+static long long pages_in_use(const ps_stage* S) {
+  return (long long)S->pages_total - (long long)S->free_pages.size();
+}
+
+static void update_onpath(ps_stage* S) {
+  if (S->S_host.empty()) return;
+  const long long gen = (long long)S->tokens.size() - S->n_prompt;
+  if (S->onpath > gen) S->onpath = (int)std::max(0LL, gen);
+  while (S->onpath < gen && S->onpath < (int)S->S_host.size() &&
+         S->tokens[S->n_prompt + S->onpath] == S->S_host[S->onpath])
+    ++S->onpath;
+}
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char* ps_last_error(void) { return g_err.c_str(); }
+int32_t ps_version(void) { return 100; }
+int64_t ps_kernel_launch_count(void) { return g_launches.load(); }
+
+static ps_status validate_shape(const ps_model_shape* s) {
+  if (!s) return fail(PS_E_INVALID, "shape is NULL");
+  if (s->vocab < 2 || s->d_model <= 0 || s->n_layers < 0 || s->n_heads <= 0 || s->n_kv_heads <= 0)
+    return fail(PS_E_INVALID, "bad shape sizes");
+  if (s->n_heads % s->n_kv_heads) return fail(PS_E_INVALID, "n_heads %% n_kv_heads != 0");
+  if (s->head_dim != 64 && s->head_dim != 128) return fail(PS_E_INVALID, "head_dim must be 64 or 128");
+  if (s->d_model % 64 || s->d_ffn % 64 || (s->n_heads * s->head_dim) % 64)
+    return fail(PS_E_INVALID, "d_model, d_ffn and n_heads*head_dim must be multiples of 64");
+  if (s->d_ffn <= 0) return fail(PS_E_INVALID, "d_ffn must be positive");
+  return PS_OK;
+}
+
+ps_status ps_stage_destroy(ps_stage* S) {
+  if (!S) return PS_OK;
+  cudaSetDevice(S->device);
+  if (S->stream) cudaStreamSynchronize(S->stream);
+  for (auto& gb : S->graph)
+    for (auto& g : gb)
+      if (g) cudaGraphExecDestroy(g);
+  void* dev[] = {S->d_page_table, S->d_in, S->d_out, S->x, S->q, S->ss, S->logits, S->ws, S->xg, S->att, S->h,
+                 S->amax, S->counters, S->attn_counters, S->attn_o, S->attn_ml, S->rope_cs, S->d_syn, S->d_S};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (S->h_page_table) cudaFreeHost(S->h_page_table);
+  if (S->h_in) cudaFreeHost(S->h_in);
+  if (S->h_out) cudaFreeHost(S->h_out);
+  if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
+  delete S;
+  return PS_OK;
+}
+
+ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, const ps_placement* pl,
+                          const ps_stage_opts* o, ps_stage** out) {
+  ps_status st;
+  if (!out || !w || !pl || !o) return fail(PS_E_INVALID, "NULL argument");
+  if ((st = validate_shape(shape)) != PS_OK) return st;
+  if (pl->tp_size > 1) return fail(PS_E_INVALID, "tensor parallelism is not built in this version");
+  if (o->max_seq < 2) return fail(PS_E_INVALID, "max_seq must be >= 2");
+  if (o->max_window < 0 || o->max_window > kMaxRows - 1) return fail(PS_E_INVALID, "max_window must be 0..31");
+  if (o->page_size != 64 && o->page_size != 128 && o->page_size != 256)
+    return fail(PS_E_INVALID, "page_size must be 64, 128 or 256");
+  if (!w->embed || !w->lm_head || !w->final_norm || (shape->n_layers > 0 && !w->layers))
+    return fail(PS_E_INVALID, "NULL weight pointer");
+  const int64_t need = ps_kv_pool_bytes(shape, o->max_seq, o->page_size);
+  if (!o->kv_pool || o->kv_pool_bytes < need)
+    return fail(PS_E_INVALID, "kv_pool too small (%lld < %lld bytes)", (long long)o->kv_pool_bytes, (long long)need);
+  if ((st = init_device_globals(pl->device)) != PS_OK) return st;
+
+  ps_stage* S = new (std::nothrow) ps_stage();
+  if (!S) return fail(PS_E_INVALID, "out of host memory");
+  auto bail = [&](ps_status s2) {
+    std::string keep = g_err;
+    ps_stage_destroy(S);
+    g_err = keep;
+    return s2;
+  };
+#define S_TRY(expr)                                                                             \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return bail(fail(PS_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)));                   \
+  } while (0)
+#define P_TRY(expr)                                                                             \
+  do {                                                                                          \
+    ps_status s_ = (expr);                                                                      \
+    if (s_ != PS_OK) return bail(s_);                                                           \
+  } while (0)
+
+  const ps_model_shape& sh = *shape;
+  S->sh = sh;
+  S->device = pl->device;
+  S->max_seq = o->max_seq;
+  S->max_window = o->max_window;
+  S->page_size = o->page_size;
+  S->use_graphs = o->use_graphs != 0;
+  if (o->stream) {
+    S->stream = (cudaStream_t)o->stream;
+  } else {
+    S_TRY(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+    S->own_stream = true;
+  }
+  S->embed = (const __nv_bfloat16*)w->embed;
+  S->lm_head = (const __nv_bfloat16*)w->lm_head;
+  S->final_norm = (const __nv_bfloat16*)w->final_norm;
+  S->lw.assign((size_t)std::max(sh.n_layers, 1) * 9, nullptr);
+  for (int i = 0; i < sh.n_layers * 9; ++i) {
+    S->lw[i] = (const __nv_bfloat16*)w->layers[i];
+    if (!S->lw[i]) return bail(fail(PS_E_INVALID, "NULL layer weight %d", i));
+  }
+  const int d = sh.d_model, hq = sh.n_heads * sh.head_dim, hkv = sh.n_kv_heads * sh.head_dim, f = sh.d_ffn;
+  // --- TMA maps over the borrowed weights
+  S->maps.resize(sh.n_layers);
+  for (int l = 0; l < sh.n_layers; ++l) {
+    const __nv_bfloat16* const* W = &S->lw[(size_t)l * 9];
+    LayerMaps& M = S->maps[l];
+    P_TRY(make_map(&M.q, W[PS_WQ], hq, d, 128));
+    P_TRY(make_map(&M.k, W[PS_WK], hkv, d, 128));
+    P_TRY(make_map(&M.v, W[PS_WV], hkv, d, 128));
+    P_TRY(make_map(&M.o, W[PS_WO], d, hq, 128));
+    P_TRY(make_map(&M.g, W[PS_WG], f, d, 64));
+    P_TRY(make_map(&M.u, W[PS_WU], f, d, 64));
+    P_TRY(make_map(&M.d, W[PS_WD], d, f, 128));
+  }
+  P_TRY(make_map(&S->map_lm, S->lm_head, sh.vocab, d, 128));
+  // --- scratch
+  S->xg_ld = d;
+  S->ss_ld = (d + 127) / 128;
+  S_TRY(cudaMalloc(&S->d_in, sizeof(StepIn)));
+  S_TRY(cudaMalloc(&S->d_out, sizeof(StepOut)));
+  S_TRY(cudaHostAlloc(&S->h_in, sizeof(StepIn), cudaHostAllocDefault));
+  S_TRY(cudaHostAlloc(&S->h_out, sizeof(StepOut), cudaHostAllocMapped));
+  S_TRY(cudaHostGetDevicePointer((void**)&S->h_out_dev, S->h_out, 0));
+  memset(S->h_in, 0, sizeof(StepIn));
+  S_TRY(cudaMalloc(&S->x, (size_t)kMaxRows * d * 4));
+  S_TRY(cudaMalloc(&S->xg, (size_t)kMaxRows * d * 2));
+  S_TRY(cudaMalloc(&S->att, (size_t)kMaxRows * hq * 2));
+  S_TRY(cudaMalloc(&S->h, (size_t)kMaxRows * f * 2));
+  S_TRY(cudaMalloc(&S->q, (size_t)kMaxRows * hq * 4));
+  S_TRY(cudaMalloc(&S->ss, (size_t)kMaxRows * S->ss_ld * 4));
+  S_TRY(cudaMalloc(&S->logits, (size_t)kMaxRows * sh.vocab * 4));
+  S_TRY(cudaMemset(S->x, 0, (size_t)kMaxRows * d * 4));
+  S_TRY(cudaMemset(S->xg, 0, (size_t)kMaxRows * d * 2));
+  S_TRY(cudaMemset(S->att, 0, (size_t)kMaxRows * hq * 2));
+  S_TRY(cudaMemset(S->h, 0, (size_t)kMaxRows * f * 2));
+  S_TRY(cudaMemset(S->q, 0, (size_t)kMaxRows * hq * 4));
+  S_TRY(cudaMemset(S->ss, 0, (size_t)kMaxRows * S->ss_ld * 4));
+  for (int b = 0; b < 2; ++b) {
+    P_TRY(make_map(&S->map_xg[b], S->xg, kMaxRows, d, bucket_rp(b)));
+    P_TRY(make_map(&S->map_att[b], S->att, kMaxRows, hq, bucket_rp(b)));
+    P_TRY(make_map(&S->map_h[b], S->h, kMaxRows, f, bucket_rp(b)));
+  }
+  // --- GEMM partitions (persistent grid = #SMs, stream-K)
+  const int n = g_num_sms;
+  S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n);
+  S->gs_o = gemm_shape((d + 127) / 128, hq, n);
+  S->gs_gu = gemm_shape((f + 63) / 64, d, n);
+  S->gs_d = gemm_shape((d + 127) / 128, f, n);
+  S->gs_lm = gemm_shape((sh.vocab + 127) / 128, d, n);
+  S->lm_tiles = S->gs_lm.n_tiles;
+  size_t ws_elems = 0;
+  int max_tiles = 0;
+  for (const GemmShape* g : {&S->gs_qkv, &S->gs_o, &S->gs_gu, &S->gs_d, &S->gs_lm}) {
+    ws_elems = std::max(ws_elems, (size_t)g->n_tiles * g->maxseg * kMaxRows * 128);
+    max_tiles = std::max(max_tiles, g->n_tiles);
+  }
+  S_TRY(cudaMalloc(&S->ws, ws_elems * 4));
+  S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * 4));
+  S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
+  S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * S->lm_tiles * 8));
+  // --- attention workspace
+  S->max_chunks = (S->max_seq + kAttnChunk - 1) / kAttnChunk;
+  S->attn_grid = std::min(sh.n_heads * S->max_chunks, 2 * n);
+  S_TRY(cudaMalloc(&S->attn_o, (size_t)sh.n_heads * S->max_chunks * kMaxRows * sh.head_dim * 4));
+  S_TRY(cudaMalloc(&S->attn_ml, (size_t)sh.n_heads * S->max_chunks * kMaxRows * 2 * 4));
+  S_TRY(cudaMalloc(&S->attn_counters, (size_t)sh.n_heads * 4));
+  S_TRY(cudaMemset(S->attn_counters, 0, (size_t)sh.n_heads * 4));
+  // --- RoPE table
+  {
+    std::vector<float2> cs;
+    rope_table(sh, S->max_seq + kMaxRows, cs);
+    S_TRY(cudaMalloc(&S->rope_cs, cs.size() * sizeof(float2)));
+    S_TRY(cudaMemcpy(S->rope_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+  // --- paged KV
+  S->kv = (__nv_bfloat16*)o->kv_pool;
+  S->page_elems = (long long)sh.n_layers * 2 * sh.n_kv_heads * S->page_size * sh.head_dim;
+  S->pages_total = (int)(o->kv_pool_bytes / (S->page_elems * 2));
+  const int lpages = (S->max_seq + kMaxRows + S->page_size - 1) / S->page_size;
+  S->page_of.assign(lpages, -1);
+  for (int p = S->pages_total - 1; p >= 0; --p) S->free_pages.push_back(p);
+  S_TRY(cudaMalloc(&S->d_page_table, (size_t)lpages * 4));
+  S_TRY(cudaMemset(S->d_page_table, 0, (size_t)lpages * 4));
+  S_TRY(cudaHostAlloc(&S->h_page_table, (size_t)lpages * 4, cudaHostAllocDefault));
+  memset(S->h_page_table, 0, (size_t)lpages * 4);
+  // --- synthetic override (disabled)
+  S_TRY(cudaMalloc(&S->d_syn, sizeof(SynthParams)));
+  S->h_syn = SynthParams{};
+  S_TRY(cudaMemcpy(S->d_syn, &S->h_syn, sizeof(SynthParams), cudaMemcpyHostToDevice));
+  S_TRY(cudaStreamSynchronize(S->stream));
+  *out = S;
+#undef S_TRY
+#undef P_TRY
+  return PS_OK;
+}
+
+// One forward over tokens [start, start+R) at positions [start, start+R);
+// with_head computes logits/argmax for all rows.
+static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long pos0, int w, bool with_head,
+                              bool want_logits) {
+  ps_status st;
+  if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
+  StepIn* in = S->h_in;
+  in->R = R;
+  in->pos0 = (int32_t)pos0;
+  in->w = w;
+  in->flags = (want_logits ? kFlagLogits : 0);
+  in->syn_p0 = 0;
+  in->syn_onpath = 0;
+  if (with_head && !S->S_host.empty()) {
+    in->flags |= kFlagSynth;
+    const long long gen = (long long)S->tokens.size() - S->n_prompt;
+    in->syn_p0 = (int32_t)gen;
+    in->syn_onpath = (gen >= 0 && S->onpath == gen) ? 1 : 0;
+  }
+  for (int j = 0; j < kMaxRows; ++j) in->tokens[j] = j < R ? toks[j] : 0;
+  return run_forward(S, R, with_head);
+}
+
+ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
+  if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
+  if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "prefill length %d not in [1, max_seq]", n);
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= S->sh.vocab) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
+  CU_TRY(cudaSetDevice(S->device));
+  // keep the KV of the longest common prefix
+  long long m = 0;
+  while (m < (long long)S->tokens.size() && m < n && S->tokens[m] == tokens[m]) ++m;
+  const long long keep_kv = std::min<long long>(S->kv_len, std::max<long long>(m - 1, 0));
+  S->tokens.assign(tokens, tokens + n);
+  S->kv_len = keep_kv;
+  free_pages_from(S, S->kv_len);
+  update_onpath(S);
+  // forward positions [kv_len, n-1) in chunks of kMaxRows rows (no lm_head)
+  while (S->kv_len < n - 1) {
+    const int R = (int)std::min<long long>(kMaxRows, n - 1 - S->kv_len);
+    ps_status st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
+    if (st != PS_OK) {
+      S->kv_len = 0;   // KV state unknown: force a full recompute next time
+      free_pages_from(S, 0);
+      return st;
+    }
+    S->kv_len += R;
+  }
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  return PS_OK;
+}
+
+static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t* a_out, int32_t* next_out,
+                             float* logits_out) {
+  const long long n = (long long)S->tokens.size();
+  if (n < 1) return fail(PS_E_CONTRACT, "verify on an empty token buffer (call ps_prefill first)");
+  if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d > max_window %d", w, S->max_window);
+  if (n + w > S->max_seq) return fail(PS_E_CAPACITY, "n + w = %lld exceeds max_seq", n + w);
+  if (S->kv_len != n - 1) return fail(PS_E_CONTRACT, "KV covers %lld positions, expected %lld", S->kv_len, n - 1);
+  int32_t rows[kMaxRows];
+  rows[0] = S->tokens[n - 1];
+  for (int j = 0; j < w; ++j) {
+    if (window[j] < 0 || window[j] >= S->sh.vocab) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
+    rows[1 + j] = window[j];
+  }
+  ps_status st = forward_rows(S, rows, w + 1, n - 1, w, true, logits_out != nullptr);
+  if (st != PS_OK) return st;
+  if (logits_out) {
+    cudaPointerAttributes at{};
+    cudaMemcpyKind kind = cudaMemcpyDeviceToHost;
+    if (cudaPointerGetAttributes(&at, logits_out) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+      kind = cudaMemcpyDeviceToDevice;
+    cudaGetLastError();
+    CU_TRY(cudaMemcpyAsync(logits_out, S->logits, (size_t)(w + 1) * S->sh.vocab * 4, kind, S->stream));
+  }
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  const StepOut* r = S->h_out;
+  const int a = r->a, nxt = r->next;
+  if (a < 0 || a > w || nxt < 0 || nxt >= S->sh.vocab) return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d", a, nxt);
+  for (int j = 0; j < a; ++j) S->tokens.push_back(window[j]);
+  S->tokens.push_back(nxt);
+  S->kv_len = n + a;
+  free_pages_from(S, S->kv_len);
+  update_onpath(S);
+  *a_out = a;
+  *next_out = nxt;
+  return PS_OK;
+}
+
+ps_status ps_verify(ps_stage* S, const int32_t* window, int32_t w, int32_t* accepted_len, int32_t* next_token,
+                    float* opt_logits) {
+  if (!S || !accepted_len || !next_token || (w > 0 && !window)) return fail(PS_E_INVALID, "NULL argument");
+  if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d not in [0, max_window=%d]", w, S->max_window);
+  CU_TRY(cudaSetDevice(S->device));
+  int32_t host_window[kMaxRows];
+  const int32_t* win = window;
+  if (w > 0) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, window) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+      CU_TRY(cudaMemcpyAsync(host_window, window, (size_t)w * 4, cudaMemcpyDeviceToHost, S->stream));
+      CU_TRY(cudaStreamSynchronize(S->stream));
+      win = host_window;
+    }
+    cudaGetLastError();
+  }
+  return verify_host(S, win, w, accepted_len, next_token, opt_logits);
+}
+
+ps_status ps_draft(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
+  if (!S || (n_steps > 0 && !out_tokens)) return fail(PS_E_INVALID, "NULL argument");
+  if (n_steps < 0) return fail(PS_E_INVALID, "n_steps < 0");
+  CU_TRY(cudaSetDevice(S->device));
+  for (int i = 0; i < n_steps; ++i) {
+    int32_t a, nxt;
+    ps_status st = verify_host(S, nullptr, 0, &a, &nxt, nullptr);
+    if (st != PS_OK) return st;
+    out_tokens[i] = nxt;
+  }
+  return PS_OK;
+}
+
+ps_status ps_kv_rollback(ps_stage* S, int64_t keep) {
+  if (!S) return fail(PS_E_INVALID, "NULL stage");
+  if (keep < 1 || keep > (int64_t)S->tokens.size())
+    return fail(PS_E_CONTRACT, "rollback keep=%lld not in [1, len=%zu]", (long long)keep, S->tokens.size());
+  S->tokens.resize((size_t)keep);
+  S->kv_len = std::min<long long>(S->kv_len, keep - 1);
+  free_pages_from(S, S->kv_len);
+  update_onpath(S);
+  return PS_OK;
+}
+
+ps_status ps_stage_tokens(const ps_stage* S, int32_t* out, int64_t cap, int64_t* len) {
+  if (!S || !len || (cap > 0 && !out)) return fail(PS_E_INVALID, "NULL argument");
+  const int64_t n = (int64_t)S->tokens.size();
+  const int64_t m = std::min(cap, n);
+  if (m > 0) memcpy(out, S->tokens.data(), (size_t)m * 4);
+  *len = n;
+  return PS_OK;
+}
+
+ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
+  if (!S || !info) return fail(PS_E_INVALID, "NULL argument");
+  memset(info, 0, sizeof *info);
+  info->n_tokens = (int64_t)S->tokens.size();
+  info->kv_len = S->kv_len;
+  info->pages_in_use = pages_in_use(S);
+  info->pages_total = S->pages_total;
+  info->launches_per_verify = 1 + 5LL * S->sh.n_layers + 2;
+  info->rows_buckets[0] = 16;
+  info->rows_buckets[1] = 32;
+  return PS_OK;
+}
+
+ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_t n_prompt, int32_t level,
+                           int32_t top, const double* alphas, uint64_t seed) {
+  if (!S) return fail(PS_E_INVALID, "NULL stage");
+  CU_TRY(cudaSetDevice(S->device));
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  if (S->d_S) { cudaFree(S->d_S); S->d_S = nullptr; }
+  S->S_host.clear();
+  S->h_syn = SynthParams{};
+  if (len_S > 0) {
+    if (!Sv || !alphas || level < 0 || top <= level || top > 8 || n_prompt < 0)
+      return fail(PS_E_INVALID, "bad synthetic parameters");
+    S->S_host.resize(len_S);
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, Sv) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+      CU_TRY(cudaMemcpy(S->S_host.data(), Sv, (size_t)len_S * 4, cudaMemcpyDeviceToHost));
+    else
+      memcpy(S->S_host.data(), Sv, (size_t)len_S * 4);
+    cudaGetLastError();
+    CU_TRY(cudaMalloc(&S->d_S, (size_t)len_S * 4));
+    CU_TRY(cudaMemcpy(S->d_S, S->S_host.data(), (size_t)len_S * 4, cudaMemcpyHostToDevice));
+    S->h_syn.S = S->d_S;
+    S->h_syn.len_S = len_S;
+    S->h_syn.level = level;
+    S->h_syn.top = top;
+    S->h_syn.vocab = S->sh.vocab;
+    S->h_syn.seed = seed;
+    for (int j = level; j < top; ++j) {
+      const double a = alphas[j - level];
+      if (!(a >= 0.0 && a <= 1.0)) return fail(PS_E_INVALID, "alpha out of [0,1]");
+      S->h_syn.thr[j] = (uint64_t)std::ldexp(a, 53);
+    }
+    S->n_prompt = n_prompt;
+    S->onpath = 0;
+    update_onpath(S);
+  }
+  CU_TRY(cudaMemcpy(S->d_syn, &S->h_syn, sizeof(SynthParams), cudaMemcpyHostToDevice));
+  return PS_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================ test hooks
+extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                  void* stream) {
+  ps_status st;
+  if (R < 1 || R > kMaxRows || K % 64 || N < 1) return fail(PS_E_INVALID, "bad test gemm shape");
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  if ((st = init_device_globals(dev)) != PS_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int RP = R <= 16 ? 16 : 32;
+  CUtensorMap mW, mX;
+  if ((st = make_map(&mW, W, N, K, 128)) != PS_OK) return st;
+  if ((st = make_map(&mX, X, kMaxRows, K, RP)) != PS_OK) return st;
+  GemmShape gs = gemm_shape((N + 127) / 128, K, g_num_sms);
+  StepIn hin{};
+  hin.R = R;
+  StepIn* din;
+  float* ws;
+  unsigned* cnt;
+  CU_TRY(cudaMalloc(&din, sizeof(StepIn)));
+  CU_TRY(cudaMalloc(&ws, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 4));
+  CU_TRY(cudaMalloc(&cnt, (size_t)gs.n_tiles * 4));
+  CU_TRY(cudaMemset(cnt, 0, (size_t)gs.n_tiles * 4));
+  CU_TRY(cudaMemcpy(din, &hin, sizeof hin, cudaMemcpyHostToDevice));
+  GemmParams p = {};
+  p.mode = EPI_STORE;
+  p.N = N;
+  p.n_tiles = gs.n_tiles;
+  p.kb_total = gs.kb_total;
+  p.maxseg = gs.maxseg;
+  p.step = din;
+  p.out = out;
+  p.ld_out = N;
+  p.ws = ws;
+  p.counters = cnt;
+  st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(din);
+  cudaFree(ws);
+  cudaFree(cnt);
+  if (st != PS_OK) return st;
+  if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
+
+extern "C" ps_status ps_pipeline_run(ps_stage* const* stages, int32_t k, const int32_t* prompt, int32_t n_prompt,
+                                     const ps_run_opts* opts, int32_t* out, int32_t* out_len, ps_run_stats* stats);

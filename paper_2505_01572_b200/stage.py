@@ -1,0 +1,163 @@
+"""Thin Python binding over the C ABI (same names as include/pipespec.h).
+
+PyTorch only provides device memory (weights, the KV pool) and streams; every
+step of the verify pass runs in libpipespec.so's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import abi
+
+LAYER_KEYS = ("wq", "wk", "wv", "wo", "wg", "wu", "wd", "n_attn", "n_mlp")
+
+
+def model_shape(s) -> abi.ModelShape:
+    """ps_model_shape from any object with the ModelShape attributes."""
+    return abi.ModelShape(s.vocab, s.d_model, s.n_layers, s.n_heads, s.n_kv_heads, s.head_dim, s.d_ffn,
+                          s.rms_eps, s.rope_theta, s.rope_kind, s.rope_factor, s.lo_ff, s.hi_ff,
+                          s.rope_orig_max, int(bool(s.tied)))
+
+
+def kv_pool_bytes(shape, max_seq: int, page_size: int) -> int:
+    sh = model_shape(shape)
+    return int(abi.lib().ps_kv_pool_bytes(C.byref(sh), max_seq, page_size))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+class Stage:
+    """One model M_i: ps_stage_create over borrowed bf16 CUDA weights."""
+
+    def __init__(self, shape, weights: dict, max_seq: int = 1024, max_window: int = 31,
+                 page_size: int = 64, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 use_graphs: bool = True):
+        self.shape = shape
+        self.weights = weights            # keep the borrowed tensors alive
+        self._sh = model_shape(shape)
+        dev = torch.device("cuda", device)
+        for k in ("embed", "lm_head", "final_norm"):
+            t = weights[k]
+            assert t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous(), k
+        ptrs = []
+        for lw in weights["layers"]:
+            for k in LAYER_KEYS:
+                t = lw[k]
+                assert t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous(), k
+                ptrs.append(t.data_ptr())
+        self._layer_ptrs = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+        self._w = abi.Weights(weights["embed"].data_ptr(), weights["lm_head"].data_ptr(),
+                              weights["final_norm"].data_ptr(),
+                              C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
+        nbytes = kv_pool_bytes(shape, max_seq, page_size)
+        self.kv_pool = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
+        self._pl = abi.Placement(device, None, 0, 1)
+        self._opts = abi.StageOpts(max_seq, max_window, page_size, self.kv_pool.data_ptr(), nbytes,
+                                   self.stream.cuda_stream, int(use_graphs))
+        h = C.c_void_p()
+        abi.check(abi.lib().ps_stage_create(C.byref(self._sh), C.byref(self._w), C.byref(self._pl),
+                                            C.byref(self._opts), C.byref(h)))
+        self._h = h
+        self.max_window = max_window
+        self.max_seq = max_seq
+
+    # ---------------------------------------------------------------- calls
+    def close(self):
+        if getattr(self, "_h", None):
+            abi.lib().ps_stage_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def prefill(self, tokens):
+        t = _i32(tokens)
+        abi.check(abi.lib().ps_prefill(self._h, t.ctypes.data, len(t)))
+
+    def draft(self, n_steps: int) -> list[int]:
+        out = np.zeros(max(1, n_steps), dtype=np.int32)
+        abi.check(abi.lib().ps_draft(self._h, n_steps, out.ctypes.data))
+        return out[:n_steps].tolist()
+
+    def verify(self, window, want_logits: bool = False):
+        """Returns (accepted_len, next_token[, logits float32 [w+1, V] numpy])."""
+        if isinstance(window, torch.Tensor) and window.is_cuda:
+            win = window.to(torch.int32).contiguous()
+            ptr, w = win.data_ptr(), win.numel()
+        else:
+            win = _i32(window)
+            ptr, w = win.ctypes.data, len(win)
+        a, nxt = C.c_int32(), C.c_int32()
+        logits = None
+        lptr = None
+        if want_logits:
+            logits = np.zeros((w + 1, self.shape.vocab), dtype=np.float32)
+            lptr = logits.ctypes.data
+        abi.check(abi.lib().ps_verify(self._h, ptr if w else None, w, C.byref(a), C.byref(nxt), lptr))
+        if want_logits:
+            return a.value, nxt.value, logits
+        return a.value, nxt.value
+
+    def kv_rollback(self, keep_len: int):
+        abi.check(abi.lib().ps_kv_rollback(self._h, keep_len))
+
+    def tokens(self) -> list[int]:
+        n = C.c_int64()
+        abi.check(abi.lib().ps_stage_tokens(self._h, None, 0, C.byref(n)))
+        out = np.zeros(max(1, n.value), dtype=np.int32)
+        abi.check(abi.lib().ps_stage_tokens(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out[:n.value].tolist()
+
+    def info(self) -> dict:
+        i = abi.StageInfo()
+        abi.check(abi.lib().ps_stage_get_info(self._h, C.byref(i)))
+        return dict(n_tokens=i.n_tokens, kv_len=i.kv_len, pages_in_use=i.pages_in_use,
+                    pages_total=i.pages_total, launches_per_verify=i.launches_per_verify)
+
+    def set_synthetic(self, S, n_prompt: int, level: int, top: int, alphas, seed: int):
+        s = _i32(S)
+        al = (C.c_double * max(1, len(alphas)))(*alphas)
+        abi.check(abi.lib().ps_set_synthetic(self._h, s.ctypes.data if len(s) else None, len(s), n_prompt,
+                                             level, top, al, seed))
+
+    def clear_synthetic(self):
+        abi.check(abi.lib().ps_set_synthetic(self._h, None, 0, 0, 0, 0, None, 0))
+
+
+def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PIPESPEC, gammas=None,
+                 lookaheads=None, eos_id: int = -1, max_lead: int = 0):
+    k = len(stages)
+    hs = (C.c_void_p * k)(*[s.handle for s in stages])
+    g = (C.c_int32 * k)(*(gammas or [0] * k))
+    la = (C.c_int32 * k)(*(lookaheads or [0] * k))
+    opts = abi.RunOpts(mode, max_new_tokens, eos_id, g, la, max_lead)
+    p = _i32(prompt)
+    out = np.zeros(max_new_tokens, dtype=np.int32)
+    n = C.c_int32()
+    stats = abi.RunStats()
+    abi.check(abi.lib().ps_pipeline_run(hs, k, p.ctypes.data, len(p), C.byref(opts), out.ctypes.data,
+                                        C.byref(n), C.byref(stats)))
+    return out[:n.value].tolist(), stats
+
+
+def test_gemm(W: torch.Tensor, X: torch.Tensor, R: int) -> torch.Tensor:
+    """Test hook: out[r, n] = X[r] . W[n] through the production tcgen05 GEMM."""
+    N, K = W.shape
+    assert X.shape == (32, K) and X.dtype == torch.bfloat16 and W.dtype == torch.bfloat16
+    out = torch.zeros(R, N, dtype=torch.float32, device=W.device)
+    s = torch.cuda.current_stream()
+    abi.check(abi.lib().ps_test_gemm(W.data_ptr(), X.data_ptr(), out.data_ptr(), N, K, R, s.cuda_stream))
+    return out
