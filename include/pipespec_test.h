@@ -16,6 +16,13 @@ extern "C" {
  * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
 ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
 
+/* Copy `bytes` of a stage scratch buffer to host dst (synchronises the stage
+ * stream).  which: 0 x (fp32 [32,d]), 1 x∘g (bf16 [32,d]), 2 q (fp32 [32,H*hd]),
+ * 3 attention out (bf16 [32,H*hd]), 4 SwiGLU out (bf16 [32,ffn]),
+ * 5 sumsq slots (fp32 [32,ceil(d/128)]), 6 KV pool, 7 attention (m,l) partials,
+ * 8 device page table (int32). */
+ps_status ps_test_read(ps_stage* stage, int32_t which, void* dst, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -200,7 +200,9 @@ struct ps_stage {
   int32_t* h_page_table = nullptr;   // pinned mirror
   // scratch (owned)
   StepIn* d_in = nullptr;
-  StepIn* h_in = nullptr;            // pinned staging
+  StepIn* h_in = nullptr;            // pinned staging ring [kInSlots]; host writes slot `in_slot`
+  cudaEvent_t in_ev[8] = {};         // recorded after each slot's H2D copy
+  int in_slot = 0;
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
   StepOut* h_out_dev = nullptr;      // its device alias
@@ -353,7 +355,11 @@ static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
 
 static ps_status run_forward(ps_stage* S, int R, bool with_head) {
   const int b = bucket_of(R);
-  CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
+  // Forwards are enqueued back to back (prefill chunks): each uses its own
+  // staging slot, and a slot is rewritten only after its previous copy ran.
+  CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
+  CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
+  S->in_slot = (S->in_slot + 1) % 8;
   if (!S->use_graphs) return enqueue_forward(S, b, with_head);
   cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
   if (!ge) {
@@ -399,8 +405,7 @@ static void free_pages_from(ps_stage* S, long long kv_len) {
   for (long long lp = (long long)S->page_of.size() - 1; lp >= first; --lp) {
     if (S->page_of[lp] < 0) continue;
     S->free_pages.push_back(S->page_of[lp]);
-    S->page_of[lp] = -1;
-    S->h_page_table[lp] = 0;
+    S->page_of[lp] = -1;   // the pinned mirror entry may still be in flight: leave it
   }
 }
 
@@ -449,6 +454,8 @@ ps_status ps_stage_destroy(ps_stage* S) {
     if (p) cudaFree(p);
   if (S->h_page_table) cudaFreeHost(S->h_page_table);
   if (S->h_in) cudaFreeHost(S->h_in);
+  for (auto& ev : S->in_ev)
+    if (ev) cudaEventDestroy(ev);
   if (S->h_out) cudaFreeHost(S->h_out);
   if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
   delete S;
@@ -533,10 +540,11 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->ss_ld = (d + 127) / 128;
   S_TRY(cudaMalloc(&S->d_in, sizeof(StepIn)));
   S_TRY(cudaMalloc(&S->d_out, sizeof(StepOut)));
-  S_TRY(cudaHostAlloc(&S->h_in, sizeof(StepIn), cudaHostAllocDefault));
+  S_TRY(cudaHostAlloc(&S->h_in, 8 * sizeof(StepIn), cudaHostAllocDefault));
+  for (auto& ev : S->in_ev) S_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   S_TRY(cudaHostAlloc(&S->h_out, sizeof(StepOut), cudaHostAllocMapped));
   S_TRY(cudaHostGetDevicePointer((void**)&S->h_out_dev, S->h_out, 0));
-  memset(S->h_in, 0, sizeof(StepIn));
+  memset(S->h_in, 0, 8 * sizeof(StepIn));
   S_TRY(cudaMalloc(&S->x, (size_t)kMaxRows * d * 4));
   S_TRY(cudaMalloc(&S->xg, (size_t)kMaxRows * d * 2));
   S_TRY(cudaMalloc(&S->att, (size_t)kMaxRows * hq * 2));
@@ -615,7 +623,8 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
                               bool want_logits) {
   ps_status st;
   if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
-  StepIn* in = S->h_in;
+  CU_TRY(cudaEventSynchronize(S->in_ev[S->in_slot]));   // slot's previous copy done
+  StepIn* in = S->h_in + S->in_slot;
   in->R = R;
   in->pos0 = (int32_t)pos0;
   in->w = w;
@@ -846,6 +855,26 @@ extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int3
   cudaFree(cnt);
   if (st != PS_OK) return st;
   if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
+
+extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t bytes) {
+  if (!S || !dst) return fail(PS_E_INVALID, "NULL argument");
+  const void* src = nullptr;
+  switch (which) {
+    case 0: src = S->x; break;
+    case 1: src = S->xg; break;
+    case 2: src = S->q; break;
+    case 3: src = S->att; break;
+    case 4: src = S->h; break;
+    case 5: src = S->ss; break;
+    case 6: src = S->kv; break;
+    case 7: src = S->attn_ml; break;
+    case 8: src = S->d_page_table; break;
+    default: return fail(PS_E_INVALID, "unknown buffer %d", which);
+  }
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  CU_TRY(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 

@@ -1,0 +1,157 @@
+"""GPU parity of the verify hot path (ps_verify / ps_draft / ps_prefill /
+ps_kv_rollback) against the fp64 oracle, on the toy shapes (BASELINE configs[0])
+and on paper-shaped widths (LLaMA-3.2-1B full depth, LLaMA-3.1-8B and
+LLaMA-2-7B widths at reduced depth, LLaMA-68M full)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import buffer as B
+from oracle import llama as L
+from oracle import synthetic as SY
+from tests._parity import check_logits, check_tokens_teacher_forced, check_verify
+
+pytestmark = pytest.mark.gpu
+
+
+def make(shape_name, seed, layers=None, max_seq=512, **kw):
+    from paper_2505_01572_b200 import Stage
+    s = synth.preset(shape_name)
+    if layers is not None:
+        s = synth.reduced_depth(s, layers)
+    w = synth.make_weights(s, seed=seed, device="cuda")
+    return s, w, Stage(s, w, max_seq=max_seq, **kw)
+
+
+@pytest.fixture(scope="module")
+def toy():
+    s, w, st = make("toy-verifier", 21, max_seq=256)
+    w64 = synth.weights_to_numpy(w)
+    prompt = synth.make_prompt(s.vocab, 64, seed=22)
+    yield s, w, w64, st, prompt
+    st.close()
+
+
+def test_ar_stream_matches_oracle(toy):
+    s, w, w64, st, prompt = toy
+    st.prefill(prompt)
+    toks = st.draft(32)
+    assert st.tokens() == list(prompt) + toks
+    check_tokens_teacher_forced(w64, s, prompt, toks)
+
+
+@pytest.mark.parametrize("case", ["w0", "full", "reject0", "reject_mid", "w15", "w16", "w31"])
+def test_verify_windows(toy, case):
+    s, w, w64, st, prompt = toy
+    x = list(prompt)
+    stream, _ = L.ar_decode(w64, s, x, 32)
+    W = {"w0": [], "full": stream[:8], "reject0": [(stream[0] + 5) % s.vocab] + stream[1:4],
+         "reject_mid": stream[:5] + [(stream[5] + 1) % s.vocab] + stream[6:9],
+         "w15": stream[:15], "w16": stream[:16], "w31": stream[:31]}[case]
+    st.prefill(x)
+    a, nxt, logits = st.verify(W, want_logits=True)
+    ref = L.verify(w64, s, x, W)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(W))
+    assert st.tokens() == x + W[:a] + [nxt]
+    info = st.info()
+    buf = B.TokenBuffer(x)
+    buf.append(W[:a] + [nxt])
+    assert info["kv_len"] == buf.kv_len == len(x) + a
+    assert info["pages_in_use"] == buf.pages(64)
+
+
+def test_row_bucket_invariance_verify_equals_ar(toy):
+    """GPU self-consistency: a verify over w accepted drafts
+    yields bit-identical logits rows to w+1 single-token steps."""
+    s, w, w64, st, prompt = toy
+    st.prefill(prompt)
+    rows = []
+    for _ in range(20):
+        a, nxt, lg = st.verify([], want_logits=True)
+        rows.append(lg[0])
+    gpu_stream = st.tokens()[len(prompt):]
+    st.prefill(prompt)
+    a, nxt, lg = st.verify(gpu_stream[:19], want_logits=True)
+    assert a == 19 and nxt == gpu_stream[19]
+    assert np.array_equal(lg, np.stack(rows)), np.abs(lg - np.stack(rows)).max()
+
+
+def test_rollback_semantics_and_recompute(toy):
+    s, w, w64, st, prompt = toy
+    st.prefill(prompt)
+    toks = st.draft(12)
+    n = len(prompt) + 12
+    from paper_2505_01572_b200 import PipeSpecError
+    with pytest.raises(PipeSpecError):
+        st.kv_rollback(n + 1)               # keep > len: contract violation
+    with pytest.raises(PipeSpecError):
+        st.kv_rollback(0)
+    st.kv_rollback(n)                       # no-op
+    assert st.info()["kv_len"] == n - 1
+    st.kv_rollback(len(prompt) + 3)
+    info = st.info()
+    assert st.tokens() == list(prompt) + toks[:3]
+    assert info["kv_len"] == len(prompt) + 2
+    assert info["pages_in_use"] == B.pages_for(len(prompt) + 2, 64)
+    # after truncation the KV is consistent: re-drafting reproduces the stream
+    assert st.draft(9) == toks[3:]
+
+
+def test_prefill_resync_keeps_common_prefix(toy):
+    s, w, w64, st, prompt = toy
+    st.prefill(prompt)
+    st.draft(10)
+    other = list(prompt[:40]) + list(synth.make_prompt(s.vocab, 30, seed=99))
+    st.prefill(other)                        # truncate to the common prefix, extend
+    a, nxt, lg = st.verify([], want_logits=True)
+    ref = L.verify(w64, s, other, [])
+    check_logits(lg, ref["logits"])
+    check_verify((a, nxt), ref, 0)
+
+
+def test_synthetic_override_matches_counter_generator(toy):
+    """The drafter's emitted tokens follow the chained construction exactly
+    (bit-exact integers) while on the target stream."""
+    s, w, w64, st, prompt = toy
+    S = [int(x) for x in synth.make_prompt(s.vocab, 40, seed=5)]
+    for alpha in (1.0, 0.0, 0.6):
+        st.prefill(prompt)
+        st.set_synthetic(S, len(prompt), level=0, top=1, alphas=[alpha], seed=1234)
+        thrs = [SY.alpha_threshold(alpha)]
+        got = st.draft(1)[0]
+        want = SY.chained_token(S[0], 0, 1, 0, 1234, thrs, s.vocab)
+        assert got == want
+        if alpha == 1.0:
+            assert st.draft(20) == S[1:21]
+        if alpha == 0.0:
+            assert got != S[0]
+    st.clear_synthetic()
+
+
+@pytest.mark.parametrize("name,layers,plen,w", [
+    ("llama-68m", None, 96, 8),
+    ("llama3.2-1b", None, 96, 16),
+    ("llama3.1-8b", 2, 160, 16),
+    ("llama2-7b", 2, 96, 7),
+])
+def test_paper_shapes_parity(name, layers, plen, w):
+    """Full-width shapes: logits within 2e-2*max|logit| of the fp64 oracle,
+    (a, next) exact unless the deciding rows are near-ties."""
+    s, wt, st = make(name, 7, layers=layers, max_seq=plen + 40)
+    w64 = synth.weights_to_numpy(wt)
+    prompt = list(synth.make_prompt(s.vocab, plen, seed=8))
+    st.prefill(prompt)
+    stream = st.draft(w + 2)
+    st.prefill(prompt)
+    window = stream[:w // 2] + [(stream[w // 2] + 3) % s.vocab] + stream[w // 2 + 1:w]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, w)
+    st.close()
+    del wt
+    torch.cuda.empty_cache()
