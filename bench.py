@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py — PipeSpec verify hot path on B200 (BASELINE.json configs[1]).
+
+Workload (N=1): k=2 LLaMA-3.2-1B-shape -> LLaMA-3.1-8B-shape, random-init bf16
+weights, 512-token synthetic prompt, 256 greedy tokens, both stages co-resident
+on one B200.  A *step* is one pass of the whole hot path (SURVEY.md §8(a)
+a1-a13): M_0 drafts gamma tokens (gamma rows=1 forwards, synthetic alpha
+override on the emitted token), M_1 verifies the window (one rows=gamma+1
+forward + argmax/compare/scan), appends the accepted prefix + correction/bonus
+token, truncates its KV, and the drafter is resynced to M_1's buffer (the
+rollback signal).  Output is lossless: identical to M_1's autoregressive
+greedy stream, which the bench checks on every run.
+
+value    tokens/s of the whole job (device time, CUDA events, max over ranks)
+e2e      the same through the C ABI with host buffers, wall clock
+roofline the dominant kernel (gate/up GEMM of M_1) timed live with CUDA events
+cpu_baseline / --impl reference: the fp64 oracle on the host cores (bounded
+         sample, extrapolated in depth)
+
+N>1 (torchrun): every rank runs an independent replica of the batch-1 job
+(weak scaling, no data-path collective); the stage-per-GPU pipeline is the
+NEXT-1 runtime.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s batch-1 greedy & speedup vs M_k autoregressive; verify HBM GB/s"
+STEP_IN_BYTES = 160     # sizeof(StepIn): uploaded per forward (host -> device)
+STEP_OUT_BYTES = 144    # sizeof(StepOut): read back per forward (device -> host, mapped pinned)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--draft", default="llama3.2-1b")
+    ap.add_argument("--target", default="llama3.1-8b")
+    ap.add_argument("--prompt", type=int, default=512)
+    ap.add_argument("--gen", type=int, default=256)
+    ap.add_argument("--gamma", type=int, default=8)
+    ap.add_argument("--alpha", type=float, default=0.8)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def oracle_sample(draft_shape, target_shape, wd, wt, gamma, alpha, seed, n_rounds, ctx=64, layers=2):
+    """The fp64 oracle (as it stands) on the host cores: sync-SD rounds of the
+    same two shapes at `layers` of their L layers (full width and vocab), ctx
+    tokens of context; per-round time extrapolated linearly in depth:
+      t(L) = t(0) + (L / layers) * (t(layers) - t(0))   for each model.
+    Accepted lengths follow the same counter-based construction as the GPU run."""
+    import numpy as np
+
+    import synth
+    from oracle import llama as OL
+    from oracle import synthetic as SY
+
+    def np64(w, nl):
+        sub = {"embed": w["embed"], "lm_head": w["lm_head"], "final_norm": w["final_norm"],
+               "layers": w["layers"][:nl]}
+        return synth.weights_to_numpy(sub)
+
+    d2, t2 = synth.reduced_depth(draft_shape, layers), synth.reduced_depth(target_shape, layers)
+    d0, t0 = synth.reduced_depth(draft_shape, 0), synth.reduced_depth(target_shape, 0)
+    wd2, wt2 = np64(wd, layers), np64(wt, layers)
+    wd0, wt0 = dict(wd2, layers=[]), dict(wt2, layers=[])
+    prompt = [int(x) for x in synth.make_prompt(target_shape.vocab, ctx, seed + 99)]
+    thr = SY.alpha_threshold(alpha)
+    times, toks = [], 0
+    p = 0
+    for _ in range(n_rounds):
+        t_start = time.perf_counter()
+        per = {}
+        for name, (w, s) in {"d2": (wd2, d2), "d0": (wd0, d0), "t2": (wt2, t2), "t0": (wt0, t0)}.items():
+            sess = OL.Session(w, s)
+            sess.forward(prompt)                       # context (not timed)
+            t1 = time.perf_counter()
+            if name.startswith("d"):
+                z = sess.forward(prompt[-1:])
+                for _ in range(gamma - 1):
+                    z = sess.forward([OL.greedy(z[-1])])
+            else:
+                sess.forward(prompt[-1:] + prompt[:gamma])   # one verify forward, R = gamma + 1
+            per[name] = time.perf_counter() - t1
+        tD = per["d0"] + draft_shape.n_layers / layers * (per["d2"] - per["d0"])
+        tT = per["t0"] + target_shape.n_layers / layers * (per["t2"] - per["t0"])
+        a = 0
+        while a < gamma and SY.agree(seed, 0, p + a, thr):
+            a += 1
+        p += a + 1
+        toks += a + 1
+        times.append(tD + tT)
+        del t_start
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((i.get("num_threads", 0) for i in threadpool_info()), default=cores)
+    except Exception:
+        blas = cores
+    return toks / sum(times), min(cores, blas), times, toks
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, same metric/config."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import torch
+
+    import synth
+    ds, ts = synth.preset(args.draft), synth.preset(args.target)
+    # the oracle only needs the first 2 layers + embeddings (CPU generation)
+    wd = synth.make_weights(synth.reduced_depth(ds, 2), seed=args.seed, device="cpu")
+    wt = synth.make_weights(synth.reduced_depth(ts, 2), seed=args.seed + 1, device="cpu")
+    del torch
+    tot_t, tot_tok = 0.0, 0
+    _, _, _, _ = oracle_sample(ds, ts, wd, wt, args.gamma, args.alpha, args.seed, 1) if args.warmup else (0, 0, 0, 0)
+    val, cores, times, toks = oracle_sample(ds, ts, wd, wt, args.gamma, args.alpha, args.seed, args.steps)
+    tot_t, tot_tok = sum(times), toks
+    line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"k=2 {args.draft}->{args.target} sync-SD round, gamma={args.gamma}, "
+                                   f"alpha={args.alpha} synthetic", "prompt": args.prompt, "gen": args.gen},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} oracle sync-SD rounds at 2 of L layers (full width/vocab), "
+                                       "64-token context, extrapolated linearly in depth"},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2505_01572_b200 import Stage, abi
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ds, ts = synth.preset(args.draft), synth.preset(args.target)
+    g = args.gamma
+    max_seq = args.prompt + args.gen + 4 * g + 64
+    wd = synth.make_weights(ds, seed=args.seed, device="cuda")
+    wt = synth.make_weights(ts, seed=args.seed + 1, device="cuda")
+    drafter = Stage(ds, wd, max_seq=max_seq, max_window=g)
+    target = Stage(ts, wt, max_seq=max_seq, max_window=g)
+    prompt = [int(x) for x in synth.make_prompt(ts.vocab, args.prompt, seed=args.seed + 17 + rank)]
+    L = abi.lib()
+
+    # --- M_K autoregressive: the lossless reference stream S and the AR baseline
+    target.prefill(prompt)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(target.stream)
+    S = target.draft(args.gen + 2 * g + 2)
+    e1.record(target.stream)
+    e1.synchronize()
+    ar_tok_s = len(S) / (e0.elapsed_time(e1) / 1e3)
+    target.kv_rollback(args.prompt)
+    drafter.prefill(prompt)
+    drafter.set_synthetic(S, args.prompt, level=0, top=1, alphas=[args.alpha], seed=args.seed + 1234)
+
+    state = {"gen": [], "pass_ms": [], "pass_ctx": []}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def step(record):
+        if len(state["gen"]) >= args.gen:          # job restarts from the prompt
+            assert state["gen"][:args.gen] == S[:args.gen], "lossless check failed"
+            target.kv_rollback(args.prompt)
+            drafter.resync(prompt)
+            state["gen"] = []
+        d = drafter.draft(g)
+        if record:
+            ev[0].record(target.stream)
+        a, nxt = target.verify(d)
+        if record:
+            ev[1].record(target.stream)
+            ev[1].synchronize()
+            state["pass_ms"].append(ev[0].elapsed_time(ev[1]))
+            state["pass_ctx"].append(args.prompt + len(state["gen"]))
+        new = d[:a] + [nxt]
+        state["gen"] += new
+        drafter.resync(prompt + state["gen"])     # rollback signal: O_0 := O_1 (lazy KV catch-up)
+        return len(new)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = L.ps_kernel_launch_count()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        t0e.record(drafter.stream)
+        for _ in range(args.steps):
+            tokens += step(True)
+        t1e.record(target.stream)
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+    launches = L.ps_kernel_launch_count() - launches0
+    dev_s = t0e.elapsed_time(t1e) / 1e3
+    wall_s = w1 - w0
+    if world > 1:
+        t = torch.tensor([dev_s, wall_s, float(tokens)], device="cuda", dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[2:], op=dist.ReduceOp.SUM)
+        dev_s, wall_s, tot_tokens = float(mx[0]), float(mx[1]), float(t[2])
+    else:
+        tot_tokens = float(tokens)
+
+    # --- dominant kernel: gate/up GEMM of M_1, timed live on its stream (cycling layers)
+    # (the target's last forward was a verify over R = gamma + 1 rows: same bucket, same StepIn)
+    R = g + 1
+    n_it = 3 * ts.n_layers
+    gu_ms = sum(target.time_kernel(4, l % ts.n_layers, 1) for l in range(n_it)) / n_it
+    rows_last = R
+    gu_bytes = 2 * ts.d_ffn * ts.d_model * 2 + rows_last * ts.d_model * 2 + rows_last * ts.d_ffn * 2
+    gu_gbs = gu_bytes / (gu_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get("gate_up_gemm_bytes_per_launch")
+    except Exception:
+        pass
+
+    # --- verify pass (whole graph) roofline
+    pass_ms = statistics.mean(state["pass_ms"]) if state["pass_ms"] else float("nan")
+    ctx = statistics.mean(state["pass_ctx"]) if state["pass_ctx"] else args.prompt
+    pass_bytes = ts.streamed_bytes_per_pass(R) + (ctx + R) * ts.kv_bytes_per_token()
+    pass_gbs = pass_bytes / (pass_ms * 1e-3) / 1e9
+
+    value = tot_tokens / dev_s
+    e2e = tot_tokens / wall_s
+    fwd_per_step = g + 1
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"k=2 {args.draft}->{args.target} (BASELINE configs[1]), sync-SD round "
+                               f"gamma={args.gamma}, synthetic alpha={args.alpha}, co-resident on 1 GPU",
+                   "prompt": args.prompt, "gen": args.gen, "global_batch": world,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs > L2 (16 GB of 8B weights streamed per verify pass)"},
+        "speedup_vs_ar": value / ar_tok_s, "ar_tokens_per_s": ar_tok_s,
+        "tokens_per_step": tot_tokens / world / args.steps,
+        "verify_pass": {"ms": pass_ms, "rows": R, "ctx": ctx, "bytes": pass_bytes, "GB/s": pass_gbs,
+                        "frac": pass_gbs / peak},
+        "roofline": {"kernel": "gate_up_gemm (M_1 layer, tcgen05 stream-K, SwiGLU epilogue)",
+                     "bound": "hbm", "achieved": gu_gbs, "peak": peak, "unit": "GB/s", "frac": gu_gbs / peak,
+                     "traffic": traffic, "rows": rows_last,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+        "e2e": {"value": e2e, "unit": "tokens/s",
+                "h2d_bytes_per_step": fwd_per_step * STEP_IN_BYTES + g * 4,
+                "d2h_bytes_per_step": fwd_per_step * STEP_OUT_BYTES},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, times, toks = oracle_sample(ds, ts, wd, wt, g, args.alpha, args.seed + 1234, 2)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                "sample": f"2 oracle sync-SD rounds (gamma={g}) at 2 of L layers, full width/vocab, "
+                                          "64-token context, extrapolated linearly in depth"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    drafter.close()
+    target.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -95,7 +95,7 @@ typedef struct ps_placement {
 typedef struct ps_stage_opts {
   int32_t max_seq;          /* max tokens in O_i (prompt + generated), >= 2   */
   int32_t max_window;       /* max w accepted by ps_verify, 0..31             */
-  int32_t page_size;        /* tokens per KV page, power of two in [16,256]   */
+  int32_t page_size;        /* tokens per KV page: 64, 128 or 256             */
   void* kv_pool;
   int64_t kv_pool_bytes;
   void* stream;
@@ -121,6 +121,13 @@ ps_status ps_stage_destroy(ps_stage* stage);
  * is pending.  Serves as prefill, as catch-up after a resync, and as the
  * extend half of "rollback O_i to match O_j". */
 ps_status ps_prefill(ps_stage* stage, const int32_t* tokens, int32_t n);
+
+/* Lazy form of ps_prefill for the rollback cascade ("Rollback O_i to match
+ * O_j's last token"; reading R2): O_i := tokens[0:n] (host), keeping the
+ * KV of the longest common prefix; the KV of the remaining positions is
+ * computed by the next ps_draft / ps_verify as extra leading rows of that
+ * forward (in 32-row chunks if more are pending).  No device work here. */
+ps_status ps_resync(ps_stage* stage, const int32_t* tokens, int32_t n);
 
 /* n_steps greedy autoregressive steps (rows = 1 each; Alg.1
  * "Generate next token, append to O_0"), appended to O_i; the tokens are

@@ -16,6 +16,13 @@ extern "C" {
  * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
 ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
 
+/* Re-launch one kernel of the stage's most recent forward configuration
+ * (same rows bucket, same device StepIn) `iters` times back to back on the
+ * stage stream and return the average CUDA-event time per launch.
+ * kind: 0 embed, 1 QKV GEMM, 2 attention, 3 O GEMM, 4 gate/up GEMM,
+ * 5 down GEMM, 6 lm_head GEMM, 7 argmax/scan; layer selects the weights. */
+ps_status ps_time_kernel(ps_stage* stage, int32_t kind, int32_t layer, int32_t iters, double* avg_ms);
+
 /* Copy `bytes` of a stage scratch buffer to host dst (synchronises the stage
  * stream).  which: 0 x (fp32 [32,d]), 1 x∘g (bf16 [32,d]), 2 q (fp32 [32,H*hd]),
  * 3 attention out (bf16 [32,H*hd]), 4 SwiGLU out (bf16 [32,ffn]),

@@ -83,6 +83,8 @@ _PROTOS = {
                                      C.POINTER(C.c_double), C.c_uint64]),
     "ps_pipeline_run": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.POINTER(RunOpts),
                                     C.c_void_p, _I32P, C.POINTER(RunStats)]),
+    "ps_resync": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "ps_time_kernel": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "ps_test_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
     "ps_test_gemm": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  C.c_void_p]),

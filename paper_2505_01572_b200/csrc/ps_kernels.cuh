@@ -35,9 +35,10 @@ struct StepIn {                    // written by the host before every forward
   int32_t pos0;                    // absolute position of row 0
   int32_t w;                       // drafts in the window (rows 1..w), verify only
   int32_t flags;                   // kFlagLogits | kFlagSynth
-  int32_t syn_p0;                  // generated index predicted by row 0 (= n - n_prompt)
+  int32_t syn_p0;                  // generated index predicted by row row0 (= n - n_prompt)
   int32_t syn_onpath;              // 1 iff the committed context is on the target stream
-  int32_t pad[2];
+  int32_t row0;                    // first prediction row (rows before it are KV catch-up)
+  int32_t pad;
   int32_t tokens[kMaxRows];        // row tokens: [pending, d_0, ..., d_{w-1}]
 };
 constexpr int kFlagLogits = 1;
@@ -594,24 +595,25 @@ __global__ void __launch_bounds__(1024) argmax_scan_kernel(const __grid_constant
   __syncthreads();
   if (threadIdx.x == 0) {
     const int w = st->w;
+    const int r0 = st->row0;             // prediction rows r0 .. r0 + w
     if ((st->flags & kFlagSynth) && p.syn != nullptr && p.syn->len_S > 0 && st->syn_onpath) {
-      // row j's context is x ++ d[0:j]; on-path while the drafts follow S
+      // prediction row j's context is x ++ d[0:j]; on-path while the drafts follow S
       bool on = true;
-      for (int j = 0; j < R && on; ++j) {
+      for (int j = 0; j <= w && on; ++j) {
         const int pj = st->syn_p0 + j;
         if (pj >= p.syn->len_S) break;
-        s_pred[j] = synth_token(p.syn, pj);
-        if (j < R - 1) on = (st->tokens[1 + j] == p.syn->S[pj]);
+        s_pred[r0 + j] = synth_token(p.syn, pj);
+        if (j < w) on = (st->tokens[r0 + 1 + j] == p.syn->S[pj]);
       }
     }
     int a = 0;
-    while (a < w && s_pred[a] == st->tokens[1 + a]) ++a;
+    while (a < w && s_pred[r0 + a] == st->tokens[r0 + 1 + a]) ++a;
     StepOut o;
     o.a = a;
-    o.next = s_pred[a];
+    o.next = s_pred[r0 + a];
     o.R = R;
     o.pad = 0;
-    for (int j = 0; j < kMaxRows; ++j) o.pred[j] = j < R ? s_pred[j] : -1;
+    for (int j = 0; j < kMaxRows; ++j) o.pred[j] = j <= w ? s_pred[r0 + j] : -1;
     *p.out = o;
     if (p.mirror != nullptr) {
       volatile int* m = reinterpret_cast<volatile int*>(p.mirror);

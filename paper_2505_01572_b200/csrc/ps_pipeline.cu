@@ -28,7 +28,7 @@ ps_status tokens_of(ps_stage* s, std::vector<int32_t>& v) {
 // stage 0 drafts autoregressively; stage i>0 runs sync SD with stage i-1.
 ps_status produce(ps_stage* const* S, int i, const std::vector<int32_t>& ctx, int m, const ps_run_opts* o,
                   std::vector<int32_t>& out, ps_run_stats* stt) {
-  ps_status st = ps_prefill(S[i], ctx.data(), (int32_t)ctx.size());
+  ps_status st = ps_resync(S[i], ctx.data(), (int32_t)ctx.size());   // rollback cascade, lazy KV catch-up
   if (st != PS_OK) return st;
   out.clear();
   const int gamma = (i > 0 && o->gamma) ? o->gamma[i] : 0;

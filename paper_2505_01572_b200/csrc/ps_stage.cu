@@ -203,6 +203,7 @@ struct ps_stage {
   StepIn* h_in = nullptr;            // pinned staging ring [kInSlots]; host writes slot `in_slot`
   cudaEvent_t in_ev[8] = {};         // recorded after each slot's H2D copy
   int in_slot = 0;
+  int last_bucket = 0;
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
   StepOut* h_out_dev = nullptr;      // its device alias
@@ -265,89 +266,109 @@ static void rope_table(const ps_model_shape& s, int max_seq, std::vector<float2>
 }
 
 // ---------------------------------------------------------------- forward
-// Enqueue one forward over StepIn rows (already uploaded): embed, L x {QKV,
-// attention, O, gate/up, down}, then (with_head) lm_head + argmax/scan.
-static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
+enum { K_EMBED = 0, K_QKV, K_ATTN, K_O, K_GU, K_DOWN, K_LMHEAD, K_ARGMAX };
+
+// Launch one kernel of the forward for rows bucket b (layer l where relevant).
+static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
   const ps_model_shape& sh = S->sh;
   const int RP = bucket_rp(b);
   const int d = sh.d_model, hq = sh.n_heads * sh.head_dim, hkv = sh.n_kv_heads * sh.head_dim;
-  ps_status st;
-  int nk = 0;
-  {
-    EmbedParams e{S->d_in, S->embed, d, S->lw[0 * 9 + PS_N_ATTN], S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
-    if (sh.n_layers == 0) e.gain = S->final_norm;
-    if ((st = launch_simple(embed_kernel, dim3(RP), dim3(128), 0, e, S->stream)) != PS_OK) return st;
-    ++nk;
-  }
   const float inv_d = 1.0f / d;
   const int ss_n = (d + 127) / 128;
-  for (int l = 0; l < sh.n_layers; ++l) {
-    const __nv_bfloat16* const* W = &S->lw[(size_t)l * 9];
-    const LayerMaps& M = S->maps[l];
-    GemmParams p = {};
-    p.step = S->d_in;
-    p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
-    p.ws = S->ws; p.counters = S->counters;
-    // --- QKV + RoPE + paged KV append
-    p.mode = EPI_QKV;
-    p.N = hq + 2 * hkv;
-    p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg;
-    p.t1 = (hq + 127) / 128; p.t2 = p.t1 + (hkv + 127) / 128;
-    p.nq = hq; p.nk = hkv;
-    p.q = S->q; p.ld_q = hq;
-    p.kv = S->kv; p.page_table = S->d_page_table; p.page_size = S->page_size; p.layer = l;
-    p.hkv = sh.n_kv_heads; p.hd = sh.head_dim; p.page_stride = S->page_elems; p.rope_cs = S->rope_cs;
-    if ((st = launch_gemm(RP, false, M.q, M.k, M.v, S->map_xg[b], p, S->gs_qkv.grid, S->stream)) != PS_OK) return st;
-    ++nk;
-    // --- attention
-    AttnParams a{};
-    a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
-    a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
-    a.H = sh.n_heads; a.hd = sh.head_dim; a.scale = 1.0f / std::sqrt((float)sh.head_dim);
-    a.max_chunks = S->max_chunks; a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
-    a.out = S->att; a.ld_out = hq;
-    if ((st = launch_simple(attn_kernel, dim3(S->attn_grid), dim3(128), kAttnSmem, a, S->stream)) != PS_OK) return st;
-    ++nk;
-    // --- O projection + residual; writes x∘g_mlp and sumsq
-    GemmParams o = {};
-    o.step = S->d_in; o.mode = EPI_RESID; o.N = d;
-    o.n_tiles = S->gs_o.n_tiles; o.kb_total = S->gs_o.kb_total; o.maxseg = S->gs_o.maxseg;
-    o.x = S->x; o.ld_x = d; o.xg = S->xg; o.ld_xg = S->xg_ld; o.gain = W[PS_N_MLP];
-    o.ss_out = S->ss; o.ss_out_ld = S->ss_ld; o.ws = S->ws; o.counters = S->counters;
-    if ((st = launch_gemm(RP, false, M.o, M.o, M.o, S->map_att[b], o, S->gs_o.grid, S->stream)) != PS_OK) return st;
-    ++nk;
-    // --- gate/up + SiLU*mul
-    GemmParams g = {};
-    g.step = S->d_in; g.mode = EPI_SWIGLU; g.N = sh.d_ffn;
-    g.n_tiles = S->gs_gu.n_tiles; g.kb_total = S->gs_gu.kb_total; g.maxseg = S->gs_gu.maxseg;
-    g.ss_in = S->ss; g.ss_n = ss_n; g.ss_ld = S->ss_ld; g.inv_d = inv_d; g.eps = sh.rms_eps;
-    g.h = S->h; g.ld_h = sh.d_ffn; g.ws = S->ws; g.counters = S->counters;
-    if ((st = launch_gemm(RP, true, M.g, M.u, M.u, S->map_xg[b], g, S->gs_gu.grid, S->stream)) != PS_OK) return st;
-    ++nk;
-    // --- down + residual; writes x∘g_next and sumsq
-    GemmParams dn = {};
-    dn.step = S->d_in; dn.mode = EPI_RESID; dn.N = d;
-    dn.n_tiles = S->gs_d.n_tiles; dn.kb_total = S->gs_d.kb_total; dn.maxseg = S->gs_d.maxseg;
-    dn.x = S->x; dn.ld_x = d; dn.xg = S->xg; dn.ld_xg = S->xg_ld;
-    dn.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
-    dn.ss_out = S->ss; dn.ss_out_ld = S->ss_ld; dn.ws = S->ws; dn.counters = S->counters;
-    if ((st = launch_gemm(RP, false, M.d, M.d, M.d, S->map_h[b], dn, S->gs_d.grid, S->stream)) != PS_OK) return st;
-    ++nk;
+  const __nv_bfloat16* const* W = sh.n_layers ? &S->lw[(size_t)l * 9] : nullptr;
+  switch (kind) {
+    case K_EMBED: {
+      EmbedParams e{S->d_in, S->embed, d, sh.n_layers ? S->lw[PS_N_ATTN] : S->final_norm,
+                    S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
+      return launch_simple(embed_kernel, dim3(RP), dim3(128), 0, e, S->stream);
+    }
+    case K_QKV: {   // QKV + RoPE + paged KV append (a4, a5)
+      const LayerMaps& M = S->maps[l];
+      GemmParams p = {};
+      p.step = S->d_in;
+      p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
+      p.ws = S->ws; p.counters = S->counters;
+      p.mode = EPI_QKV;
+      p.N = hq + 2 * hkv;
+      p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg;
+      p.t1 = (hq + 127) / 128; p.t2 = p.t1 + (hkv + 127) / 128;
+      p.nq = hq; p.nk = hkv;
+      p.q = S->q; p.ld_q = hq;
+      p.kv = S->kv; p.page_table = S->d_page_table; p.page_size = S->page_size; p.layer = l;
+      p.hkv = sh.n_kv_heads; p.hd = sh.head_dim; p.page_stride = S->page_elems; p.rope_cs = S->rope_cs;
+      return launch_gemm(RP, false, M.q, M.k, M.v, S->map_xg[b], p, S->gs_qkv.grid, S->stream);
+    }
+    case K_ATTN: {  // split-KV decode attention (a6)
+      AttnParams a{};
+      a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
+      a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
+      a.H = sh.n_heads; a.hd = sh.head_dim; a.scale = 1.0f / std::sqrt((float)sh.head_dim);
+      a.max_chunks = S->max_chunks; a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
+      a.out = S->att; a.ld_out = hq;
+      return launch_simple(attn_kernel, dim3(S->attn_grid), dim3(128), kAttnSmem, a, S->stream);
+    }
+    case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
+      const LayerMaps& M = S->maps[l];
+      GemmParams o = {};
+      o.step = S->d_in; o.mode = EPI_RESID; o.N = d;
+      o.n_tiles = S->gs_o.n_tiles; o.kb_total = S->gs_o.kb_total; o.maxseg = S->gs_o.maxseg;
+      o.x = S->x; o.ld_x = d; o.xg = S->xg; o.ld_xg = S->xg_ld; o.gain = W[PS_N_MLP];
+      o.ss_out = S->ss; o.ss_out_ld = S->ss_ld; o.ws = S->ws; o.counters = S->counters;
+      return launch_gemm(RP, false, M.o, M.o, M.o, S->map_att[b], o, S->gs_o.grid, S->stream);
+    }
+    case K_GU: {    // gate/up + SiLU*mul (a8)
+      const LayerMaps& M = S->maps[l];
+      GemmParams g = {};
+      g.step = S->d_in; g.mode = EPI_SWIGLU; g.N = sh.d_ffn;
+      g.n_tiles = S->gs_gu.n_tiles; g.kb_total = S->gs_gu.kb_total; g.maxseg = S->gs_gu.maxseg;
+      g.ss_in = S->ss; g.ss_n = ss_n; g.ss_ld = S->ss_ld; g.inv_d = inv_d; g.eps = sh.rms_eps;
+      g.h = S->h; g.ld_h = sh.d_ffn; g.ws = S->ws; g.counters = S->counters;
+      return launch_gemm(RP, true, M.g, M.u, M.u, S->map_xg[b], g, S->gs_gu.grid, S->stream);
+    }
+    case K_DOWN: {  // down + residual; writes x∘g_next and sumsq (a9)
+      const LayerMaps& M = S->maps[l];
+      GemmParams dn = {};
+      dn.step = S->d_in; dn.mode = EPI_RESID; dn.N = d;
+      dn.n_tiles = S->gs_d.n_tiles; dn.kb_total = S->gs_d.kb_total; dn.maxseg = S->gs_d.maxseg;
+      dn.x = S->x; dn.ld_x = d; dn.xg = S->xg; dn.ld_xg = S->xg_ld;
+      dn.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
+      dn.ss_out = S->ss; dn.ss_out_ld = S->ss_ld; dn.ws = S->ws; dn.counters = S->counters;
+      return launch_gemm(RP, false, M.d, M.d, M.d, S->map_h[b], dn, S->gs_d.grid, S->stream);
+    }
+    case K_LMHEAD: {  // final norm + lm_head + argmax partials (a10)
+      GemmParams p = {};
+      p.step = S->d_in; p.mode = EPI_LMHEAD; p.N = sh.vocab;
+      p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
+      p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
+      p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
+      p.ws = S->ws; p.counters = S->counters;
+      return launch_gemm(RP, false, S->map_lm, S->map_lm, S->map_lm, S->map_xg[b], p, S->gs_lm.grid, S->stream);
+    }
+    case K_ARGMAX: {  // argmax + compare + first-mismatch scan (a11)
+      ArgmaxParams ap{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
+      return launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, ap, S->stream);
+    }
   }
+  return fail(PS_E_INVALID, "unknown kernel kind %d", kind);
+}
+
+// Enqueue one forward over StepIn rows (already uploaded): embed, L x {QKV,
+// attention, O, gate/up, down}, then (with_head) lm_head + argmax/scan.
+// Consecutive kernels are chained with programmatic dependent launch.
+static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
+  ps_status st;
+  int nk = 0;
+  if ((st = launch_one(S, b, K_EMBED, 0)) != PS_OK) return st;
+  ++nk;
+  for (int l = 0; l < S->sh.n_layers; ++l)
+    for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
+      if ((st = launch_one(S, b, kind, l)) != PS_OK) return st;
+      ++nk;
+    }
   if (with_head) {
-    GemmParams p = {};
-    p.step = S->d_in; p.mode = EPI_LMHEAD; p.N = sh.vocab;
-    p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
-    p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
-    p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
-    p.ws = S->ws; p.counters = S->counters;
-    if ((st = launch_gemm(RP, false, S->map_lm, S->map_lm, S->map_lm, S->map_xg[b], p, S->gs_lm.grid, S->stream)) !=
-        PS_OK)
-      return st;
-    ++nk;
-    ArgmaxParams ap{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
-    if ((st = launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, ap, S->stream)) != PS_OK) return st;
-    ++nk;
+    if ((st = launch_one(S, b, K_LMHEAD, 0)) != PS_OK) return st;
+    if ((st = launch_one(S, b, K_ARGMAX, 0)) != PS_OK) return st;
+    nk += 2;
   }
   S->kernels_per_fwd[with_head ? 1 : 0] = nk;
   return PS_OK;
@@ -355,6 +376,7 @@ static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
 
 static ps_status run_forward(ps_stage* S, int R, bool with_head) {
   const int b = bucket_of(R);
+  S->last_bucket = b;
   // Forwards are enqueued back to back (prefill chunks): each uses its own
   // staging slot, and a slot is rewritten only after its previous copy ran.
   CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
@@ -620,7 +642,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
 // One forward over tokens [start, start+R) at positions [start, start+R);
 // with_head computes logits/argmax for all rows.
 static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long pos0, int w, bool with_head,
-                              bool want_logits) {
+                              bool want_logits, int row0 = 0) {
   ps_status st;
   if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
   CU_TRY(cudaEventSynchronize(S->in_ev[S->in_slot]));   // slot's previous copy done
@@ -631,6 +653,7 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   in->flags = (want_logits ? kFlagLogits : 0);
   in->syn_p0 = 0;
   in->syn_onpath = 0;
+  in->row0 = row0;
   if (with_head && !S->S_host.empty()) {
     in->flags |= kFlagSynth;
     const long long gen = (long long)S->tokens.size() - S->n_prompt;
@@ -650,7 +673,8 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   // keep the KV of the longest common prefix
   long long m = 0;
   while (m < (long long)S->tokens.size() && m < n && S->tokens[m] == tokens[m]) ++m;
-  const long long keep_kv = std::min<long long>(S->kv_len, std::max<long long>(m - 1, 0));
+  // KV at position p depends on tokens[0..p] only: valid for p < m
+  const long long keep_kv = std::min<long long>(S->kv_len, std::min<long long>(m, n - 1));
   S->tokens.assign(tokens, tokens + n);
   S->kv_len = keep_kv;
   free_pages_from(S, S->kv_len);
@@ -670,20 +694,50 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   return PS_OK;
 }
 
+// Rows of one verify forward: the KV catch-up suffix tokens[kv_len .. n-2]
+// (non-empty only after a lazy ps_resync), the pending token x[n-1], then the
+// window; predictions are read from rows row0 = n-1-kv_len onwards.
+static ps_status catch_up(ps_stage* S, int reserve_rows) {
+  const long long n = (long long)S->tokens.size();
+  while ((n - 1 - S->kv_len) + reserve_rows > kMaxRows) {
+    const int R = (int)std::min<long long>(kMaxRows, n - 1 - S->kv_len);
+    ps_status st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
+    if (st != PS_OK) return st;
+    S->kv_len += R;
+  }
+  return PS_OK;
+}
+
+ps_status ps_resync(ps_stage* S, const int32_t* tokens, int32_t n) {
+  if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
+  if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "resync length %d not in [1, max_seq]", n);
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= S->sh.vocab) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
+  long long m = 0;
+  while (m < (long long)S->tokens.size() && m < n && S->tokens[m] == tokens[m]) ++m;
+  S->kv_len = std::min<long long>(S->kv_len, std::min<long long>(m, n - 1));
+  S->tokens.assign(tokens, tokens + n);
+  free_pages_from(S, S->kv_len);
+  update_onpath(S);
+  return PS_OK;
+}
+
 static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t* a_out, int32_t* next_out,
                              float* logits_out) {
   const long long n = (long long)S->tokens.size();
   if (n < 1) return fail(PS_E_CONTRACT, "verify on an empty token buffer (call ps_prefill first)");
   if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d > max_window %d", w, S->max_window);
   if (n + w > S->max_seq) return fail(PS_E_CAPACITY, "n + w = %lld exceeds max_seq", n + w);
-  if (S->kv_len != n - 1) return fail(PS_E_CONTRACT, "KV covers %lld positions, expected %lld", S->kv_len, n - 1);
-  int32_t rows[kMaxRows];
-  rows[0] = S->tokens[n - 1];
-  for (int j = 0; j < w; ++j) {
+  if (S->kv_len > n - 1) return fail(PS_E_CONTRACT, "KV covers %lld positions > n-1 = %lld", S->kv_len, n - 1);
+  for (int j = 0; j < w; ++j)
     if (window[j] < 0 || window[j] >= S->sh.vocab) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
-    rows[1 + j] = window[j];
-  }
-  ps_status st = forward_rows(S, rows, w + 1, n - 1, w, true, logits_out != nullptr);
+  ps_status st = catch_up(S, 1 + w);
+  if (st != PS_OK) return st;
+  const int row0 = (int)(n - 1 - S->kv_len);
+  int32_t rows[kMaxRows];
+  for (int j = 0; j <= row0; ++j) rows[j] = S->tokens[S->kv_len + j];
+  for (int j = 0; j < w; ++j) rows[row0 + 1 + j] = window[j];
+  st = forward_rows(S, rows, row0 + 1 + w, S->kv_len, w, true, logits_out != nullptr, row0);
   if (st != PS_OK) return st;
   if (logits_out) {
     cudaPointerAttributes at{};
@@ -691,7 +745,8 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
     if (cudaPointerGetAttributes(&at, logits_out) == cudaSuccess && at.type == cudaMemoryTypeDevice)
       kind = cudaMemcpyDeviceToDevice;
     cudaGetLastError();
-    CU_TRY(cudaMemcpyAsync(logits_out, S->logits, (size_t)(w + 1) * S->sh.vocab * 4, kind, S->stream));
+    CU_TRY(cudaMemcpyAsync(logits_out, S->logits + (size_t)row0 * S->sh.vocab, (size_t)(w + 1) * S->sh.vocab * 4,
+                           kind, S->stream));
   }
   CU_TRY(cudaStreamSynchronize(S->stream));
   const StepOut* r = S->h_out;
@@ -855,6 +910,28 @@ extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int3
   cudaFree(cnt);
   if (st != PS_OK) return st;
   if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
+
+extern "C" ps_status ps_time_kernel(ps_stage* S, int32_t kind, int32_t layer, int32_t iters, double* avg_ms) {
+  if (!S || !avg_ms || iters < 1) return fail(PS_E_INVALID, "bad arguments");
+  if (kind < K_EMBED || kind > K_ARGMAX) return fail(PS_E_INVALID, "unknown kernel kind %d", kind);
+  if (layer < 0 || (S->sh.n_layers > 0 && layer >= S->sh.n_layers)) return fail(PS_E_INVALID, "bad layer");
+  CU_TRY(cudaSetDevice(S->device));
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  ps_status st = PS_OK;
+  CU_TRY(cudaEventRecord(e0, S->stream));
+  for (int i = 0; i < iters && st == PS_OK; ++i) st = launch_one(S, S->last_bucket, kind, layer);
+  CU_TRY(cudaEventRecord(e1, S->stream));
+  CU_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != PS_OK) return st;
+  *avg_ms = ms / iters;
   return PS_OK;
 }
 

@@ -87,6 +87,17 @@ class Stage:
         t = _i32(tokens)
         abi.check(abi.lib().ps_prefill(self._h, t.ctypes.data, len(t)))
 
+    def resync(self, tokens):
+        """Lazy rollback-and-extend to `tokens` (KV catch-up folded into the next forward)."""
+        t = _i32(tokens)
+        abi.check(abi.lib().ps_resync(self._h, t.ctypes.data, len(t)))
+
+    def time_kernel(self, kind: int, layer: int = 0, iters: int = 20) -> float:
+        """Average ms per launch of one kernel of the last forward configuration."""
+        ms = C.c_double()
+        abi.check(abi.lib().ps_time_kernel(self._h, kind, layer, iters, C.byref(ms)))
+        return ms.value
+
     def draft(self, n_steps: int) -> list[int]:
         out = np.zeros(max(1, n_steps), dtype=np.int32)
         abi.check(abi.lib().ps_draft(self._h, n_steps, out.ctypes.data))

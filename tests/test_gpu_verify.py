@@ -155,3 +155,26 @@ def test_paper_shapes_parity(name, layers, plen, w):
     st.close()
     del wt
     torch.cuda.empty_cache()
+
+
+def test_lazy_resync_catch_up_equals_eager(toy):
+    """ps_resync defers the KV of a resynced suffix into the next forward's
+    leading rows; the result equals an eager ps_prefill bit-exactly."""
+    s, w, w64, st, prompt = toy
+    st.prefill(prompt)
+    base = st.draft(6)
+    other = list(prompt) + base[:2] + [(base[2] + 9) % s.vocab] + list(synth.make_prompt(s.vocab, 5, 3))
+    st.resync(other)
+    assert st.tokens() == other
+    a1, n1, l1 = st.verify(base[:3], want_logits=True)
+    st.prefill(prompt)
+    st.prefill(other)
+    a2, n2, l2 = st.verify(base[:3], want_logits=True)
+    assert (a1, n1) == (a2, n2) and np.array_equal(l1, l2)
+    # a long pending suffix (> 31 rows) is caught up in chunks
+    longer = list(prompt[:10]) + list(synth.make_prompt(s.vocab, 70, 4))
+    st.resync(longer)
+    a3, n3, l3 = st.verify([], want_logits=True)
+    ref = L.verify(w64, s, longer, [])
+    check_logits(l3, ref["logits"])
+    check_verify((a3, n3), ref, 0)
