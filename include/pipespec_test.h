@@ -16,6 +16,20 @@ extern "C" {
  * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
 ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
 
+/* As ps_test_gemm, then `iters` timed launches: *avg_ms = CUDA-event time per
+ * launch; cta_trace (host, may be NULL) receives per-CTA %globaltimer stamps
+ * [iters][grid][4] = {entry, producer done, MMA done, exit} of every launch
+ * (grid = min(#SMs, tiles * K/64)). */
+ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                             void* stream, int32_t iters, float* avg_ms, uint64_t* cta_trace);
+
+/* Launch-overhead probe: an empty kernel with `smem` bytes of dynamic shared
+ * memory, `iters` back-to-back launches; *avg_ms per launch. */
+ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters, int32_t flags,
+                                  float* avg_ms);
+/* Test-only launch flags (bit0: launch GEMMs without programmatic dependent launch). */
+void ps_test_set_flags(int32_t flags);
+
 /* Re-launch one kernel of the stage's most recent forward configuration
  * (same rows bucket, same device StepIn) `iters` times back to back on the
  * stage stream and return the average CUDA-event time per launch.

@@ -86,6 +86,11 @@ _PROTOS = {
     "ps_resync": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32]),
     "ps_time_kernel": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "ps_test_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
+    "ps_test_gemm_timed": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_void_p, C.c_int32, C.POINTER(C.c_float), C.c_void_p]),
+    "ps_test_launch_overhead": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.POINTER(C.c_float)]),
+    "ps_test_set_flags": (None, [C.c_int32]),
     "ps_test_gemm": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  C.c_void_p]),
 }

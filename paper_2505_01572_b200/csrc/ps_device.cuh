@@ -139,6 +139,11 @@ PS_DEV void tmem_ld16(uint32_t taddr, float* v) {
 }
 
 // ------------------------------------------------------------------ misc
+PS_DEV unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 PS_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -152,6 +157,8 @@ PS_DEV unsigned long long warp_max_u64(unsigned long long v) {
   }
   return v;
 }
+// Release / acquire at GPU scope (lighter than __threadfence()'s fence.sc.gpu).
+PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 PS_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 // Greedy key: larger logit wins, equal logits -> lower index wins (reading R12).

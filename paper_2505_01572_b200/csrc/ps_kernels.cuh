@@ -86,6 +86,8 @@ struct GemmParams {
   float* out; int ld_out;
   // stream-K fixup
   float* ws; unsigned* counters;
+  unsigned long long* dbg;         // optional per-CTA %globaltimer trace [grid][4]
+  int test_mode;                   // test hooks: bit0 skip TMA, bit1 skip MMA
 };
 
 // ------------------------------------------------------------------ stream-K partition
@@ -103,7 +105,8 @@ struct GemmSmem {
   static constexpr int kOffScratch = kOffX + STAGES * kXBytes;
   static constexpr int kOffRed = kOffScratch + kScratch;            // u64 [4][RP]
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;             // float [RP]
-  static constexpr int kOffBar = (kOffRstd + RP * 4 + 7) / 8 * 8;   // full, empty, tfull[2], tempty[2]
+  static constexpr int kOffKvRow = kOffRstd + RP * 4;               // long long [RP]
+  static constexpr int kOffBar = kOffKvRow + RP * 8;                // full, empty, tfull[2], tempty[2]
   static constexpr int kOffMisc = kOffBar + (2 * STAGES + 4) * 8;   // tmem base, flag
   static constexpr int kBytes = kOffMisc + 16 + 1024;               // + alignment slack
 };
@@ -114,8 +117,15 @@ PS_DEV void load_acc(uint32_t taddr, float* v) {
   if constexpr (RP == 32) tmem_ld16(taddr + 16, v + 16);
 }
 
+// 192 threads: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-5
+// epilogue (TMEM lane quarter = warp % 4).  <= ~110 KB smem and <= 170 regs so
+// two CTAs fit per SM: under programmatic dependent launch the next kernel's
+// CTA becomes resident beside this one and streams its first weight tiles
+// while this kernel's tail (stream-K fixup, epilogue) is still running.
+constexpr int kGemmThreads = 192;
+
 template <int RP, int STAGES, bool GU>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kGemmThreads, 2)
 gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
             const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mX,
             const __grid_constant__ GemmParams p) {
@@ -127,6 +137,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
   float* scratch = (float*)(smem + L::kOffScratch);
   unsigned long long* red = (unsigned long long*)(smem + L::kOffRed);
   float* rstd = (float*)(smem + L::kOffRstd);
+  long long* kvrow = (long long*)(smem + L::kOffKvRow);
   uint64_t* full = (uint64_t*)(smem + L::kOffBar);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -141,6 +152,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
   const int G = gridDim.x, c = blockIdx.x;
   const long long u_begin = sk_begin(U, G, c), u_end = sk_begin(U, G, c + 1);
   const int kbt = p.kb_total;
+  const unsigned long long t_entry = (p.dbg != nullptr && threadIdx.x == 0) ? globaltimer() : 0ull;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mA0);
@@ -151,12 +163,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
+  if (p.dbg != nullptr && threadIdx.x == 0) p.dbg[c * 4 + 0] = t_entry;
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -183,21 +196,29 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
       const int pre = (int)(n_units < STAGES ? n_units : STAGES);
       // Weights do not depend on the previous kernel: stream them before the
       // grid dependency resolves (PDL), then fetch the activation tiles.
+      const bool no_tma = p.test_mode & 1;
       for (int i = 0; i < pre; ++i) {
+        if (no_tma) { mbar_arrive(&full[i]); continue; }
         mbar_arrive_expect_tx(&full[i], L::kABytes + L::kXBytes);
         load_A(u_begin + i, i);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) load_X(u_begin + i, i);
+      if (!no_tma)
+        for (int i = 0; i < pre; ++i) load_X(u_begin + i, i);
       int stage = 0;
       uint32_t phase = 1;   // ring wrapped once by the prologue (if pre == STAGES)
       for (long long u = u_begin + pre; u < u_end; ++u) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], L::kABytes + L::kXBytes);
-        load_A(u, stage);
-        load_X(u, stage);
+        if (no_tma) {
+          mbar_arrive(&full[stage]);
+        } else {
+          mbar_arrive_expect_tx(&full[stage], L::kABytes + L::kXBytes);
+          load_A(u, stage);
+          load_X(u, stage);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (p.dbg != nullptr) p.dbg[c * 4 + 1] = globaltimer();
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
@@ -219,34 +240,66 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * L::kABytes);
           const uint32_t x0 = smem_u32(sX + stage * L::kXBytes);
+          if (p.test_mode & 2) {
+            mbar_arrive(&empty[stage]);
+          } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
-                     (u != seg_begin || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
+                       (u != seg_begin || k > 0) ? 1u : 0u);
+            mma_commit(&empty[stage]);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if (p.test_mode & 2) mbar_arrive(&tfull[acc]);
+        else mma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+      if (p.dbg != nullptr) p.dbg[c * 4 + 2] = globaltimer();
     }
-  } else if (warp >= 4) {
+  } else {
     // ================= epilogue (128 threads, TMEM lane = e) =================
-    const int e = threadIdx.x - 128;
-    const int quarter = warp - 4;
+    const int quarter = warp & 3;
+    const int e = quarter * 32 + lane;
     pdl_wait();
     const StepIn* st = p.step;
     const int R = st->R;
     const int pos0 = st->pos0;
+    // rstd_r from the producer's sum-of-squares slots: 128/RP threads per row
+    // each load their slots in one batch; partials are combined in fixed order.
+    {
+      constexpr int TPR = 128 / RP;            // threads per row
+      constexpr int MAXS = 64 / TPR;           // slots per thread (ss_n <= 64, d <= 8192)
+      const int row = e % RP, part = e / RP;
+      float sv[MAXS];
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        const int j = part + k * TPR;
+        sv[k] = (p.ss_in != nullptr && j < p.ss_n) ? p.ss_in[row * p.ss_ld + j] : 0.f;
+      }
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) s += sv[k];
+      scratch[part * RP + row] = s;
+    }
+    named_bar(1, 128);
     if (e < RP) {
       float r_ = 1.0f;
       if (p.ss_in != nullptr) {
         float s = 0.f;
-        for (int j = 0; j < p.ss_n; ++j) s += p.ss_in[e * p.ss_ld + j];
+        for (int k = 0; k < 128 / RP; ++k) s += scratch[k * RP + e];
         r_ = rsqrtf(s * p.inv_d + p.eps);
       }
       rstd[e] = r_;
+      if (p.mode == EPI_QKV) {   // element offset of row e's KV slot (page + slot), head-independent
+        long long off = 0;
+        if (e < R) {
+          const int pos = pos0 + e;
+          off = (long long)p.page_table[pos / p.page_size] * p.page_stride + (long long)(pos % p.page_size) * p.hd;
+        }
+        kvrow[e] = off;
+      }
     }
     named_bar(1, 128);
     int acc = 0;
@@ -267,45 +320,82 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
       u = seg_end;
 
       // ---- stream-K fixup: deterministic, fixed segment order ----
+      // Partials are laid out [tile][seg][lane e][RP] so every thread moves
+      // RP contiguous floats with 16-byte accesses; the reducing CTA issues all
+      // of a segment's loads before using them (latency, not bandwidth, bound).
       const long long tile_u0 = (long long)t * kbt;
       if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
         const int first = sk_owner(U, G, tile_u0);
         const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
         const int seg = c - first;
-        float* wsp = p.ws + (size_t)(t * p.maxseg) * RP * 128;
+        float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
+        constexpr int V4 = RP / 4;
 #pragma unroll
-        for (int r = 0; r < RP; ++r) __stcg(&wsp[((size_t)seg * RP + r) * 128 + e], v[r]);
-        __threadfence();
+        for (int j = 0; j < V4; ++j)
+          __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        fence_acq_rel_gpu();
         named_bar(1, 128);
         if (e == 0) *flag = (atomicAdd(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
         named_bar(1, 128);
         const int last = *flag;
         named_bar(1, 128);
         if (!last) continue;
-        __threadfence();
+        fence_acq_rel_gpu();
+        float acc_r[RP];
 #pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          float s = 0.f;
-          for (int q = 0; q < nseg; ++q) s += (q == seg) ? v[r] : __ldcg(&wsp[((size_t)q * RP + r) * 128 + e]);
-          v[r] = s;
+        for (int r = 0; r < RP; ++r) acc_r[r] = 0.f;
+        constexpr int NIF = RP == 16 ? 2 : 1;   // segments with loads in flight at once
+        for (int q0 = 0; q0 < nseg; q0 += NIF) {
+          float4 w4[NIF][V4];
+#pragma unroll
+          for (int h = 0; h < NIF; ++h) {
+            const int q = q0 + h;
+            if (q == seg) {
+#pragma unroll
+              for (int j = 0; j < V4; ++j) w4[h][j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else if (q < nseg) {
+#pragma unroll
+              for (int j = 0; j < V4; ++j) w4[h][j] = __ldcg(&wsp[((size_t)q * 128 + e) * V4 + j]);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < NIF; ++h) {
+            if (q0 + h < nseg) {
+#pragma unroll
+              for (int j = 0; j < V4; ++j) {
+                acc_r[4 * j] += w4[h][j].x;
+                acc_r[4 * j + 1] += w4[h][j].y;
+                acc_r[4 * j + 2] += w4[h][j].z;
+                acc_r[4 * j + 3] += w4[h][j].w;
+              }
+            }
+          }
         }
+#pragma unroll
+        for (int r = 0; r < RP; ++r) v[r] = acc_r[r];
         if (e == 0) p.counters[t] = 0u;
       }
 
-      // ---- fused epilogues ----
+      // ---- fused epilogues (global loads batched ahead of use) ----
       if (p.mode == EPI_STORE) {
         const int f = t * 128 + e;
-        if (f < p.N)
-          for (int r = 0; r < R; ++r) p.out[(size_t)r * p.ld_out + f] = v[r];
+        if (f < p.N) {
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r < R) p.out[(size_t)r * p.ld_out + f] = v[r];
+        }
       } else if (p.mode == EPI_RESID) {
         const int f = t * 128 + e;
         const bool ok = f < p.N;
         const float g = ok ? __bfloat162float(p.gain[f]) : 0.f;
+        float xo[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) xo[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
 #pragma unroll
         for (int r = 0; r < RP; ++r) {
           float sq = 0.f;
           if (r < R && ok) {
-            const float xn = p.x[(size_t)r * p.ld_x + f] + v[r];
+            const float xn = xo[r] + v[r];
             p.x[(size_t)r * p.ld_x + f] = xn;
             p.xg[(size_t)r * p.ld_xg + f] = __float2bfloat16(xn * g);
             sq = xn * xn;
@@ -324,12 +414,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         named_bar(1, 128);
         if (e < 64) {
           const int f = t * 64 + e;
-          if (f < p.N)
-            for (int r = 0; r < R; ++r) {
-              const float gt = scratch[e * (RP + 1) + r];
-              const float up = scratch[(e + 64) * (RP + 1) + r];
-              p.h[(size_t)r * p.ld_h + f] = __float2bfloat16(gt / (1.0f + __expf(-gt)) * up);
+          if (f < p.N) {
+#pragma unroll
+            for (int r = 0; r < RP; ++r) {
+              if (r < R) {
+                const float gt = scratch[e * (RP + 1) + r];
+                const float up = scratch[(e + 64) * (RP + 1) + r];
+                p.h[(size_t)r * p.ld_h + f] = __float2bfloat16(gt / (1.0f + __expf(-gt)) * up);
+              }
             }
+          }
         }
         named_bar(1, 128);
       } else if (p.mode == EPI_QKV) {
@@ -342,31 +436,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         const int hd = p.hd, half = hd >> 1;
         const int i = f % hd;
         if (kind < 2) {   // rotate-half RoPE at absolute positions pos0 + r
+          const int j = i & (half - 1);
+          float2 cs[RP];
+#pragma unroll
+          for (int r = 0; r < RP; ++r) cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * half + j] : make_float2(1.f, 0.f);
 #pragma unroll
           for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r];
           named_bar(1, 128);
           const int pe = e ^ half;
-          const int j = i & (half - 1);
-          for (int r = 0; r < R; ++r) {
-            const float2 cs = p.rope_cs[(size_t)(pos0 + r) * half + j];
+#pragma unroll
+          for (int r = 0; r < RP; ++r) {
             const float pv = scratch[pe * (RP + 1) + r];
-            v[r] = (i < half) ? (v[r] * cs.x - pv * cs.y) : (v[r] * cs.x + pv * cs.y);
+            v[r] = (i < half) ? (v[r] * cs[r].x - pv * cs[r].y) : (v[r] * cs[r].x + pv * cs[r].y);
           }
           named_bar(1, 128);
         }
         if (f < nrows) {
           if (kind == 0) {
-            for (int r = 0; r < R; ++r) p.q[(size_t)r * p.ld_q + f] = v[r];
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (r < R) p.q[(size_t)r * p.ld_q + f] = v[r];
           } else {
             const int kh = f / hd;
-            for (int r = 0; r < R; ++r) {
-              const int pos = pos0 + r;
-              const long long page = p.page_table[pos / p.page_size];
-              const int slot = pos % p.page_size;
-              const size_t off = (size_t)page * p.page_stride +
-                                 ((size_t)((p.layer * 2 + (kind - 1)) * p.hkv + kh) * p.page_size + slot) * hd + i;
-              p.kv[off] = __float2bfloat16(v[r]);
-            }
+            const size_t head_off = ((size_t)((p.layer * 2 + (kind - 1)) * p.hkv + kh) * p.page_size) * hd + i;
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (r < R) p.kv[(size_t)kvrow[r] + head_off] = __float2bfloat16(v[r]);
           }
         }
       } else {  // EPI_LMHEAD
@@ -393,7 +488,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
+  if (p.dbg != nullptr && threadIdx.x == 0) p.dbg[c * 4 + 3] = globaltimer();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
 }
 
 // ------------------------------------------------------------------ embed (a1-a3)
@@ -433,119 +529,245 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Embe
 }
 
 // ------------------------------------------------------------------ attention (a6)
+// Split-KV decode attention, GQA-grouped.  Work item = (KV head kh, row block
+// rb of up to 128 query rows, chunk c of 64 keys at absolute positions
+// [64c, 64c+64)).  Query row m of a block is (window row r = m / g, query head
+// kh*g + m % g), so one K/V chunk read serves all g heads that share it.
+// S = Q K^T and O = P V run on the tensor cores (mma.sync m16n8k16 bf16 ->
+// fp32; one warp per 16 rows), softmax in fp32 in the exp2 domain.  Chunk
+// partials (m, l, O) go to a workspace; the last CTA of each (kh, rb)
+// combines them in chunk order (deterministic; a row's result does not depend
+// on R because chunks sit at absolute positions and fully masked chunks
+// contribute exact zeros).
 struct AttnParams {
   const StepIn* step;
   const float* q; int ld_q;
   const __nv_bfloat16* kv; const int32_t* page_table; int page_size; long long page_stride;
   int layer, hkv, H, hd;
-  float scale;
-  int max_chunks;
-  float* ws_o;     // [H][max_chunks][kMaxRows][hd]
-  float* ws_ml;    // [H][max_chunks][kMaxRows][2]
-  unsigned* counters;
+  float scale_log2;                // log2(e) / sqrt(hd)
+  int max_chunks, max_rb;
+  float* ws_o;                     // [hkv][max_rb][max_chunks][128][hd]
+  float* ws_ml;                    // [hkv][max_rb][max_chunks][128][2]
+  unsigned* counters;              // [hkv][max_rb]
   __nv_bfloat16* out; int ld_out;
 };
 
-// One work item = (query head h, chunk c of kAttnChunk keys at absolute
-// positions [c*64, c*64+64)).  Scores, softmax and P·V in fp32 on CUDA cores.
-constexpr int kAttnSmem = 2 * kAttnChunk * 128 * 2 + kMaxRows * 128 * 4 + kMaxRows * (kAttnChunk + 1) * 4 + 16;
+constexpr int kAttnRowsPerBlock = 128;
+constexpr int kAttnPad = 8;        // smem row padding (bf16 elements): conflict-free ldmatrix
+constexpr int kAttnSmem = (kAttnRowsPerBlock + 2 * kAttnChunk) * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64;
 
-__global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnParams p) {
+PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+PS_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+PS_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+PS_DEV uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(16) uint8_t attn_smem[];
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sV = sK + kAttnChunk * 128;
-  float* sQ = reinterpret_cast<float*>(sV + kAttnChunk * 128);
-  float* sP = sQ + kMaxRows * 128;
-  int& s_last = *reinterpret_cast<int*>(sP + kMaxRows * (kAttnChunk + 1));
+  constexpr int LD = HD + kAttnPad;                     // smem row stride (elements)
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
+  __nv_bfloat16* sK = sQ + kAttnRowsPerBlock * LD;
+  __nv_bfloat16* sV = sK + kAttnChunk * LD;
+  float* sM = reinterpret_cast<float*>(sV + kAttnChunk * LD);   // combine scratch [64]
+  int& s_last = *reinterpret_cast<int*>(sM + 3 * 64);
   pdl_wait();
   pdl_launch_dependents();
-  const int R = p.step->R, pos0 = p.step->pos0;
+  const StepIn* st = p.step;
+  const int R = st->R, pos0 = st->pos0;
+  const int g = p.H / p.hkv;
+  const int rows = R * g;
+  const int n_rb = (rows + kAttnRowsPerBlock - 1) / kAttnRowsPerBlock;
   const int n_keys = pos0 + R;
   const int nchunks = (n_keys + kAttnChunk - 1) / kAttnChunk;
-  const int hd = p.hd, g = p.H / p.hkv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int item = blockIdx.x; item < p.H * nchunks; item += gridDim.x) {
-    const int h = item / nchunks, c = item % nchunks, kh = h / g;
+  const int n_items = p.hkv * n_rb * nchunks;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int c = item % nchunks;
+    const int rb = (item / nchunks) % n_rb;
+    const int kh = item / (nchunks * n_rb);
+    const int m0 = rb * kAttnRowsPerBlock;
+    const int mrows = min(kAttnRowsPerBlock, rows - m0);
     const int k0 = c * kAttnChunk;
     const int nk = min(kAttnChunk, n_keys - k0);
-    // K/V chunk: one page holds page_size >= 64 consecutive positions.
-    const int page = p.page_table[k0 / p.page_size];
+    // ---- stage K/V chunk (one page run of 64 positions) and the Q rows (bf16, pre-scaled)
+    const long long page = p.page_table[k0 / p.page_size];
     const int slot0 = k0 % p.page_size;
     const __nv_bfloat16* Kp = p.kv + (size_t)page * p.page_stride +
-                              ((size_t)((p.layer * 2 + 0) * p.hkv + kh) * p.page_size + slot0) * hd;
+                              ((size_t)((p.layer * 2 + 0) * p.hkv + kh) * p.page_size + slot0) * HD;
     const __nv_bfloat16* Vp = p.kv + (size_t)page * p.page_stride +
-                              ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * hd;
-    const int nvec = nk * hd / 8;
-    for (int i = tid; i < nvec; i += 128) {
-      reinterpret_cast<uint4*>(sK)[i] = reinterpret_cast<const uint4*>(Kp)[i];
-      reinterpret_cast<uint4*>(sV)[i] = reinterpret_cast<const uint4*>(Vp)[i];
-    }
-    for (int i = tid; i < R * hd; i += 128) sQ[i] = p.q[(size_t)(i / hd) * p.ld_q + h * hd + (i % hd)];
-    __syncthreads();
-    for (int i = tid; i < R * kAttnChunk; i += 128) {
-      const int r = i / kAttnChunk, j = i % kAttnChunk;
-      float s = -INFINITY;
-      if (j < nk && k0 + j <= pos0 + r) {   // causal: key position <= query position
-        s = 0.f;
-        const float* qr = sQ + r * hd;
-        const __nv_bfloat16* kj = sK + j * hd;
-        for (int d = 0; d < hd; d += 2) {
-          const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kj + d));
-          s = fmaf(qr[d], kf.x, s);
-          s = fmaf(qr[d + 1], kf.y, s);
-        }
-        s *= p.scale;
+                              ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
+    constexpr int VPR = HD / 8;                          // 16-byte vectors per row
+    for (int i = tid; i < kAttnChunk * VPR; i += 256) {
+      const int row = i / VPR, cv = i % VPR;
+      uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (row < nk) {
+        kk = reinterpret_cast<const uint4*>(Kp + (size_t)row * HD)[cv];
+        vv = reinterpret_cast<const uint4*>(Vp + (size_t)row * HD)[cv];
       }
-      sP[r * (kAttnChunk + 1) + j] = s;
+      *reinterpret_cast<uint4*>(sK + row * LD + cv * 8) = kk;
+      *reinterpret_cast<uint4*>(sV + row * LD + cv * 8) = vv;
+    }
+    const int nwarps_used = (mrows + 15) / 16;
+    for (int i = tid; i < nwarps_used * 16 * (HD / 4); i += 256) {
+      const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
+      float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < mrows) {
+        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+        qv = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
+      }
+      uint2 pk = make_uint2(pack_bf16(qv.x * p.scale_log2, qv.y * p.scale_log2),
+                            pack_bf16(qv.z * p.scale_log2, qv.w * p.scale_log2));
+      *reinterpret_cast<uint2*>(sQ + m * LD + d4) = pk;
     }
     __syncthreads();
-    float* mlp = p.ws_ml + ((size_t)(h * p.max_chunks + c) * kMaxRows) * 2;
-    for (int r = warp; r < R; r += 4) {
-      float* row = sP + r * (kAttnChunk + 1);
-      const float a0 = row[lane], a1 = row[lane + 32];
-      float m = fmaxf(a0, a1);
+    if (warp < nwarps_used) {
+      // ---- S = Q K^T for this warp's 16 rows x 64 keys
+      float sacc[8][4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      float e0 = 0.f, e1 = 0.f;
-      if (m != -INFINITY) { e0 = __expf(a0 - m); e1 = __expf(a1 - m); }
-      row[lane] = e0;
-      row[lane + 32] = e1;
-      const float l = warp_sum(e0 + e1);
-      if (lane == 0) { mlp[r * 2 + 0] = m; mlp[r * 2 + 1] = l; }
-    }
-    __syncthreads();
-    if (tid < hd) {
-      float* op = p.ws_o + ((size_t)(h * p.max_chunks + c) * kMaxRows) * hd;
-      for (int r = 0; r < R; ++r) {
-        const float* pr = sP + r * (kAttnChunk + 1);
-        float acc = 0.f;
-        for (int j = 0; j < nk; ++j) acc = fmaf(pr[j], __bfloat162float(sV[j * hd + tid]), acc);
-        __stcg(&op[(size_t)r * hd + tid], acc);
+      for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+      const uint32_t qbase = smem_u32(sQ + (warp * 16 + (lane % 16)) * LD + (lane / 16) * 8);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        uint32_t a[4];
+        ldsm_x4(qbase + kk * 32, a[0], a[1], a[2], a[3]);
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {   // pairs of 8-key n-tiles
+          const int krow = jp * 16 + (lane & 7) + ((lane >> 4) << 3);
+          const int kcol = kk * 16 + ((lane >> 3) & 1) * 8;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(smem_u32(sK + krow * LD + kcol), b0, b1, b2, b3);
+          mma16816(sacc[2 * jp], a, b0, b1);
+          mma16816(sacc[2 * jp + 1], a, b2, b3);
+        }
+      }
+      // ---- causal / length mask and chunk-local softmax (rows lane/4 and lane/4+8)
+      float mrow[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int m = warp * 16 + (lane >> 2) + hr * 8;
+        const int qpos = pos0 + (m0 + m) / g;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int key = j * 8 + (lane & 3) * 2 + e2;
+            float& sv = sacc[j][hr * 2 + e2];
+            if (key >= nk || k0 + key > qpos) sv = -INFINITY;
+            mrow[hr] = fmaxf(mrow[hr], sv);
+          }
+        mrow[hr] = fmaxf(mrow[hr], __shfl_xor_sync(0xffffffffu, mrow[hr], 1));
+        mrow[hr] = fmaxf(mrow[hr], __shfl_xor_sync(0xffffffffu, mrow[hr], 2));
+      }
+      float lrow[2] = {0.f, 0.f};
+      uint32_t pa[4][4];                 // P as A fragments, 4 k-blocks of 16 keys
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float pv[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int hr = q4 >> 1;
+          pv[q4] = (mrow[hr] == -INFINITY) ? 0.f : exp2f(sacc[j][q4] - mrow[hr]);
+          lrow[hr] += pv[q4];
+        }
+        const int kb = j >> 1, half2 = j & 1;
+        pa[kb][half2 * 2 + 0] = pack_bf16(pv[0], pv[1]);
+        pa[kb][half2 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+      }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 1);
+        lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 2);
+      }
+      // ---- O = P V  (16 rows x HD)
+      float oacc[HD / 8][4];
+#pragma unroll
+      for (int n = 0; n < HD / 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+#pragma unroll
+        for (int np = 0; np < HD / 16; ++np) {
+          const int vrow = kb * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int vcol = np * 16 + (lane >> 4) * 8;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(smem_u32(sV + vrow * LD + vcol), b0, b1, b2, b3);
+          mma16816(oacc[2 * np], pa[kb], b0, b1);
+          mma16816(oacc[2 * np + 1], pa[kb], b2, b3);
+        }
+      }
+      // ---- chunk partials -> workspace
+      const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kAttnRowsPerBlock);
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int m = warp * 16 + (lane >> 2) + hr * 8;
+        float* op = p.ws_o + (base + m) * HD;
+#pragma unroll
+        for (int n = 0; n < HD / 8; ++n)
+          __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2),
+                 make_float2(oacc[n][hr * 2], oacc[n][hr * 2 + 1]));
+        if ((lane & 3) == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[hr], lrow[hr]));
       }
     }
-    __threadfence();
+    fence_acq_rel_gpu();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&p.counters[h], 1u) == (unsigned)(nchunks - 1);
+    if (tid == 0) s_last = atomicAdd(&p.counters[kh * p.max_rb + rb], 1u) == (unsigned)(nchunks - 1);
     __syncthreads();
     if (s_last) {
-      __threadfence();
-      if (tid < hd) {
-        for (int r = 0; r < R; ++r) {
-          float M = -INFINITY;
-          for (int cc = 0; cc < nchunks; ++cc)
-            M = fmaxf(M, __ldcg(&p.ws_ml[((size_t)(h * p.max_chunks + cc) * kMaxRows + r) * 2]));
-          float O = 0.f, Lsum = 0.f;
-          for (int cc = 0; cc < nchunks; ++cc) {
-            const size_t base = (size_t)(h * p.max_chunks + cc) * kMaxRows + r;
-            const float mc = __ldcg(&p.ws_ml[base * 2]);
-            const float sc = (mc == -INFINITY) ? 0.f : __expf(mc - M);
-            Lsum += sc * __ldcg(&p.ws_ml[base * 2 + 1]);
-            O += sc * __ldcg(&p.ws_o[base * hd + tid]);
-          }
-          p.out[(size_t)r * p.ld_out + h * hd + tid] = __float2bfloat16(O / Lsum);
+      fence_acq_rel_gpu();
+      // combine: per row M = max_c m_c, L = sum_c 2^(m_c-M) l_c, O = sum_c 2^(m_c-M) O_c / L
+      const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
+      for (int m = warp; m < mrows; m += 8) {
+        float M = -INFINITY;
+        for (int cc = lane; cc < nchunks; cc += 32)
+          M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        float Lp = 0.f;
+        for (int cc = lane; cc < nchunks; cc += 32) {
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2));
+          Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
         }
+        // fixed-order sum over chunks: lanes hold chunk-strided partials, reduce by tree
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
+        const float invL = 1.0f / Lp;
+        constexpr int DPL = HD / 32;   // dims per lane
+        float acc[DPL];
+#pragma unroll
+        for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
+#pragma unroll 8
+        for (int cc = 0; cc < nchunks; ++cc) {
+          const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2);
+          const float sc = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
+          const float* op = p.ws_o + ((rbase + cc) * kAttnRowsPerBlock + m) * HD + lane * DPL;
+          if constexpr (DPL == 4) {
+            const float4 o4 = __ldcg(reinterpret_cast<const float4*>(op));
+            acc[0] += sc * o4.x; acc[1] += sc * o4.y; acc[2] += sc * o4.z; acc[3] += sc * o4.w;
+          } else {
+            const float2 o2 = __ldcg(reinterpret_cast<const float2*>(op));
+            acc[0] += sc * o2.x; acc[1] += sc * o2.y;
+          }
+        }
+        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+        __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
+#pragma unroll
+        for (int t = 0; t < DPL; ++t) dst[t] = __float2bfloat16(acc[t] * invL);
       }
-      if (tid == 0) p.counters[h] = 0u;
+      if (tid == 0) p.counters[kh * p.max_rb + rb] = 0u;
     }
     __syncthreads();
   }

@@ -72,8 +72,9 @@ static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64
 }
 
 // ============================================================================ GEMM launch
-constexpr int kStages = 8;
+constexpr int kStages = 4;   // x (16 KB weights + RP*128 B activations): 2 CTAs/SM
 static int g_num_sms = 0;
+static int g_test_flags = 0;   // test hooks only: bit0 = launch without PDL
 
 template <int RP, bool GU>
 static ps_status gemm_setup_attr() {
@@ -108,13 +109,13 @@ static ps_status launch_gemm(int RP, bool GU, const CUtensorMap& a0, const CUten
                              const CUtensorMap& x, const GemmParams& p, int grid, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kGemmThreads);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (g_test_flags & 1) ? 0 : 1;
   cudaError_t e;
   if (RP == 16 && !GU) {
     cfg.dynamicSmemBytes = GemmSmem<16, kStages, false>::kBytes;
@@ -166,7 +167,8 @@ static ps_status init_device_globals(int device) {
   if ((st = gemm_setup_attr<16, true>()) != PS_OK) return st;
   if ((st = gemm_setup_attr<32, false>()) != PS_OK) return st;
   if ((st = gemm_setup_attr<32, true>()) != PS_OK) return st;
-  CU_TRY(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+  CU_TRY(cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+  CU_TRY(cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
   return PS_OK;
 }
 
@@ -217,7 +219,7 @@ struct ps_stage {
   SynthParams h_syn{};
   int32_t* d_S = nullptr;
   int n_prompt = 0;
-  int ss_ld = 0, xg_ld = 0, max_chunks = 0, attn_grid = 0;
+  int ss_ld = 0, xg_ld = 0, max_chunks = 0, max_rb = 0, attn_grid = 0;
   GemmShape gs_qkv, gs_o, gs_gu, gs_d, gs_lm;
   int lm_tiles = 0;
   // graphs per (bucket, with_head)
@@ -302,10 +304,13 @@ static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
       AttnParams a{};
       a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
       a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
-      a.H = sh.n_heads; a.hd = sh.head_dim; a.scale = 1.0f / std::sqrt((float)sh.head_dim);
-      a.max_chunks = S->max_chunks; a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
+      a.H = sh.n_heads; a.hd = sh.head_dim; a.scale_log2 = 1.4426950408889634f / std::sqrt((float)sh.head_dim);
+      a.max_chunks = S->max_chunks; a.max_rb = S->max_rb;
+      a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
       a.out = S->att; a.ld_out = hq;
-      return launch_simple(attn_kernel, dim3(S->attn_grid), dim3(128), kAttnSmem, a, S->stream);
+      if (sh.head_dim == 128)
+        return launch_simple(attn_kernel<128>, dim3(S->attn_grid), dim3(256), kAttnSmem, a, S->stream);
+      return launch_simple(attn_kernel<64>, dim3(S->attn_grid), dim3(256), kAttnSmem, a, S->stream);
     }
     case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
       const LayerMaps& M = S->maps[l];
@@ -604,12 +609,17 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
   S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * S->lm_tiles * 8));
   // --- attention workspace
-  S->max_chunks = (S->max_seq + kAttnChunk - 1) / kAttnChunk;
-  S->attn_grid = std::min(sh.n_heads * S->max_chunks, 2 * n);
-  S_TRY(cudaMalloc(&S->attn_o, (size_t)sh.n_heads * S->max_chunks * kMaxRows * sh.head_dim * 4));
-  S_TRY(cudaMalloc(&S->attn_ml, (size_t)sh.n_heads * S->max_chunks * kMaxRows * 2 * 4));
-  S_TRY(cudaMalloc(&S->attn_counters, (size_t)sh.n_heads * 4));
-  S_TRY(cudaMemset(S->attn_counters, 0, (size_t)sh.n_heads * 4));
+  S->max_chunks = (S->max_seq + kMaxRows + kAttnChunk - 1) / kAttnChunk;
+  {
+    const int g = sh.n_heads / sh.n_kv_heads;
+    S->max_rb = (kMaxRows * g + kAttnRowsPerBlock - 1) / kAttnRowsPerBlock;
+  }
+  S->attn_grid = std::min(sh.n_kv_heads * S->max_rb * S->max_chunks, 2 * n);
+  const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * kAttnRowsPerBlock;
+  S_TRY(cudaMalloc(&S->attn_o, attn_rows * sh.head_dim * 4));
+  S_TRY(cudaMalloc(&S->attn_ml, attn_rows * 2 * 4));
+  S_TRY(cudaMalloc(&S->attn_counters, (size_t)sh.n_kv_heads * S->max_rb * 4));
+  S_TRY(cudaMemset(S->attn_counters, 0, (size_t)sh.n_kv_heads * S->max_rb * 4));
   // --- RoPE table
   {
     std::vector<float2> cs;
@@ -869,8 +879,8 @@ ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_
 }  // extern "C"
 
 // ============================================================================ test hooks
-extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                  void* stream) {
+static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                void* stream, int iters, float* ms_out, unsigned long long* dbg_host) {
   ps_status st;
   if (R < 1 || R > kMaxRows || K % 64 || N < 1) return fail(PS_E_INVALID, "bad test gemm shape");
   int dev = 0;
@@ -903,14 +913,72 @@ extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int3
   p.ld_out = N;
   p.ws = ws;
   p.counters = cnt;
-  st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  p.test_mode = g_test_flags >> 1;
+  unsigned long long* dbg = nullptr;
+  const int nl = iters > 0 ? iters : 1;
+  if (dbg_host) CU_TRY(cudaMalloc(&dbg, (size_t)nl * gs.grid * 4 * 8));
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  if (iters == 0) st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  p.dbg = dbg;
+  CU_TRY(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters && st == PS_OK; ++i) {
+    p.dbg = dbg ? dbg + (size_t)i * gs.grid * 4 : nullptr;
+    st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  }
+  CU_TRY(cudaEventRecord(e1, s));
   cudaError_t e = cudaStreamSynchronize(s);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (ms_out) *ms_out = ms / (iters > 0 ? iters : 1);
+  if (dbg_host && e == cudaSuccess) e = cudaMemcpy(dbg_host, dbg, (size_t)nl * gs.grid * 4 * 8, cudaMemcpyDeviceToHost);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (dbg) cudaFree(dbg);
   cudaFree(din);
   cudaFree(ws);
   cudaFree(cnt);
   if (st != PS_OK) return st;
   if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
   return PS_OK;
+}
+
+__global__ void empty_smem_kernel(int* p) {
+  extern __shared__ int sm_[];
+  if (threadIdx.x == 0 && p) sm_[0] = p[0];
+}
+
+extern "C" ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters,
+                                             int32_t flags, float* avg_ms) {
+  g_test_flags = flags;
+  CU_TRY(cudaFuncSetAttribute(empty_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
+  CU_TRY(cudaEventRecord(e0, 0));
+  for (int i = 0; i < iters; ++i) empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
+  CU_TRY(cudaEventRecord(e1, 0));
+  CU_TRY(cudaEventSynchronize(e1));
+  float ms;
+  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  *avg_ms = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return PS_OK;
+}
+
+extern "C" void ps_test_set_flags(int32_t flags) { g_test_flags = flags; }
+
+extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                  void* stream) {
+  return test_gemm_impl(W, X, out, N, K, R, stream, 0, nullptr, nullptr);
+}
+
+extern "C" ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                        void* stream, int32_t iters, float* avg_ms, uint64_t* cta_trace) {
+  return test_gemm_impl(W, X, out, N, K, R, stream, iters, avg_ms, (unsigned long long*)cta_trace);
 }
 
 extern "C" ps_status ps_time_kernel(ps_stage* S, int32_t kind, int32_t layer, int32_t iters, double* avg_ms) {
