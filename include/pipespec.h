@@ -100,6 +100,8 @@ typedef struct ps_stage_opts {
   int64_t kv_pool_bytes;
   void* stream;
   int32_t use_graphs;       /* 1: capture one CUDA graph per rows bucket      */
+  int32_t use_megakernel;   /* 1: whole forward as one persistent cooperative
+                               kernel (ps_mega.cuh); 0: one kernel per step   */
 } ps_stage_opts;
 
 typedef struct ps_stage ps_stage;

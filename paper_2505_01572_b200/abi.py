@@ -45,7 +45,7 @@ class Placement(C.Structure):
 class StageOpts(C.Structure):
     _fields_ = [("max_seq", C.c_int32), ("max_window", C.c_int32), ("page_size", C.c_int32),
                 ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_int64), ("stream", C.c_void_p),
-                ("use_graphs", C.c_int32)]
+                ("use_graphs", C.c_int32), ("use_megakernel", C.c_int32)]
 
 
 class StageInfo(C.Structure):

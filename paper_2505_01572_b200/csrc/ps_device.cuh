@@ -55,6 +55,11 @@ PS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int
       "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
+// TMA prefetch of one box into L2 only (no smem, no mbarrier).
+PS_DEV void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"((uint64_t)m), "r"(c0), "r"(c1)
+               : "memory");
+}
 // L2 eviction-priority policies (createpolicy encodings used by CUTLASS).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;

@@ -9,8 +9,8 @@
 //                          EPI_QKV    RMSNorm row scale + RoPE + paged KV append (a3,a5)
 //                          EPI_RESID  residual add + next RMSNorm operand + sumsq (a7,a9)
 //                          EPI_SWIGLU RMSNorm row scale + SiLU(gate)*up           (a8)
-//                          EPI_LMHEAD final-norm scale + fp32 logits + per-tile
-//                                     (max,idx) argmax partials                   (a10)
+//                          EPI_LMHEAD final-norm scale + fp32 logits (on request)
+//                                     + per-row greedy key by atomicMax       (a10)
 //                          EPI_STORE  plain fp32 store (unit tests)
 //   attn_kernel         a6: split-KV decode attention over the paged KV cache,
 //                        fixed 64-key chunks at absolute positions, causal inside the
@@ -38,7 +38,9 @@ struct StepIn {                    // written by the host before every forward
   int32_t syn_p0;                  // generated index predicted by row row0 (= n - n_prompt)
   int32_t syn_onpath;              // 1 iff the committed context is on the target stream
   int32_t row0;                    // first prediction row (rows before it are KV catch-up)
-  int32_t pad;
+  int32_t gen;                     // forwards so far on this stage (megakernel counter target)
+  int32_t gen_head;                // forwards with lm_head so far (targets of the head phases)
+  int32_t pad2[3];
   int32_t tokens[kMaxRows];        // row tokens: [pending, d_0, ..., d_{w-1}]
 };
 constexpr int kFlagLogits = 1;
@@ -115,6 +117,226 @@ template <int RP>
 PS_DEV void load_acc(uint32_t taddr, float* v) {
   tmem_ld16(taddr, v);
   if constexpr (RP == 32) tmem_ld16(taddr + 16, v + 16);
+}
+
+// Per-kernel (or per-phase) epilogue preparation: rstd_r from the producer's
+// sum-of-squares slots (128/RP threads per row load their slots in one batch;
+// partials combined in fixed order) and, for QKV, each row's KV slot offset.
+template <int RP>
+PS_DEV void epi_prepare(const GemmParams& p, int e, int R, int pos0, float* scratch, float* rstd, long long* kvrow) {
+  // rstd_r from the producer's sum-of-squares slots: 128/RP threads per row
+  // each load their slots in one batch; partials are combined in fixed order.
+  {
+    constexpr int TPR = 128 / RP;            // threads per row
+    constexpr int MAXS = 64 / TPR;           // slots per thread (ss_n <= 64, d <= 8192)
+    const int row = e % RP, part = e / RP;
+    float sv[MAXS];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+      const int j = part + k * TPR;
+      sv[k] = (p.ss_in != nullptr && j < p.ss_n) ? p.ss_in[row * p.ss_ld + j] : 0.f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) s += sv[k];
+    scratch[part * RP + row] = s;
+  }
+  named_bar(1, 128);
+  if (e < RP) {
+    float r_ = 1.0f;
+    if (p.ss_in != nullptr) {
+      float s = 0.f;
+      for (int k = 0; k < 128 / RP; ++k) s += scratch[k * RP + e];
+      r_ = rsqrtf(s * p.inv_d + p.eps);
+    }
+    rstd[e] = r_;
+    if (p.mode == EPI_QKV) {   // element offset of row e's KV slot (page + slot), head-independent
+      long long off = 0;
+      if (e < R) {
+        const int pos = pos0 + e;
+        off = (long long)p.page_table[pos / p.page_size] * p.page_stride + (long long)(pos % p.page_size) * p.hd;
+      }
+      kvrow[e] = off;
+    }
+  }
+  named_bar(1, 128);
+}
+
+// One accumulator segment of tile t (units [seg_begin, seg_end) of this CTA c
+// out of G): stream-K fixup (deterministic fixed segment order) then the
+// fused epilogue for the tile if this CTA completes it.  128 epilogue threads.
+template <int RP>
+PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long long seg_end, long long U, int G, int c,
+                        int kbt, float* v, int e, int lane, int quarter, int R, int pos0, float* scratch,
+                        unsigned long long* red, const float* rstd, const long long* kvrow, volatile int* flag) {
+  do {
+    // ---- stream-K fixup: deterministic, fixed segment order ----
+    // Partials are laid out [tile][seg][lane e][RP] so every thread moves
+    // RP contiguous floats with 16-byte accesses; the reducing CTA issues all
+    // of a segment's loads before using them (latency, not bandwidth, bound).
+    const long long tile_u0 = (long long)t * kbt;
+    if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
+      const int first = sk_owner(U, G, tile_u0);
+      const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
+      const int seg = c - first;
+      float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
+      constexpr int V4 = RP / 4;
+#pragma unroll
+      for (int j = 0; j < V4; ++j)
+        __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+      fence_acq_rel_gpu();
+      named_bar(1, 128);
+      if (e == 0) *flag = (atomicAdd(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
+      named_bar(1, 128);
+      const int last = *flag;
+      named_bar(1, 128);
+      if (!last) break;
+      fence_acq_rel_gpu();
+      float acc_r[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) acc_r[r] = 0.f;
+      constexpr int NIF = RP == 16 ? 2 : 1;   // segments with loads in flight at once
+      for (int q0 = 0; q0 < nseg; q0 += NIF) {
+        float4 w4[NIF][V4];
+#pragma unroll
+        for (int h = 0; h < NIF; ++h) {
+          const int q = q0 + h;
+          if (q == seg) {
+#pragma unroll
+            for (int j = 0; j < V4; ++j) w4[h][j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else if (q < nseg) {
+#pragma unroll
+            for (int j = 0; j < V4; ++j) w4[h][j] = __ldcg(&wsp[((size_t)q * 128 + e) * V4 + j]);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < NIF; ++h) {
+          if (q0 + h < nseg) {
+#pragma unroll
+            for (int j = 0; j < V4; ++j) {
+              acc_r[4 * j] += w4[h][j].x;
+              acc_r[4 * j + 1] += w4[h][j].y;
+              acc_r[4 * j + 2] += w4[h][j].z;
+              acc_r[4 * j + 3] += w4[h][j].w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) v[r] = acc_r[r];
+      if (e == 0) p.counters[t] = 0u;
+    }
+
+    // ---- fused epilogues (global loads batched ahead of use) ----
+    if (p.mode == EPI_STORE) {
+      const int f = t * 128 + e;
+      if (f < p.N) {
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          if (r < R) p.out[(size_t)r * p.ld_out + f] = v[r];
+      }
+    } else if (p.mode == EPI_RESID) {
+      const int f = t * 128 + e;
+      const bool ok = f < p.N;
+      const float g = ok ? __bfloat162float(p.gain[f]) : 0.f;
+      float xo[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) xo[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        float sq = 0.f;
+        if (r < R && ok) {
+          const float xn = xo[r] + v[r];
+          p.x[(size_t)r * p.ld_x + f] = xn;
+          p.xg[(size_t)r * p.ld_xg + f] = __float2bfloat16(xn * g);
+          sq = xn * xn;
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) scratch[quarter * RP + r] = sq;
+      }
+      named_bar(1, 128);
+      if (e < R)
+        p.ss_out[(size_t)e * p.ss_out_ld + t] =
+            ((scratch[0 * RP + e] + scratch[1 * RP + e]) + scratch[2 * RP + e]) + scratch[3 * RP + e];
+      named_bar(1, 128);
+    } else if (p.mode == EPI_SWIGLU) {
+#pragma unroll
+      for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r] * rstd[r];
+      named_bar(1, 128);
+      if (e < 64) {
+        const int f = t * 64 + e;
+        if (f < p.N) {
+#pragma unroll
+          for (int r = 0; r < RP; ++r) {
+            if (r < R) {
+              const float gt = scratch[e * (RP + 1) + r];
+              const float up = scratch[(e + 64) * (RP + 1) + r];
+              p.h[(size_t)r * p.ld_h + f] = __float2bfloat16(gt / (1.0f + __expf(-gt)) * up);
+            }
+          }
+        }
+      }
+      named_bar(1, 128);
+    } else if (p.mode == EPI_QKV) {
+      int kind, f, nrows;
+      if (t < p.t1) { kind = 0; f = t * 128 + e; nrows = p.nq; }
+      else if (t < p.t2) { kind = 1; f = (t - p.t1) * 128 + e; nrows = p.nk; }
+      else { kind = 2; f = (t - p.t2) * 128 + e; nrows = p.nk; }
+#pragma unroll
+      for (int r = 0; r < RP; ++r) v[r] *= rstd[r];
+      const int hd = p.hd, half = hd >> 1;
+      const int i = f % hd;
+      if (kind < 2) {   // rotate-half RoPE at absolute positions pos0 + r
+        const int j = i & (half - 1);
+        float2 cs[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * half + j] : make_float2(1.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r];
+        named_bar(1, 128);
+        const int pe = e ^ half;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          const float pv = scratch[pe * (RP + 1) + r];
+          v[r] = (i < half) ? (v[r] * cs[r].x - pv * cs[r].y) : (v[r] * cs[r].x + pv * cs[r].y);
+        }
+        named_bar(1, 128);
+      }
+      if (f < nrows) {
+        if (kind == 0) {
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r < R) p.q[(size_t)r * p.ld_q + f] = v[r];
+        } else {
+          const int kh = f / hd;
+          const size_t head_off = ((size_t)((p.layer * 2 + (kind - 1)) * p.hkv + kh) * p.page_size) * hd + i;
+#pragma unroll
+          for (int r = 0; r < RP; ++r)
+            if (r < R) p.kv[(size_t)kvrow[r] + head_off] = __float2bfloat16(v[r]);
+        }
+      }
+    } else {  // EPI_LMHEAD: logits (on request) + per-row greedy key, atomicMax (order-free, exact)
+      const int f = t * 128 + e;
+      const bool ok = f < p.N;
+      const bool want = p.logits != nullptr && (p.step->flags & kFlagLogits);
+#pragma unroll
+      for (int r = 0; r < RP; ++r) {
+        const float z = v[r] * rstd[r];
+        if (want && ok && r < R) p.logits[(size_t)r * p.ld_logits + f] = z;
+        unsigned long long k = ok ? argmax_key(z, (uint32_t)f) : 0ull;
+        k = warp_max_u64(k);
+        if (lane == 0) red[quarter * RP + r] = k;
+      }
+      named_bar(1, 128);
+      if (e < R) {
+        unsigned long long k = red[e];
+        for (int q = 1; q < 4; ++q) k = red[q * RP + e] > k ? red[q * RP + e] : k;
+        atomicMax(&p.amax[e], k);
+      }
+      named_bar(1, 128);
+    }
+
+  } while (0);
 }
 
 // 192 threads: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-5
@@ -266,42 +488,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
     const StepIn* st = p.step;
     const int R = st->R;
     const int pos0 = st->pos0;
-    // rstd_r from the producer's sum-of-squares slots: 128/RP threads per row
-    // each load their slots in one batch; partials are combined in fixed order.
-    {
-      constexpr int TPR = 128 / RP;            // threads per row
-      constexpr int MAXS = 64 / TPR;           // slots per thread (ss_n <= 64, d <= 8192)
-      const int row = e % RP, part = e / RP;
-      float sv[MAXS];
-#pragma unroll
-      for (int k = 0; k < MAXS; ++k) {
-        const int j = part + k * TPR;
-        sv[k] = (p.ss_in != nullptr && j < p.ss_n) ? p.ss_in[row * p.ss_ld + j] : 0.f;
-      }
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < MAXS; ++k) s += sv[k];
-      scratch[part * RP + row] = s;
-    }
-    named_bar(1, 128);
-    if (e < RP) {
-      float r_ = 1.0f;
-      if (p.ss_in != nullptr) {
-        float s = 0.f;
-        for (int k = 0; k < 128 / RP; ++k) s += scratch[k * RP + e];
-        r_ = rsqrtf(s * p.inv_d + p.eps);
-      }
-      rstd[e] = r_;
-      if (p.mode == EPI_QKV) {   // element offset of row e's KV slot (page + slot), head-independent
-        long long off = 0;
-        if (e < R) {
-          const int pos = pos0 + e;
-          off = (long long)p.page_table[pos / p.page_size] * p.page_stride + (long long)(pos % p.page_size) * p.hd;
-        }
-        kvrow[e] = off;
-      }
-    }
-    named_bar(1, 128);
+    epi_prepare<RP>(p, e, R, pos0, scratch, rstd, kvrow);
     int acc = 0;
     uint32_t acc_phase = 0;
     long long u = u_begin;
@@ -319,170 +506,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
       if (acc == 0) acc_phase ^= 1;
       u = seg_end;
 
-      // ---- stream-K fixup: deterministic, fixed segment order ----
-      // Partials are laid out [tile][seg][lane e][RP] so every thread moves
-      // RP contiguous floats with 16-byte accesses; the reducing CTA issues all
-      // of a segment's loads before using them (latency, not bandwidth, bound).
-      const long long tile_u0 = (long long)t * kbt;
-      if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
-        const int first = sk_owner(U, G, tile_u0);
-        const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
-        const int seg = c - first;
-        float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
-        constexpr int V4 = RP / 4;
-#pragma unroll
-        for (int j = 0; j < V4; ++j)
-          __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-        fence_acq_rel_gpu();
-        named_bar(1, 128);
-        if (e == 0) *flag = (atomicAdd(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
-        named_bar(1, 128);
-        const int last = *flag;
-        named_bar(1, 128);
-        if (!last) continue;
-        fence_acq_rel_gpu();
-        float acc_r[RP];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) acc_r[r] = 0.f;
-        constexpr int NIF = RP == 16 ? 2 : 1;   // segments with loads in flight at once
-        for (int q0 = 0; q0 < nseg; q0 += NIF) {
-          float4 w4[NIF][V4];
-#pragma unroll
-          for (int h = 0; h < NIF; ++h) {
-            const int q = q0 + h;
-            if (q == seg) {
-#pragma unroll
-              for (int j = 0; j < V4; ++j) w4[h][j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            } else if (q < nseg) {
-#pragma unroll
-              for (int j = 0; j < V4; ++j) w4[h][j] = __ldcg(&wsp[((size_t)q * 128 + e) * V4 + j]);
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < NIF; ++h) {
-            if (q0 + h < nseg) {
-#pragma unroll
-              for (int j = 0; j < V4; ++j) {
-                acc_r[4 * j] += w4[h][j].x;
-                acc_r[4 * j + 1] += w4[h][j].y;
-                acc_r[4 * j + 2] += w4[h][j].z;
-                acc_r[4 * j + 3] += w4[h][j].w;
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < RP; ++r) v[r] = acc_r[r];
-        if (e == 0) p.counters[t] = 0u;
-      }
-
-      // ---- fused epilogues (global loads batched ahead of use) ----
-      if (p.mode == EPI_STORE) {
-        const int f = t * 128 + e;
-        if (f < p.N) {
-#pragma unroll
-          for (int r = 0; r < RP; ++r)
-            if (r < R) p.out[(size_t)r * p.ld_out + f] = v[r];
-        }
-      } else if (p.mode == EPI_RESID) {
-        const int f = t * 128 + e;
-        const bool ok = f < p.N;
-        const float g = ok ? __bfloat162float(p.gain[f]) : 0.f;
-        float xo[RP];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) xo[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
-#pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          float sq = 0.f;
-          if (r < R && ok) {
-            const float xn = xo[r] + v[r];
-            p.x[(size_t)r * p.ld_x + f] = xn;
-            p.xg[(size_t)r * p.ld_xg + f] = __float2bfloat16(xn * g);
-            sq = xn * xn;
-          }
-          sq = warp_sum(sq);
-          if (lane == 0) scratch[quarter * RP + r] = sq;
-        }
-        named_bar(1, 128);
-        if (e < R)
-          p.ss_out[(size_t)e * p.ss_out_ld + t] =
-              ((scratch[0 * RP + e] + scratch[1 * RP + e]) + scratch[2 * RP + e]) + scratch[3 * RP + e];
-        named_bar(1, 128);
-      } else if (p.mode == EPI_SWIGLU) {
-#pragma unroll
-        for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r] * rstd[r];
-        named_bar(1, 128);
-        if (e < 64) {
-          const int f = t * 64 + e;
-          if (f < p.N) {
-#pragma unroll
-            for (int r = 0; r < RP; ++r) {
-              if (r < R) {
-                const float gt = scratch[e * (RP + 1) + r];
-                const float up = scratch[(e + 64) * (RP + 1) + r];
-                p.h[(size_t)r * p.ld_h + f] = __float2bfloat16(gt / (1.0f + __expf(-gt)) * up);
-              }
-            }
-          }
-        }
-        named_bar(1, 128);
-      } else if (p.mode == EPI_QKV) {
-        int kind, f, nrows;
-        if (t < p.t1) { kind = 0; f = t * 128 + e; nrows = p.nq; }
-        else if (t < p.t2) { kind = 1; f = (t - p.t1) * 128 + e; nrows = p.nk; }
-        else { kind = 2; f = (t - p.t2) * 128 + e; nrows = p.nk; }
-#pragma unroll
-        for (int r = 0; r < RP; ++r) v[r] *= rstd[r];
-        const int hd = p.hd, half = hd >> 1;
-        const int i = f % hd;
-        if (kind < 2) {   // rotate-half RoPE at absolute positions pos0 + r
-          const int j = i & (half - 1);
-          float2 cs[RP];
-#pragma unroll
-          for (int r = 0; r < RP; ++r) cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * half + j] : make_float2(1.f, 0.f);
-#pragma unroll
-          for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r];
-          named_bar(1, 128);
-          const int pe = e ^ half;
-#pragma unroll
-          for (int r = 0; r < RP; ++r) {
-            const float pv = scratch[pe * (RP + 1) + r];
-            v[r] = (i < half) ? (v[r] * cs[r].x - pv * cs[r].y) : (v[r] * cs[r].x + pv * cs[r].y);
-          }
-          named_bar(1, 128);
-        }
-        if (f < nrows) {
-          if (kind == 0) {
-#pragma unroll
-            for (int r = 0; r < RP; ++r)
-              if (r < R) p.q[(size_t)r * p.ld_q + f] = v[r];
-          } else {
-            const int kh = f / hd;
-            const size_t head_off = ((size_t)((p.layer * 2 + (kind - 1)) * p.hkv + kh) * p.page_size) * hd + i;
-#pragma unroll
-            for (int r = 0; r < RP; ++r)
-              if (r < R) p.kv[(size_t)kvrow[r] + head_off] = __float2bfloat16(v[r]);
-          }
-        }
-      } else {  // EPI_LMHEAD
-        const int f = t * 128 + e;
-        const bool ok = f < p.N;
-#pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          const float z = v[r] * rstd[r];
-          if (ok && r < R && p.logits != nullptr) p.logits[(size_t)r * p.ld_logits + f] = z;
-          unsigned long long k = ok ? argmax_key(z, (uint32_t)f) : 0ull;
-          k = warp_max_u64(k);
-          if (lane == 0) red[quarter * RP + r] = k;
-        }
-        named_bar(1, 128);
-        if (e < R) {
-          unsigned long long k = red[e];
-          for (int q = 1; q < 4; ++q) k = red[q * RP + e] > k ? red[q * RP + e] : k;
-          p.amax[(size_t)e * p.amax_ld + t] = k;
-        }
-        named_bar(1, 128);
-      }
+      epi_segment<RP>(p, t, seg_begin, seg_end, U, G, c, kbt, v, e, lane, quarter, R, pos0, scratch, red, rstd,
+                      kvrow, flag);
     }
   }
 
@@ -502,30 +527,57 @@ struct EmbedParams {
   float* ss; int ss_ld;
 };
 
+// Row r of the window: x = E[tok] (fp32), x∘g (bf16 operand), per-128-col sum of squares.
+PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
+  // thread t owns columns [32t, 32t+32) (d <= 4096 per pass); 4 threads per
+  // 128-column sum-of-squares slot.  All loads are issued before any use.
+  const int tok = p.step->tokens[r];
+  const __nv_bfloat16* src = p.embed + (size_t)tok * p.d;
+  for (int c0 = 0; c0 < p.d; c0 += 128 * 32) {
+    const int col = c0 + tid * 32;
+    const bool ok = col < p.d;
+    uint4 xr[4], gr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      xr[k] = ok ? reinterpret_cast<const uint4*>(src + col)[k] : make_uint4(0, 0, 0, 0);
+      gr[k] = ok ? reinterpret_cast<const uint4*>(p.gain + col)[k] : make_uint4(0, 0, 0, 0);
+    }
+    float sq = 0.f;
+    if (ok) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&xr[k]);
+        const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gr[k]);
+        float xf[8];
+        uint4 og;
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&og);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 xv = __bfloat1622float2(xb[q]);
+          const float2 gv = __bfloat1622float2(gb[q]);
+          xf[2 * q] = xv.x;
+          xf[2 * q + 1] = xv.y;
+          ob[q] = __floats2bfloat162_rn(xv.x * gv.x, xv.y * gv.y);
+          sq += xv.x * xv.x + xv.y * xv.y;
+        }
+        float4* xd = reinterpret_cast<float4*>(p.x + (size_t)r * p.ld_x + col + 8 * k);
+        xd[0] = make_float4(xf[0], xf[1], xf[2], xf[3]);
+        xd[1] = make_float4(xf[4], xf[5], xf[6], xf[7]);
+        *reinterpret_cast<uint4*>(p.xg + (size_t)r * p.ld_xg + col + 8 * k) = og;
+      }
+    }
+    sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+    if (ok && (tid & 3) == 0) p.ss[(size_t)r * p.ss_ld + col / 128] = sq;
+  }
+}
+
 __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ EmbedParams p) {
   pdl_wait();
   pdl_launch_dependents();
   const int r = blockIdx.x;
   if (r >= p.step->R) return;
-  const int tok = p.step->tokens[r];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nslots = (p.d + 127) / 128;
-  const __nv_bfloat16* src = p.embed + (size_t)tok * p.d;
-  for (int j = warp; j < nslots; j += 4) {
-    float sq = 0.f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int col = j * 128 + lane * 4 + k;
-      if (col < p.d) {
-        const float xv = __bfloat162float(src[col]);
-        p.x[(size_t)r * p.ld_x + col] = xv;
-        p.xg[(size_t)r * p.ld_xg + col] = __float2bfloat16(xv * __bfloat162float(p.gain[col]));
-        sq += xv * xv;
-      }
-    }
-    sq = warp_sum(sq);
-    if (lane == 0) p.ss[(size_t)r * p.ss_ld + j] = sq;
-  }
+  embed_row(p, r, threadIdx.x);
 }
 
 // ------------------------------------------------------------------ attention (a6)
@@ -546,15 +598,16 @@ struct AttnParams {
   int layer, hkv, H, hd;
   float scale_log2;                // log2(e) / sqrt(hd)
   int max_chunks, max_rb;
-  float* ws_o;                     // [hkv][max_rb][max_chunks][128][hd]
-  float* ws_ml;                    // [hkv][max_rb][max_chunks][128][2]
+  float* ws_o;                     // [hkv][max_rb][max_chunks][rows per block][hd]
+  float* ws_ml;                    // [hkv][max_rb][max_chunks][rows per block][2]
   unsigned* counters;              // [hkv][max_rb]
   __nv_bfloat16* out; int ld_out;
 };
 
-constexpr int kAttnRowsPerBlock = 128;
 constexpr int kAttnPad = 8;        // smem row padding (bf16 elements): conflict-free ldmatrix
-constexpr int kAttnSmem = (kAttnRowsPerBlock + 2 * kAttnChunk) * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64;
+// smem for NW warps: Q [NW*16][HD+8] + K,V [64][HD+8] bf16 + scratch
+constexpr int attn_smem_bytes(int nw) { return (nw * 16 + 2 * kAttnChunk) * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64; }
+constexpr int kAttnSmem = attn_smem_bytes(8);
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -576,32 +629,34 @@ PS_DEV uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnParams p) {
-  extern __shared__ __align__(16) uint8_t attn_smem[];
+// NW warps (16 query rows each) of one CTA run the work items
+// item = cta, cta + ncta, ...; `bar` is the named barrier id for the NW*32
+// participating threads (tid in [0, NW*32)).
+template <int HD, int NW, bool kInlineCombine = true>
+PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, int ncta, int bar) {
+  constexpr int kRB = NW * 16;                          // query rows per block
+  constexpr int NT = NW * 32;
   constexpr int LD = HD + kAttnPad;                     // smem row stride (elements)
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sK = sQ + kAttnRowsPerBlock * LD;
+  __nv_bfloat16* sK = sQ + kRB * LD;
   __nv_bfloat16* sV = sK + kAttnChunk * LD;
   float* sM = reinterpret_cast<float*>(sV + kAttnChunk * LD);   // combine scratch [64]
   int& s_last = *reinterpret_cast<int*>(sM + 3 * 64);
-  pdl_wait();
-  pdl_launch_dependents();
   const StepIn* st = p.step;
   const int R = st->R, pos0 = st->pos0;
   const int g = p.H / p.hkv;
   const int rows = R * g;
-  const int n_rb = (rows + kAttnRowsPerBlock - 1) / kAttnRowsPerBlock;
+  const int n_rb = (rows + kRB - 1) / kRB;
   const int n_keys = pos0 + R;
   const int nchunks = (n_keys + kAttnChunk - 1) / kAttnChunk;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   const int n_items = p.hkv * n_rb * nchunks;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  for (int item = cta; item < n_items; item += ncta) {
     const int c = item % nchunks;
     const int rb = (item / nchunks) % n_rb;
     const int kh = item / (nchunks * n_rb);
-    const int m0 = rb * kAttnRowsPerBlock;
-    const int mrows = min(kAttnRowsPerBlock, rows - m0);
+    const int m0 = rb * kRB;
+    const int mrows = min(kRB, rows - m0);
     const int k0 = c * kAttnChunk;
     const int nk = min(kAttnChunk, n_keys - k0);
     // ---- stage K/V chunk (one page run of 64 positions) and the Q rows (bf16, pre-scaled)
@@ -612,29 +667,46 @@ __global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnP
     const __nv_bfloat16* Vp = p.kv + (size_t)page * p.page_stride +
                               ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
     constexpr int VPR = HD / 8;                          // 16-byte vectors per row
-    for (int i = tid; i < kAttnChunk * VPR; i += 256) {
+    // K/V chunk: cp.async (16 B, zero-fill past nk) -- every copy in flight at once
+    for (int i = tid; i < kAttnChunk * VPR; i += NT) {
       const int row = i / VPR, cv = i % VPR;
-      uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (row < nk) {
-        kk = reinterpret_cast<const uint4*>(Kp + (size_t)row * HD)[cv];
-        vv = reinterpret_cast<const uint4*>(Vp + (size_t)row * HD)[cv];
-      }
-      *reinterpret_cast<uint4*>(sK + row * LD + cv * 8) = kk;
-      *reinterpret_cast<uint4*>(sV + row * LD + cv * 8) = vv;
+      const int ok = row < nk ? 16 : 0;
+      const __nv_bfloat16* ksrc = Kp + (size_t)(row < nk ? row : 0) * HD + cv * 8;
+      const __nv_bfloat16* vsrc = Vp + (size_t)(row < nk ? row : 0) * HD + cv * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sK + row * LD + cv * 8)),
+                   "l"(ksrc), "r"(ok) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sV + row * LD + cv * 8)),
+                   "l"(vsrc), "r"(ok) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // Q rows (fp32 -> bf16, pre-scaled): loads batched ahead of the conversion
     const int nwarps_used = (mrows + 15) / 16;
-    for (int i = tid; i < nwarps_used * 16 * (HD / 4); i += 256) {
-      const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
-      float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < mrows) {
-        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-        qv = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
+    {
+      constexpr int QIT = (NW * 16 * (HD / 4) + NT - 1) / NT;   // float4 per thread
+      float4 qv[QIT];
+#pragma unroll
+      for (int k = 0; k < QIT; ++k) {
+        const int i = tid + k * NT;
+        const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
+        qv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < mrows) {
+          const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+          qv[k] = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
+        }
       }
-      uint2 pk = make_uint2(pack_bf16(qv.x * p.scale_log2, qv.y * p.scale_log2),
-                            pack_bf16(qv.z * p.scale_log2, qv.w * p.scale_log2));
-      *reinterpret_cast<uint2*>(sQ + m * LD + d4) = pk;
+#pragma unroll
+      for (int k = 0; k < QIT; ++k) {
+        const int i = tid + k * NT;
+        const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
+        if (m < nwarps_used * 16) {
+          uint2 pk = make_uint2(pack_bf16(qv[k].x * p.scale_log2, qv[k].y * p.scale_log2),
+                                pack_bf16(qv[k].z * p.scale_log2, qv[k].w * p.scale_log2));
+          *reinterpret_cast<uint2*>(sQ + m * LD + d4) = pk;
+        }
+      }
     }
-    __syncthreads();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    named_bar(bar, NT);
     if (warp < nwarps_used) {
       // ---- S = Q K^T for this warp's 16 rows x 64 keys
       float sacc[8][4];
@@ -710,7 +782,7 @@ __global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnP
         }
       }
       // ---- chunk partials -> workspace
-      const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kAttnRowsPerBlock);
+      const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kRB);
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
         const int m = warp * 16 + (lane >> 2) + hr * 8;
@@ -722,23 +794,27 @@ __global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnP
         if ((lane & 3) == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[hr], lrow[hr]));
       }
     }
+    if constexpr (!kInlineCombine) {    // partials only; attn_combine runs after a grid barrier
+      named_bar(bar, NT);
+      continue;
+    }
     fence_acq_rel_gpu();
-    __syncthreads();
+    named_bar(bar, NT);
     if (tid == 0) s_last = atomicAdd(&p.counters[kh * p.max_rb + rb], 1u) == (unsigned)(nchunks - 1);
-    __syncthreads();
+    named_bar(bar, NT);
     if (s_last) {
       fence_acq_rel_gpu();
       // combine: per row M = max_c m_c, L = sum_c 2^(m_c-M) l_c, O = sum_c 2^(m_c-M) O_c / L
       const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
-      for (int m = warp; m < mrows; m += 8) {
+      for (int m = warp; m < mrows; m += NW) {
         float M = -INFINITY;
         for (int cc = lane; cc < nchunks; cc += 32)
-          M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2));
+          M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         float Lp = 0.f;
         for (int cc = lane; cc < nchunks; cc += 32) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2));
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
           Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
         }
         // fixed-order sum over chunks: lanes hold chunk-strided partials, reduce by tree
@@ -751,9 +827,9 @@ __global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnP
         for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
 #pragma unroll 8
         for (int cc = 0; cc < nchunks; ++cc) {
-          const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kAttnRowsPerBlock + m) * 2);
+          const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2);
           const float sc = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
-          const float* op = p.ws_o + ((rbase + cc) * kAttnRowsPerBlock + m) * HD + lane * DPL;
+          const float* op = p.ws_o + ((rbase + cc) * kRB + m) * HD + lane * DPL;
           if constexpr (DPL == 4) {
             const float4 o4 = __ldcg(reinterpret_cast<const float4*>(op));
             acc[0] += sc * o4.x; acc[1] += sc * o4.y; acc[2] += sc * o4.z; acc[3] += sc * o4.w;
@@ -769,14 +845,73 @@ __global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnP
       }
       if (tid == 0) p.counters[kh * p.max_rb + rb] = 0u;
     }
-    __syncthreads();
+    named_bar(bar, NT);
   }
+}
+
+// Combine of the chunk partials written by attn_run<.., false>: one warp per
+// output row (kh, m); lanes hold HD/32 dims.  Deterministic chunk order.
+template <int HD, int kRB>
+PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
+  const StepIn* st = p.step;
+  const int R = st->R, pos0 = st->pos0;
+  const int g = p.H / p.hkv;
+  const int rows = R * g;
+  const int nchunks = (pos0 + R + kAttnChunk - 1) / kAttnChunk;
+  const int lane = threadIdx.x & 31;
+  constexpr int DPL = HD / 32;
+  for (int item = gwarp; item < p.hkv * rows; item += nwarps_total) {
+    const int kh = item / rows, mg = item % rows;
+    const int rb = mg / kRB, m = mg % kRB;
+    const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
+    float M = -INFINITY;
+    for (int cc = lane; cc < nchunks; cc += 32)
+      M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float Lp = 0.f;
+    for (int cc = lane; cc < nchunks; cc += 32) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
+      Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
+    const float invL = 1.0f / Lp;
+    float acc[DPL];
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
+#pragma unroll 8
+    for (int cc = 0; cc < nchunks; ++cc) {
+      const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2);
+      const float sc = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
+      const float* op = p.ws_o + ((rbase + cc) * kRB + m) * HD + lane * DPL;
+      if constexpr (DPL == 4) {
+        const float4 o4 = __ldcg(reinterpret_cast<const float4*>(op));
+        acc[0] += sc * o4.x; acc[1] += sc * o4.y; acc[2] += sc * o4.z; acc[3] += sc * o4.w;
+      } else {
+        const float2 o2 = __ldcg(reinterpret_cast<const float2*>(op));
+        acc[0] += sc * o2.x; acc[1] += sc * o2.y;
+      }
+    }
+    const int r = mg / g, h = kh * g + mg % g;
+    __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) dst[t] = __float2bfloat16(acc[t] * invL);
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ __align__(16) uint8_t attn_smem[];
+  pdl_wait();
+  pdl_launch_dependents();
+  attn_run<HD, 8>(p, attn_smem, threadIdx.x, blockIdx.x, gridDim.x, 0);
 }
 
 // ------------------------------------------------------------------ argmax + compare + scan (a11)
 struct ArgmaxParams {
   const StepIn* step;
-  const unsigned long long* amax; int n_tiles, amax_ld;
+  unsigned long long* amax; int n_tiles, amax_ld;   // amax[r]: per-row greedy key (atomicMax)
   StepOut* out;            // device
   StepOut* mirror;         // mapped pinned host memory (zero-copy), may be null
   const SynthParams* syn;  // may be null
@@ -798,24 +933,18 @@ PS_DEV int synth_token(const SynthParams* sp, int p) {
   return t;
 }
 
-__global__ void __launch_bounds__(1024) argmax_scan_kernel(const __grid_constant__ ArgmaxParams p) {
-  __shared__ int s_pred[kMaxRows];
-  pdl_wait();
-  pdl_launch_dependents();
+// Vocab argmax from the per-tile partials, synthetic override, compare + scan.
+// NT threads (multiple of 32); s_pred: smem int[kMaxRows]; bar: named barrier id.
+template <int NT>
+PS_DEV void argmax_run(const ArgmaxParams& p, int tid, int* s_pred, int bar) {
   const StepIn* st = p.step;
   const int R = st->R;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp < R) {
-    unsigned long long k = 0;
-    for (int t = lane; t < p.n_tiles; t += 32) {
-      const unsigned long long v = p.amax[(size_t)warp * p.amax_ld + t];
-      k = v > k ? v : k;
-    }
-    k = warp_max_u64(k);
-    if (lane == 0) s_pred[warp] = (int)argmax_key_idx(k);
+  for (int row = tid; row < R; row += NT) {
+    s_pred[row] = (int)argmax_key_idx(__ldcg(&p.amax[row]));
+    p.amax[row] = 0ull;                  // reset the atomicMax slot for the next forward
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  named_bar(bar, NT);
+  if (tid == 0) {
     const int w = st->w;
     const int r0 = st->row0;             // prediction rows r0 .. r0 + w
     if ((st->flags & kFlagSynth) && p.syn != nullptr && p.syn->len_S > 0 && st->syn_onpath) {
@@ -846,6 +975,13 @@ __global__ void __launch_bounds__(1024) argmax_scan_kernel(const __grid_constant
       __threadfence_system();
     }
   }
+}
+
+__global__ void __launch_bounds__(1024) argmax_scan_kernel(const __grid_constant__ ArgmaxParams p) {
+  __shared__ int s_pred[kMaxRows];
+  pdl_wait();
+  pdl_launch_dependents();
+  argmax_run<1024>(p, threadIdx.x, s_pred, 0);
 }
 
 }  // namespace ps

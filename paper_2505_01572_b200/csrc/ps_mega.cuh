@@ -1,0 +1,398 @@
+// ps_mega.cuh — the whole verify forward as ONE persistent cooperative kernel.
+//
+// Batch-1 verification is a chain of ~5L+3 HBM-bound steps, each only a few
+// microseconds long at the roofline; launched as separate kernels every step
+// pays a launch, a prologue, a cold TMA pipeline and a drained tail.  Here one
+// CTA per SM walks the phase table
+//     EMBED, {QKV, ATTN, O, GATE/UP, DOWN} x L, [LM_HEAD, ARGMAX]
+// with the same warp roles as the standalone GEMM:
+//   warp 0      TMA producer: streams the weight tiles of every GEMM phase in
+//               order through one STAGES-deep ring.  Weights do not depend on
+//               activations, so it runs AHEAD across phase boundaries and only
+//               the small activation tile of a stage waits for the previous
+//               phase to complete (grid-wide counter, acquire) -- the HBM pipe
+//               never drains between phases.
+//   warp 1      TMEM owner + tcgen05.mma issuer (double-buffered accumulators).
+//   warps 2-5   epilogues (stream-K fixup + fused epilogue), the attention
+//               phase (mma.sync, 4 warps), embed and argmax/scan; after each
+//               phase a CTA publishes completion with a release atomic.
+// Phase completion counters are cumulative (target = gen * gridDim.x, gen
+// from StepIn), so the graph-captured kernel needs no reset.  Cooperative
+// launch guarantees every CTA is resident (the waits would deadlock otherwise).
+#pragma once
+#include "ps_kernels.cuh"
+
+namespace ps {
+
+enum { PH_EMBED = 0, PH_GEMM = 1, PH_ATTN = 2, PH_ARGMAX = 3, PH_ACOMB = 4 };
+
+struct MegaPhase {
+  int kind;
+  int gu;                          // GEMM: gate/up (two 64-row boxes per A tile)
+  int head;                        // 1: runs only in forwards with lm_head (counter target gen_head)
+  const CUtensorMap* mA0;          // global-memory tensor maps (64-byte aligned)
+  const CUtensorMap* mA1;
+  const CUtensorMap* mA2;
+  const CUtensorMap* mX;
+  GemmParams g;
+  AttnParams a;
+  EmbedParams em;
+  ArgmaxParams am;
+};
+
+struct MegaParams {
+  const MegaPhase* ph;
+  int n_ph;
+  const StepIn* step;
+  unsigned* done;                  // [n_ph] cumulative CTA completion counters
+  unsigned long long* dbg;         // optional [G][n_ph][2] %globaltimer (phase start, end)
+};
+
+constexpr int kMegaThreads = 192;
+// ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
+template <int RP> constexpr int mega_stages() { return RP == 16 ? 8 : 7; }
+constexpr int kL2Ahead = 24;       // weight tiles (16 KB) per SM prefetched into L2 ahead of the ring
+
+template <int RP>
+struct MegaSmem {
+  static constexpr int kMegaStages = mega_stages<RP>();
+  static constexpr int kABytes = 128 * 64 * 2;
+  static constexpr int kXBytes = RP * 64 * 2;
+  static constexpr int kOffX = kMegaStages * kABytes;
+  static constexpr int kOffScratch = kOffX + kMegaStages * kXBytes;
+  static constexpr int kOffRed = kOffScratch + 128 * (RP + 1) * 4;
+  static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
+  static constexpr int kOffKvRow = kOffRstd + RP * 4;
+  static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 127) / 128 * 128;
+  static constexpr int kOffBar = kOffAttn + attn_smem_bytes(4);
+  static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
+  static constexpr int kOffPhase = (kOffMisc + 64 + 127) / 128 * 128;   // MegaPhase copy (epilogue warps)
+  static constexpr int kBytes = kOffPhase + (int)((sizeof(MegaPhase) + 127) / 128 * 128) + 1024;
+};
+
+PS_DEV unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PS_DEV void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PS_DEV void spin_until(const unsigned* p, unsigned target) {
+  while ((int)(ld_acquire_u32(p) - target) < 0) {
+  }
+}
+// Generic-proxy global writes of another CTA (epilogue st.global) must be
+// visible to this CTA's async-proxy (TMA) reads of the same buffers.
+PS_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <int RP>
+__global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_constant__ MegaParams P) {
+  using L = MegaSmem<RP>;
+  constexpr int kMegaStages = L::kMegaStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sX = smem + L::kOffX;
+  float* scratch = (float*)(smem + L::kOffScratch);
+  unsigned long long* red = (unsigned long long*)(smem + L::kOffRed);
+  float* rstd = (float*)(smem + L::kOffRstd);
+  long long* kvrow = (long long*)(smem + L::kOffKvRow);
+  uint8_t* attn_smem = smem + L::kOffAttn;
+  uint64_t* full = (uint64_t*)(smem + L::kOffBar);
+  uint64_t* empty = full + kMegaStages;
+  uint64_t* tfull = empty + kMegaStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffMisc);
+  volatile int* flag = (volatile int*)(smem + L::kOffMisc + 4);
+  MegaPhase* sph = (MegaPhase*)(smem + L::kOffPhase);
+
+  constexpr int kTmemCols = RP == 16 ? 32 : 64;
+  constexpr uint32_t kIdesc = idesc_bf16_f32<128, RP>();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMegaStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // phase ph is complete when all G CTAs of every forward that ran it so far
+  // have published it: target = (#forwards containing ph) * G
+  const unsigned tgt_body = (unsigned)P.step->gen * (unsigned)G;
+  const unsigned tgt_head = (unsigned)P.step->gen_head * (unsigned)G;
+
+  if (warp == 0) {
+    // ================= TMA producer: all GEMM phases, one ring =================
+    if (lane == 0) {
+      // L2 prefetch cursor: runs kL2Ahead weight tiles ahead of the ring --
+      // across phase boundaries -- so the HBM pipe keeps streaming the next
+      // phase's weights into L2 while this phase's tail and the grid-wide
+      // dependency resolve (L2 is the staging buffer smem is too small for).
+      struct Cursor {
+        int ph = -1;
+        long long u = 0, ue = 0;
+        int kbt = 1, gu = 0, qkv = 0, t1 = 0, t2 = 0;
+        const CUtensorMap *m0 = nullptr, *m1 = nullptr, *m2 = nullptr;
+      } pf;
+      auto pf_next_phase = [&]() -> bool {
+        while (++pf.ph < P.n_ph) {
+          const MegaPhase& Q = P.ph[pf.ph];
+          if (Q.kind != PH_GEMM) continue;
+          const long long U = (long long)Q.g.n_tiles * Q.g.kb_total;
+          const int Gp = (int)min((long long)G, U);
+          if (c >= Gp) continue;
+          pf.u = sk_begin(U, Gp, c);
+          pf.ue = sk_begin(U, Gp, c + 1);
+          pf.kbt = Q.g.kb_total;
+          pf.gu = Q.gu;
+          pf.qkv = Q.g.mode == EPI_QKV;
+          pf.t1 = Q.g.t1;
+          pf.t2 = Q.g.t2;
+          pf.m0 = Q.mA0;
+          pf.m1 = Q.mA1;
+          pf.m2 = Q.mA2;
+          if (pf.u < pf.ue) return true;
+        }
+        return false;
+      };
+      // keep the prefetch cursor strictly ahead of the unit being issued
+      auto pf_sync = [&](int ph, long long u) {
+        if (pf.ph < ph || (pf.ph == ph && pf.u <= u)) {
+          const MegaPhase& Q = P.ph[ph];
+          const long long U = (long long)Q.g.n_tiles * Q.g.kb_total;
+          const int Gp = (int)min((long long)G, U);
+          pf.ph = ph;
+          pf.u = u + 1;
+          pf.ue = sk_begin(U, Gp, c + 1);
+          pf.kbt = Q.g.kb_total;
+          pf.gu = Q.gu;
+          pf.qkv = Q.g.mode == EPI_QKV;
+          pf.t1 = Q.g.t1;
+          pf.t2 = Q.g.t2;
+          pf.m0 = Q.mA0;
+          pf.m1 = Q.mA1;
+          pf.m2 = Q.mA2;
+        }
+      };
+      auto pf_one = [&]() {
+        if (pf.ph >= P.n_ph) return;
+        if (pf.ph < 0 || pf.u >= pf.ue) {
+          if (!pf_next_phase()) return;
+        }
+        const int t = (int)(pf.u / pf.kbt), kb = (int)(pf.u % pf.kbt);
+        if (pf.gu) {
+          tma_prefetch_l2_2d(pf.m0, kb * 64, t * 64);
+          tma_prefetch_l2_2d(pf.m1, kb * 64, t * 64);
+        } else if (pf.qkv) {
+          if (t < pf.t1) tma_prefetch_l2_2d(pf.m0, kb * 64, t * 128);
+          else if (t < pf.t2) tma_prefetch_l2_2d(pf.m1, kb * 64, (t - pf.t1) * 128);
+          else tma_prefetch_l2_2d(pf.m2, kb * 64, (t - pf.t2) * 128);
+        } else {
+          tma_prefetch_l2_2d(pf.m0, kb * 64, t * 128);
+        }
+        ++pf.u;
+      };
+      uint32_t it = 0;   // units issued so far (ring position)
+      for (int ph = 0; ph < P.n_ph; ++ph) {
+        const MegaPhase& Q = P.ph[ph];
+        if (Q.kind != PH_GEMM) continue;
+        const int n_tiles = Q.g.n_tiles, kbt = Q.g.kb_total;
+        const long long U = (long long)n_tiles * kbt;
+        const int Gp = (int)min((long long)G, U);
+        if (c >= Gp) continue;
+        const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
+        const CUtensorMap* mA0 = Q.mA0;
+        const CUtensorMap* mA1 = Q.mA1;
+        const CUtensorMap* mA2 = Q.mA2;
+        const CUtensorMap* mX = Q.mX;
+        const int gu = Q.gu, qkv = (Q.g.mode == EPI_QKV), t1 = Q.g.t1, t2 = Q.g.t2;
+        tma_prefetch_desc(mA0);
+        tma_prefetch_desc(mX);
+        bool ready = false;
+        int pend_slot[kMegaStages];
+        int pend_kb[kMegaStages];
+        int npend = 0;
+        const unsigned* dep = P.done + (ph - 1);
+        const unsigned target = P.ph[ph - 1].head ? tgt_head : tgt_body;
+        auto flush = [&]() {
+          for (int i = 0; i < npend; ++i)
+            tma_load_2d(sX + pend_slot[i] * L::kXBytes, mX, &full[pend_slot[i]], pend_kb[i] * 64, 0, kEvictLast);
+          npend = 0;
+        };
+        for (long long u = ub; u < ue; ++u) {
+          const int slot = it % kMegaStages;
+          const uint32_t par = ((it / kMegaStages) & 1) ^ 1;
+          if (!mbar_try_wait(&empty[slot], par)) {
+            if (npend) {             // ring full of tiles waiting for activations:
+              // while the dependency resolves, stream the NEXT tiles into L2
+              pf_sync(ph, u - 1);
+              int nprf = 0;
+              while ((int)(ld_acquire_u32(dep) - target) < 0)
+                if (nprf < kL2Ahead) { pf_one(); ++nprf; }
+              fence_proxy_async_global();
+              ready = true;
+              flush();
+            }
+            mbar_wait(&empty[slot], par);
+          }
+          const int t = (int)(u / kbt), kb = (int)(u % kbt);
+          uint8_t* dst = sA + slot * L::kABytes;
+          mbar_arrive_expect_tx(&full[slot], L::kABytes + L::kXBytes);
+          if (gu) {
+            tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 64, kEvictFirst);
+            tma_load_2d(dst + 64 * 128, mA1, &full[slot], kb * 64, t * 64, kEvictFirst);
+          } else if (qkv) {
+            if (t < t1) tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
+            else if (t < t2) tma_load_2d(dst, mA1, &full[slot], kb * 64, (t - t1) * 128, kEvictFirst);
+            else tma_load_2d(dst, mA2, &full[slot], kb * 64, (t - t2) * 128, kEvictFirst);
+          } else {
+            tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
+          }
+          if (!ready) {
+            ready = (int)(ld_acquire_u32(dep) - target) >= 0;
+            if (ready) fence_proxy_async_global();
+          }
+          if (ready) {
+            flush();
+            tma_load_2d(sX + slot * L::kXBytes, mX, &full[slot], kb * 64, 0, kEvictLast);
+          } else {
+            pend_slot[npend] = slot;
+            pend_kb[npend] = kb;
+            ++npend;
+          }
+          ++it;
+        }
+        if (npend) {
+          pf_sync(ph, ue - 1);
+          int nprf = 0;
+          while ((int)(ld_acquire_u32(dep) - target) < 0)
+            if (nprf < kL2Ahead) { pf_one(); ++nprf; }
+          fence_proxy_async_global();
+          flush();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      uint32_t it = 0, nacc = 0;
+      for (int ph = 0; ph < P.n_ph; ++ph) {
+        const MegaPhase& Q = P.ph[ph];
+        if (Q.kind != PH_GEMM) continue;
+        const int kbt = Q.g.kb_total;
+        const long long U = (long long)Q.g.n_tiles * kbt;
+        const int Gp = (int)min((long long)G, U);
+        if (c >= Gp) continue;
+        const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
+        long long u = ub;
+        while (u < ue) {
+          const int t = (int)(u / kbt);
+          const long long seg_begin = u;
+          const long long seg_end = min(ue, (long long)(t + 1) * kbt);
+          const int acc = nacc & 1;
+          mbar_wait(&tempty[acc], ((nacc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dcol = tmem + acc * RP;
+          for (; u < seg_end; ++u, ++it) {
+            const int slot = it % kMegaStages;
+            mbar_wait(&full[slot], (it / kMegaStages) & 1);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + slot * L::kABytes);
+            const uint32_t x0 = smem_u32(sX + slot * L::kXBytes);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
+                       (u != seg_begin || k > 0) ? 1u : 0u);
+            mma_commit(&empty[slot]);
+          }
+          mma_commit(&tfull[acc]);
+          ++nacc;
+        }
+      }
+    }
+  } else {
+    // ================= epilogue / attention / embed / argmax (warps 2-5) =================
+    const int quarter = warp & 3;
+    const int e = quarter * 32 + lane;
+    const int et = threadIdx.x - 64;                   // 0..127 in warp order 2..5
+    uint32_t nacc = 0;
+    const StepIn* st = P.step;
+    const int R = st->R;
+    const int pos0 = st->pos0;
+    for (int ph = 0; ph < P.n_ph; ++ph) {
+      // phase descriptor -> smem (one batch of 8-byte loads; every later
+      // parameter access is a shared-memory hit instead of an L2 round trip)
+      {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(P.ph + ph);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(sph);
+        constexpr int NW8 = (int)(sizeof(MegaPhase) / 8);
+        for (int i = et; i < NW8; i += 128) dst[i] = src[i];
+      }
+      const int prev_head = ph > 0 ? P.ph[ph - 1].head : 0;
+      if (ph > 0) {                                    // inputs of this phase are complete
+        if (et == 0) spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
+      }
+      named_bar(1, 128);
+      if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 2] = globaltimer();
+      const MegaPhase& Q = *sph;
+      const int kind = Q.kind;
+      if (kind == PH_EMBED) {
+        for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
+      } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
+        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1);
+        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1);
+      } else if (kind == PH_ACOMB) {
+        if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
+        else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
+      } else if (kind == PH_ARGMAX) {
+        if (c == 0) argmax_run<128>(Q.am, et, (int*)scratch, 1);
+      } else {
+        const GemmParams& gp = Q.g;
+        const int kbt = gp.kb_total;
+        const long long U = (long long)gp.n_tiles * kbt;
+        const int Gp = (int)min((long long)G, U);
+        if (c < Gp) {
+          epi_prepare<RP>(gp, e, R, pos0, scratch, rstd, kvrow);
+          const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
+          long long u = ub;
+          while (u < ue) {
+            const int t = (int)(u / kbt);
+            const long long seg_begin = u;
+            const long long seg_end = min(ue, (long long)(t + 1) * kbt);
+            const int acc = nacc & 1;
+            mbar_wait(&tfull[acc], (nacc >> 1) & 1);
+            tc_fence_after();
+            float v[RP];
+            load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * RP, v);
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            ++nacc;
+            u = seg_end;
+            epi_segment<RP>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch, red,
+                            rstd, kvrow, flag);
+          }
+        }
+      }
+      // publish this CTA's completion of phase ph (release: orders all of the
+      // CTA's phase writes, observed through the named barrier, before it)
+      named_bar(1, 128);
+      if (et == 0) {
+        fence_proxy_async_global();
+        red_release_add(P.done + ph, 1u);
+        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 2 + 1] = globaltimer();
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+}
+
+}  // namespace ps

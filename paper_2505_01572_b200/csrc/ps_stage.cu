@@ -18,7 +18,7 @@
 
 #include "../../include/pipespec.h"
 #include "../../include/pipespec_test.h"
-#include "ps_kernels.cuh"
+#include "ps_mega.cuh"
 
 using namespace ps;
 
@@ -169,6 +169,8 @@ static ps_status init_device_globals(int device) {
   if ((st = gemm_setup_attr<32, true>()) != PS_OK) return st;
   CU_TRY(cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
   CU_TRY(cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
   return PS_OK;
 }
 
@@ -206,6 +208,14 @@ struct ps_stage {
   cudaEvent_t in_ev[8] = {};         // recorded after each slot's H2D copy
   int in_slot = 0;
   int last_bucket = 0;
+  // megakernel: phase tables per (bucket, with_head), device tensor maps, counters
+  bool use_mega = true;
+  MegaPhase* mega_ph[4] = {nullptr, nullptr, nullptr, nullptr};
+  CUtensorMap* mega_maps[4] = {nullptr, nullptr, nullptr, nullptr};
+  int mega_n[4] = {0, 0, 0, 0};
+  unsigned* mega_done = nullptr;
+  unsigned long long* mega_dbg = nullptr;
+  unsigned gen = 0, gen_head = 0;
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
   StepOut* h_out_dev = nullptr;      // its device alias
@@ -270,26 +280,35 @@ static void rope_table(const ps_model_shape& s, int max_seq, std::vector<float2>
 // ---------------------------------------------------------------- forward
 enum { K_EMBED = 0, K_QKV, K_ATTN, K_O, K_GU, K_DOWN, K_LMHEAD, K_ARGMAX };
 
-// Launch one kernel of the forward for rows bucket b (layer l where relevant).
-static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
+// Host-side TMA maps of one GEMM step: A0..A2 (weights) and X (activations).
+struct HostMaps {
+  const CUtensorMap *a0 = nullptr, *a1 = nullptr, *a2 = nullptr, *x = nullptr;
+};
+
+// Parameters of one step of the forward (rows bucket b, layer l) -- shared by
+// the per-kernel path (launch_one) and the megakernel phase table.
+static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostMaps& hm) {
   const ps_model_shape& sh = S->sh;
-  const int RP = bucket_rp(b);
   const int d = sh.d_model, hq = sh.n_heads * sh.head_dim, hkv = sh.n_kv_heads * sh.head_dim;
   const float inv_d = 1.0f / d;
   const int ss_n = (d + 127) / 128;
   const __nv_bfloat16* const* W = sh.n_layers ? &S->lw[(size_t)l * 9] : nullptr;
+  memset(&P, 0, sizeof P);
+  GemmParams& p = P.g;
+  p.step = S->d_in;
+  p.ws = S->ws;
+  p.counters = S->counters;
   switch (kind) {
     case K_EMBED: {
-      EmbedParams e{S->d_in, S->embed, d, sh.n_layers ? S->lw[PS_N_ATTN] : S->final_norm,
-                    S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
-      return launch_simple(embed_kernel, dim3(RP), dim3(128), 0, e, S->stream);
+      P.kind = PH_EMBED;
+      P.em = EmbedParams{S->d_in, S->embed, d, sh.n_layers ? S->lw[PS_N_ATTN] : S->final_norm,
+                         S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
+      return;
     }
     case K_QKV: {   // QKV + RoPE + paged KV append (a4, a5)
       const LayerMaps& M = S->maps[l];
-      GemmParams p = {};
-      p.step = S->d_in;
+      P.kind = PH_GEMM;
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
-      p.ws = S->ws; p.counters = S->counters;
       p.mode = EPI_QKV;
       p.N = hq + 2 * hkv;
       p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg;
@@ -298,63 +317,184 @@ static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
       p.q = S->q; p.ld_q = hq;
       p.kv = S->kv; p.page_table = S->d_page_table; p.page_size = S->page_size; p.layer = l;
       p.hkv = sh.n_kv_heads; p.hd = sh.head_dim; p.page_stride = S->page_elems; p.rope_cs = S->rope_cs;
-      return launch_gemm(RP, false, M.q, M.k, M.v, S->map_xg[b], p, S->gs_qkv.grid, S->stream);
+      hm = HostMaps{&M.q, &M.k, &M.v, &S->map_xg[b]};
+      return;
     }
     case K_ATTN: {  // split-KV decode attention (a6)
-      AttnParams a{};
+      P.kind = PH_ATTN;
+      AttnParams& a = P.a;
       a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
       a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
       a.H = sh.n_heads; a.hd = sh.head_dim; a.scale_log2 = 1.4426950408889634f / std::sqrt((float)sh.head_dim);
       a.max_chunks = S->max_chunks; a.max_rb = S->max_rb;
       a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
       a.out = S->att; a.ld_out = hq;
-      if (sh.head_dim == 128)
-        return launch_simple(attn_kernel<128>, dim3(S->attn_grid), dim3(256), kAttnSmem, a, S->stream);
-      return launch_simple(attn_kernel<64>, dim3(S->attn_grid), dim3(256), kAttnSmem, a, S->stream);
+      return;
     }
     case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
       const LayerMaps& M = S->maps[l];
-      GemmParams o = {};
-      o.step = S->d_in; o.mode = EPI_RESID; o.N = d;
-      o.n_tiles = S->gs_o.n_tiles; o.kb_total = S->gs_o.kb_total; o.maxseg = S->gs_o.maxseg;
-      o.x = S->x; o.ld_x = d; o.xg = S->xg; o.ld_xg = S->xg_ld; o.gain = W[PS_N_MLP];
-      o.ss_out = S->ss; o.ss_out_ld = S->ss_ld; o.ws = S->ws; o.counters = S->counters;
-      return launch_gemm(RP, false, M.o, M.o, M.o, S->map_att[b], o, S->gs_o.grid, S->stream);
+      P.kind = PH_GEMM;
+      p.mode = EPI_RESID; p.N = d;
+      p.n_tiles = S->gs_o.n_tiles; p.kb_total = S->gs_o.kb_total; p.maxseg = S->gs_o.maxseg;
+      p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld; p.gain = W[PS_N_MLP];
+      p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
+      hm = HostMaps{&M.o, &M.o, &M.o, &S->map_att[b]};
+      return;
     }
     case K_GU: {    // gate/up + SiLU*mul (a8)
       const LayerMaps& M = S->maps[l];
-      GemmParams g = {};
-      g.step = S->d_in; g.mode = EPI_SWIGLU; g.N = sh.d_ffn;
-      g.n_tiles = S->gs_gu.n_tiles; g.kb_total = S->gs_gu.kb_total; g.maxseg = S->gs_gu.maxseg;
-      g.ss_in = S->ss; g.ss_n = ss_n; g.ss_ld = S->ss_ld; g.inv_d = inv_d; g.eps = sh.rms_eps;
-      g.h = S->h; g.ld_h = sh.d_ffn; g.ws = S->ws; g.counters = S->counters;
-      return launch_gemm(RP, true, M.g, M.u, M.u, S->map_xg[b], g, S->gs_gu.grid, S->stream);
+      P.kind = PH_GEMM;
+      P.gu = 1;
+      p.mode = EPI_SWIGLU; p.N = sh.d_ffn;
+      p.n_tiles = S->gs_gu.n_tiles; p.kb_total = S->gs_gu.kb_total; p.maxseg = S->gs_gu.maxseg;
+      p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
+      p.h = S->h; p.ld_h = sh.d_ffn;
+      hm = HostMaps{&M.g, &M.u, &M.u, &S->map_xg[b]};
+      return;
     }
     case K_DOWN: {  // down + residual; writes x∘g_next and sumsq (a9)
       const LayerMaps& M = S->maps[l];
-      GemmParams dn = {};
-      dn.step = S->d_in; dn.mode = EPI_RESID; dn.N = d;
-      dn.n_tiles = S->gs_d.n_tiles; dn.kb_total = S->gs_d.kb_total; dn.maxseg = S->gs_d.maxseg;
-      dn.x = S->x; dn.ld_x = d; dn.xg = S->xg; dn.ld_xg = S->xg_ld;
-      dn.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
-      dn.ss_out = S->ss; dn.ss_out_ld = S->ss_ld; dn.ws = S->ws; dn.counters = S->counters;
-      return launch_gemm(RP, false, M.d, M.d, M.d, S->map_h[b], dn, S->gs_d.grid, S->stream);
+      P.kind = PH_GEMM;
+      p.mode = EPI_RESID; p.N = d;
+      p.n_tiles = S->gs_d.n_tiles; p.kb_total = S->gs_d.kb_total; p.maxseg = S->gs_d.maxseg;
+      p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld;
+      p.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
+      p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
+      hm = HostMaps{&M.d, &M.d, &M.d, &S->map_h[b]};
+      return;
     }
     case K_LMHEAD: {  // final norm + lm_head + argmax partials (a10)
-      GemmParams p = {};
-      p.step = S->d_in; p.mode = EPI_LMHEAD; p.N = sh.vocab;
+      P.kind = PH_GEMM;
+      p.mode = EPI_LMHEAD; p.N = sh.vocab;
       p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
       p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
-      p.ws = S->ws; p.counters = S->counters;
-      return launch_gemm(RP, false, S->map_lm, S->map_lm, S->map_lm, S->map_xg[b], p, S->gs_lm.grid, S->stream);
+      hm = HostMaps{&S->map_lm, &S->map_lm, &S->map_lm, &S->map_xg[b]};
+      return;
     }
     case K_ARGMAX: {  // argmax + compare + first-mismatch scan (a11)
-      ArgmaxParams ap{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
-      return launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, ap, S->stream);
+      P.kind = PH_ARGMAX;
+      P.am = ArgmaxParams{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
+      return;
     }
   }
-  return fail(PS_E_INVALID, "unknown kernel kind %d", kind);
+}
+
+static int gemm_grid(const ps_stage* S, int kind) {
+  switch (kind) {
+    case K_QKV: return S->gs_qkv.grid;
+    case K_O: return S->gs_o.grid;
+    case K_GU: return S->gs_gu.grid;
+    case K_DOWN: return S->gs_d.grid;
+    default: return S->gs_lm.grid;
+  }
+}
+
+// Launch one kernel of the forward for rows bucket b (layer l where relevant).
+static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
+  MegaPhase P;
+  HostMaps hm;
+  build_phase(S, b, kind, l, P, hm);
+  const int RP = bucket_rp(b);
+  switch (P.kind) {
+    case PH_EMBED:
+      return launch_simple(embed_kernel, dim3(RP), dim3(128), 0, P.em, S->stream);
+    case PH_ATTN:
+      if (S->sh.head_dim == 128)
+        return launch_simple(attn_kernel<128>, dim3(S->attn_grid), dim3(256), kAttnSmem, P.a, S->stream);
+      return launch_simple(attn_kernel<64>, dim3(S->attn_grid), dim3(256), kAttnSmem, P.a, S->stream);
+    case PH_ARGMAX:
+      return launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, P.am, S->stream);
+    default:
+      return launch_gemm(RP, P.gu != 0, *hm.a0, *hm.a1, *hm.a2, *hm.x, P.g, gemm_grid(S, kind), S->stream);
+  }
+}
+
+// ---------------------------------------------------------------- megakernel
+// Phase table of one forward (bucket b; with_head adds LM_HEAD + ARGMAX), with
+// tensor maps copied to device memory.
+static ps_status build_mega(ps_stage* S, int b, bool with_head) {
+  const int L = S->sh.n_layers;
+  std::vector<MegaPhase> ph;
+  std::vector<CUtensorMap> maps;
+  auto add = [&](int kind, int l) {
+    MegaPhase P;
+    HostMaps hm;
+    build_phase(S, b, kind, l, P, hm);
+    if (P.kind == PH_GEMM) {   // device map indices, patched to pointers below
+      const size_t base = maps.size();
+      maps.push_back(*hm.a0);
+      maps.push_back(*hm.a1);
+      maps.push_back(*hm.a2);
+      maps.push_back(*hm.x);
+      P.mA0 = reinterpret_cast<const CUtensorMap*>(base + 1);   // 1-based index
+    }
+    ph.push_back(P);
+  };
+  add(K_EMBED, 0);
+  for (int l = 0; l < L; ++l)
+    for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
+      add(kind, l);
+      if (kind == K_ATTN) {          // chunk partials, then a separate combine phase
+        ph.push_back(ph.back());
+        ph.back().kind = PH_ACOMB;
+      }
+    }
+  if (with_head) {
+    add(K_LMHEAD, 0);
+    ph.back().head = 1;
+    add(K_ARGMAX, 0);
+    ph.back().head = 1;
+  }
+  const int key = b * 2 + (with_head ? 1 : 0);
+  if (S->mega_maps[key]) cudaFree(S->mega_maps[key]);
+  if (S->mega_ph[key]) cudaFree(S->mega_ph[key]);
+  CU_TRY(cudaMalloc(&S->mega_maps[key], std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
+  CU_TRY(cudaMemcpy(S->mega_maps[key], maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  const CUtensorMap* dm = S->mega_maps[key];
+  for (auto& P : ph) {
+    if (P.kind != PH_GEMM) continue;
+    const size_t base = reinterpret_cast<size_t>(P.mA0) - 1;
+    P.mA0 = dm + base;
+    P.mA1 = dm + base + 1;
+    P.mA2 = dm + base + 2;
+    P.mX = dm + base + 3;
+  }
+  CU_TRY(cudaMalloc(&S->mega_ph[key], ph.size() * sizeof(MegaPhase)));
+  CU_TRY(cudaMemcpy(S->mega_ph[key], ph.data(), ph.size() * sizeof(MegaPhase), cudaMemcpyHostToDevice));
+  S->mega_n[key] = (int)ph.size();
+  return PS_OK;
+}
+
+static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
+  const int key = b * 2 + (with_head ? 1 : 0);
+  if (!S->mega_ph[key]) {
+    ps_status st = build_mega(S, b, with_head);
+    if (st != PS_OK) return st;
+  }
+  if ((g_test_flags & 8) && !S->mega_dbg)
+    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 2 * 8));
+  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g_num_sms);
+  cfg.blockDim = dim3(kMegaThreads);
+  cfg.stream = S->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (b == 0) {
+    cfg.dynamicSmemBytes = MegaSmem<16>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, mega_kernel<16>, mp);
+  } else {
+    cfg.dynamicSmemBytes = MegaSmem<32>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, mega_kernel<32>, mp);
+  }
+  if (e != cudaSuccess) return fail(PS_E_CUDA, "megakernel launch: %s", cudaGetErrorString(e));
+  g_launches++;
+  return PS_OK;
 }
 
 // Enqueue one forward over StepIn rows (already uploaded): embed, L x {QKV,
@@ -387,6 +527,7 @@ static ps_status run_forward(ps_stage* S, int R, bool with_head) {
   CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
   CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
   S->in_slot = (S->in_slot + 1) % 8;
+  if (S->use_mega) return launch_mega(S, b, with_head);
   if (!S->use_graphs) return enqueue_forward(S, b, with_head);
   cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
   if (!ge) {
@@ -475,6 +616,12 @@ ps_status ps_stage_destroy(ps_stage* S) {
   for (auto& gb : S->graph)
     for (auto& g : gb)
       if (g) cudaGraphExecDestroy(g);
+  for (int k = 0; k < 4; ++k) {
+    if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
+    if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
+  }
+  if (S->mega_done) cudaFree(S->mega_done);
+  if (S->mega_dbg) cudaFree(S->mega_dbg);
   void* dev[] = {S->d_page_table, S->d_in, S->d_out, S->x, S->q, S->ss, S->logits, S->ws, S->xg, S->att, S->h,
                  S->amax, S->counters, S->attn_counters, S->attn_o, S->attn_ml, S->rope_cs, S->d_syn, S->d_S};
   for (void* p : dev)
@@ -533,6 +680,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->max_window = o->max_window;
   S->page_size = o->page_size;
   S->use_graphs = o->use_graphs != 0;
+  S->use_mega = o->use_megakernel != 0;
   if (o->stream) {
     S->stream = (cudaStream_t)o->stream;
   } else {
@@ -607,15 +755,16 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMalloc(&S->ws, ws_elems * 4));
   S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * 4));
   S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
-  S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * S->lm_tiles * 8));
+  S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * 8));
+  S_TRY(cudaMemset(S->amax, 0, (size_t)kMaxRows * 8));
   // --- attention workspace
   S->max_chunks = (S->max_seq + kMaxRows + kAttnChunk - 1) / kAttnChunk;
   {
     const int g = sh.n_heads / sh.n_kv_heads;
-    S->max_rb = (kMaxRows * g + kAttnRowsPerBlock - 1) / kAttnRowsPerBlock;
+    S->max_rb = (kMaxRows * g + 63) / 64;   // row blocks of >= 64 rows (megakernel: 64, standalone: 128)
   }
   S->attn_grid = std::min(sh.n_kv_heads * S->max_rb * S->max_chunks, 2 * n);
-  const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * kAttnRowsPerBlock;
+  const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * 128;
   S_TRY(cudaMalloc(&S->attn_o, attn_rows * sh.head_dim * 4));
   S_TRY(cudaMalloc(&S->attn_ml, attn_rows * 2 * 4));
   S_TRY(cudaMalloc(&S->attn_counters, (size_t)sh.n_kv_heads * S->max_rb * 4));
@@ -638,6 +787,9 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->d_page_table, 0, (size_t)lpages * 4));
   S_TRY(cudaHostAlloc(&S->h_page_table, (size_t)lpages * 4, cudaHostAllocDefault));
   memset(S->h_page_table, 0, (size_t)lpages * 4);
+  // --- megakernel phase-completion counters (cumulative; see ps_mega.cuh)
+  S_TRY(cudaMalloc(&S->mega_done, (size_t)(6 * sh.n_layers + 8) * 4));
+  S_TRY(cudaMemset(S->mega_done, 0, (size_t)(6 * sh.n_layers + 8) * 4));
   // --- synthetic override (disabled)
   S_TRY(cudaMalloc(&S->d_syn, sizeof(SynthParams)));
   S->h_syn = SynthParams{};
@@ -664,6 +816,9 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   in->syn_p0 = 0;
   in->syn_onpath = 0;
   in->row0 = row0;
+  in->gen = (int32_t)(++S->gen);
+  if (with_head) ++S->gen_head;
+  in->gen_head = (int32_t)S->gen_head;
   if (with_head && !S->S_host.empty()) {
     in->flags |= kFlagSynth;
     const long long gen = (long long)S->tokens.size() - S->n_prompt;
@@ -831,7 +986,7 @@ ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
   info->kv_len = S->kv_len;
   info->pages_in_use = pages_in_use(S);
   info->pages_total = S->pages_total;
-  info->launches_per_verify = 1 + 5LL * S->sh.n_layers + 2;
+  info->launches_per_verify = S->use_mega ? 1 : 1 + 5LL * S->sh.n_layers + 2;
   info->rows_buckets[0] = 16;
   info->rows_buckets[1] = 32;
   return PS_OK;
@@ -1016,6 +1171,7 @@ extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t
     case 6: src = S->kv; break;
     case 7: src = S->attn_ml; break;
     case 8: src = S->d_page_table; break;
+    case 9: src = S->mega_dbg; break;
     default: return fail(PS_E_INVALID, "unknown buffer %d", which);
   }
   CU_TRY(cudaStreamSynchronize(S->stream));

@@ -36,7 +36,7 @@ class Stage:
 
     def __init__(self, shape, weights: dict, max_seq: int = 1024, max_window: int = 31,
                  page_size: int = 64, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, megakernel: bool = True):
         self.shape = shape
         self.weights = weights            # keep the borrowed tensors alive
         self._sh = model_shape(shape)
@@ -59,7 +59,7 @@ class Stage:
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self._pl = abi.Placement(device, None, 0, 1)
         self._opts = abi.StageOpts(max_seq, max_window, page_size, self.kv_pool.data_ptr(), nbytes,
-                                   self.stream.cuda_stream, int(use_graphs))
+                                   self.stream.cuda_stream, int(use_graphs), int(megakernel))
         h = C.c_void_p()
         abi.check(abi.lib().ps_stage_create(C.byref(self._sh), C.byref(self._w), C.byref(self._pl),
                                             C.byref(self._opts), C.byref(h)))
