@@ -166,7 +166,13 @@ typedef struct ps_stage_info {
   int64_t n_tokens, kv_len, pages_in_use, pages_total;
   int64_t launches_per_verify;  /* kernels one verify pass enqueues */
   int32_t rows_buckets[4];      /* padded row counts with captured graphs */
+  /* device time of the forward kernels (CUDA events around the launches on
+   * the stage stream): the last verify/draft forward, and the running sums
+   * over all verify/draft forwards since creation (ps_stage_reset_timers). */
+  double last_fwd_ms, sum_fwd_ms;
+  int64_t n_fwd;
 } ps_stage_info;
+ps_status ps_stage_reset_timers(ps_stage* stage);
 ps_status ps_stage_get_info(const ps_stage* stage, ps_stage_info* info);
 
 /* Synthetic-alpha override (SURVEY §8(c)

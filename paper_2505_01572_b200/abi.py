@@ -50,7 +50,8 @@ class StageOpts(C.Structure):
 
 class StageInfo(C.Structure):
     _fields_ = [("n_tokens", C.c_int64), ("kv_len", C.c_int64), ("pages_in_use", C.c_int64),
-                ("pages_total", C.c_int64), ("launches_per_verify", C.c_int64), ("rows_buckets", C.c_int32 * 4)]
+                ("pages_total", C.c_int64), ("launches_per_verify", C.c_int64), ("rows_buckets", C.c_int32 * 4),
+                ("last_fwd_ms", C.c_double), ("sum_fwd_ms", C.c_double), ("n_fwd", C.c_int64)]
 
 
 class RunOpts(C.Structure):
@@ -79,6 +80,7 @@ _PROTOS = {
     "ps_kv_rollback": (C.c_int32, [C.c_void_p, C.c_int64]),
     "ps_stage_tokens": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "ps_stage_get_info": (C.c_int32, [C.c_void_p, C.POINTER(StageInfo)]),
+    "ps_stage_reset_timers": (C.c_int32, [C.c_void_p]),
     "ps_set_synthetic": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(C.c_double), C.c_uint64]),
     "ps_pipeline_run": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.POINTER(RunOpts),

@@ -602,6 +602,7 @@ struct AttnParams {
   float* ws_ml;                    // [hkv][max_rb][max_chunks][rows per block][2]
   unsigned* counters;              // [hkv][max_rb]
   __nv_bfloat16* out; int ld_out;
+  unsigned long long* dbg;         // optional per-CTA stage stamps [cta][8] (first item)
 };
 
 constexpr int kAttnPad = 8;        // smem row padding (bf16 elements): conflict-free ldmatrix
@@ -659,6 +660,8 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     const int mrows = min(kRB, rows - m0);
     const int k0 = c * kAttnChunk;
     const int nk = min(kAttnChunk, n_keys - k0);
+    const bool stamp = p.dbg != nullptr && tid == 0 && item == cta;
+    if (stamp) p.dbg[cta * 8 + 0] = globaltimer();
     // ---- stage K/V chunk (one page run of 64 positions) and the Q rows (bf16, pre-scaled)
     const long long page = p.page_table[k0 / p.page_size];
     const int slot0 = k0 % p.page_size;
@@ -707,6 +710,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     named_bar(bar, NT);
+    if (stamp) p.dbg[cta * 8 + 1] = globaltimer();
     if (warp < nwarps_used) {
       // ---- S = Q K^T for this warp's 16 rows x 64 keys
       float sacc[8][4];
@@ -765,6 +769,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
         lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 1);
         lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 2);
       }
+      if (stamp) p.dbg[cta * 8 + 2] = globaltimer();
       // ---- O = P V  (16 rows x HD)
       float oacc[HD / 8][4];
 #pragma unroll
@@ -781,6 +786,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
           mma16816(oacc[2 * np + 1], pa[kb], b2, b3);
         }
       }
+      if (stamp) p.dbg[cta * 8 + 3] = globaltimer();
       // ---- chunk partials -> workspace
       const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kRB);
 #pragma unroll
@@ -796,6 +802,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     }
     if constexpr (!kInlineCombine) {    // partials only; attn_combine runs after a grid barrier
       named_bar(bar, NT);
+      if (stamp) p.dbg[cta * 8 + 4] = globaltimer();
       continue;
     }
     fence_acq_rel_gpu();

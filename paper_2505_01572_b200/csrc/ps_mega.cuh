@@ -46,6 +46,8 @@ struct MegaParams {
   const StepIn* step;
   unsigned* done;                  // [n_ph] cumulative CTA completion counters
   unsigned long long* dbg;         // optional [G][n_ph][2] %globaltimer (phase start, end)
+  int l2_ahead;                    // L2-prefetch depth while blocked on a dependency (tiles)
+  int l2_head;                     // tiles of the next GEMM phase prefetched into L2 at phase start
 };
 
 constexpr int kMegaThreads = 192;
@@ -53,9 +55,9 @@ constexpr int kMegaThreads = 192;
 template <int RP> constexpr int mega_stages() { return RP == 16 ? 8 : 7; }
 constexpr int kL2Ahead = 24;       // weight tiles (16 KB) per SM prefetched into L2 ahead of the ring
 
-template <int RP>
+template <int RP, int STAGES = mega_stages<RP>()>
 struct MegaSmem {
-  static constexpr int kMegaStages = mega_stages<RP>();
+  static constexpr int kMegaStages = STAGES;
   static constexpr int kABytes = 128 * 64 * 2;
   static constexpr int kXBytes = RP * 64 * 2;
   static constexpr int kOffX = kMegaStages * kABytes;
@@ -78,17 +80,34 @@ PS_DEV unsigned ld_acquire_u32(const unsigned* p) {
 PS_DEV void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+PS_DEV unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PS_DEV void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Poll with relaxed loads and a short back-off (a tight acquire spin from 148
+// SMs hammers one L2 line and invalidates L1 on every poll), then acquire once.
 PS_DEV void spin_until(const unsigned* p, unsigned target) {
-  while ((int)(ld_acquire_u32(p) - target) < 0) {
+  unsigned ns = 32;
+  while ((int)(ld_relaxed_u32(p) - target) < 0) {
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
   }
+  fence_acquire_gpu();
+}
+PS_DEV bool poll_ready(const unsigned* p, unsigned target) {
+  if ((int)(ld_relaxed_u32(p) - target) < 0) return false;
+  fence_acquire_gpu();
+  return true;
 }
 // Generic-proxy global writes of another CTA (epilogue st.global) must be
 // visible to this CTA's async-proxy (TMA) reads of the same buffers.
 PS_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-template <int RP>
+template <int RP, int STAGES = mega_stages<RP>()>
 __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_constant__ MegaParams P) {
-  using L = MegaSmem<RP>;
+  using L = MegaSmem<RP, STAGES>;
   constexpr int kMegaStages = L::kMegaStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -214,6 +233,11 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const int gu = Q.gu, qkv = (Q.g.mode == EPI_QKV), t1 = Q.g.t1, t2 = Q.g.t2;
         tma_prefetch_desc(mA0);
         tma_prefetch_desc(mX);
+        if (P.l2_head > 0) {      // stage the head of the NEXT GEMM phase in L2 now,
+          pf.ph = ph;             // so its weights are on chip when this phase's tail ends
+          pf.u = pf.ue = 0;
+          for (int i = 0; i < P.l2_head; ++i) pf_one();
+        }
         bool ready = false;
         int pend_slot[kMegaStages];
         int pend_kb[kMegaStages];
@@ -233,8 +257,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
               // while the dependency resolves, stream the NEXT tiles into L2
               pf_sync(ph, u - 1);
               int nprf = 0;
-              while ((int)(ld_acquire_u32(dep) - target) < 0)
-                if (nprf < kL2Ahead) { pf_one(); ++nprf; }
+              while (!poll_ready(dep, target)) {
+                if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
+                else __nanosleep(128);
+              }
               fence_proxy_async_global();
               ready = true;
               flush();
@@ -255,7 +281,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
           }
           if (!ready) {
-            ready = (int)(ld_acquire_u32(dep) - target) >= 0;
+            ready = poll_ready(dep, target);
             if (ready) fence_proxy_async_global();
           }
           if (ready) {
@@ -271,8 +297,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         if (npend) {
           pf_sync(ph, ue - 1);
           int nprf = 0;
-          while ((int)(ld_acquire_u32(dep) - target) < 0)
-            if (nprf < kL2Ahead) { pf_one(); ++nprf; }
+          while (!poll_ready(dep, target)) {
+            if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
+            else __nanosleep(128);
+          }
           fence_proxy_async_global();
           flush();
         }

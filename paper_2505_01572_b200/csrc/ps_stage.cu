@@ -72,6 +72,7 @@ static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64
 }
 
 // ============================================================================ GEMM launch
+constexpr int kL2Head = 0;    // megakernel: next-phase tiles staged in L2 at phase start (measured: no gain)
 constexpr int kStages = 4;   // x (16 KB weights + RP*128 B activations): 2 CTAs/SM
 static int g_num_sms = 0;
 static int g_test_flags = 0;   // test hooks only: bit0 = launch without PDL
@@ -171,6 +172,8 @@ static ps_status init_device_globals(int device) {
   CU_TRY(cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 4>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32, 4>::kBytes));
   return PS_OK;
 }
 
@@ -208,6 +211,9 @@ struct ps_stage {
   cudaEvent_t in_ev[8] = {};         // recorded after each slot's H2D copy
   int in_slot = 0;
   int last_bucket = 0;
+  cudaEvent_t fwd_ev[2] = {nullptr, nullptr};   // around the last head forward's kernels
+  double last_fwd_ms = 0, sum_fwd_ms = 0;
+  long long n_fwd = 0;
   // megakernel: phase tables per (bucket, with_head), device tensor maps, counters
   bool use_mega = true;
   MegaPhase* mega_ph[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -215,6 +221,7 @@ struct ps_stage {
   int mega_n[4] = {0, 0, 0, 0};
   unsigned* mega_done = nullptr;
   unsigned long long* mega_dbg = nullptr;
+  unsigned long long* attn_dbg = nullptr;
   unsigned gen = 0, gen_head = 0;
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
@@ -329,6 +336,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       a.max_chunks = S->max_chunks; a.max_rb = S->max_rb;
       a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
       a.out = S->att; a.ld_out = hq;
+      a.dbg = (g_test_flags & 64) ? S->attn_dbg : nullptr;
       return;
     }
     case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
@@ -474,7 +482,8 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   }
   if ((g_test_flags & 8) && !S->mega_dbg)
     CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 2 * 8));
-  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr};
+  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr,
+                (g_test_flags & 16) ? 0 : kL2Ahead, (g_test_flags & 128) ? 0 : kL2Head};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g_num_sms);
   cfg.blockDim = dim3(kMegaThreads);
@@ -485,7 +494,15 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (b == 0) {
+  if (g_test_flags & 32) {   // test: shallow ring
+    if (b == 0) {
+      cfg.dynamicSmemBytes = MegaSmem<16, 4>::kBytes;
+      e = cudaLaunchKernelEx(&cfg, mega_kernel<16, 4>, mp);
+    } else {
+      cfg.dynamicSmemBytes = MegaSmem<32, 4>::kBytes;
+      e = cudaLaunchKernelEx(&cfg, mega_kernel<32, 4>, mp);
+    }
+  } else if (b == 0) {
     cfg.dynamicSmemBytes = MegaSmem<16>::kBytes;
     e = cudaLaunchKernelEx(&cfg, mega_kernel<16>, mp);
   } else {
@@ -519,6 +536,7 @@ static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
   return PS_OK;
 }
 
+static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head);
 static ps_status run_forward(ps_stage* S, int R, bool with_head) {
   const int b = bucket_of(R);
   S->last_bucket = b;
@@ -527,7 +545,19 @@ static ps_status run_forward(ps_stage* S, int R, bool with_head) {
   CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
   CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
   S->in_slot = (S->in_slot + 1) % 8;
-  if (S->use_mega) return launch_mega(S, b, with_head);
+  if (S->use_mega) {
+    if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
+    ps_status st = launch_mega(S, b, with_head);
+    if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[1], S->stream));
+    return st;
+  }
+  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
+  ps_status st_fwd = run_forward_kernels(S, b, with_head);
+  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[1], S->stream));
+  return st_fwd;
+}
+
+static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head) {
   if (!S->use_graphs) return enqueue_forward(S, b, with_head);
   cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
   if (!ge) {
@@ -622,6 +652,7 @@ ps_status ps_stage_destroy(ps_stage* S) {
   }
   if (S->mega_done) cudaFree(S->mega_done);
   if (S->mega_dbg) cudaFree(S->mega_dbg);
+  if (S->attn_dbg) cudaFree(S->attn_dbg);
   void* dev[] = {S->d_page_table, S->d_in, S->d_out, S->x, S->q, S->ss, S->logits, S->ws, S->xg, S->att, S->h,
                  S->amax, S->counters, S->attn_counters, S->attn_o, S->attn_ml, S->rope_cs, S->d_syn, S->d_S};
   for (void* p : dev)
@@ -629,6 +660,8 @@ ps_status ps_stage_destroy(ps_stage* S) {
   if (S->h_page_table) cudaFreeHost(S->h_page_table);
   if (S->h_in) cudaFreeHost(S->h_in);
   for (auto& ev : S->in_ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : S->fwd_ev)
     if (ev) cudaEventDestroy(ev);
   if (S->h_out) cudaFreeHost(S->h_out);
   if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
@@ -649,7 +682,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   if (!w->embed || !w->lm_head || !w->final_norm || (shape->n_layers > 0 && !w->layers))
     return fail(PS_E_INVALID, "NULL weight pointer");
   const int64_t need = ps_kv_pool_bytes(shape, o->max_seq, o->page_size);
-  if (!o->kv_pool || o->kv_pool_bytes < need)
+  if ((need > 0 && !o->kv_pool) || o->kv_pool_bytes < need)
     return fail(PS_E_INVALID, "kv_pool too small (%lld < %lld bytes)", (long long)o->kv_pool_bytes, (long long)need);
   if ((st = init_device_globals(pl->device)) != PS_OK) return st;
 
@@ -717,6 +750,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMalloc(&S->d_out, sizeof(StepOut)));
   S_TRY(cudaHostAlloc(&S->h_in, 8 * sizeof(StepIn), cudaHostAllocDefault));
   for (auto& ev : S->in_ev) S_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  for (auto& ev : S->fwd_ev) S_TRY(cudaEventCreate(&ev));
   S_TRY(cudaHostAlloc(&S->h_out, sizeof(StepOut), cudaHostAllocMapped));
   S_TRY(cudaHostGetDevicePointer((void**)&S->h_out_dev, S->h_out, 0));
   memset(S->h_in, 0, 8 * sizeof(StepIn));
@@ -779,14 +813,16 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   // --- paged KV
   S->kv = (__nv_bfloat16*)o->kv_pool;
   S->page_elems = (long long)sh.n_layers * 2 * sh.n_kv_heads * S->page_size * sh.head_dim;
-  S->pages_total = (int)(o->kv_pool_bytes / (S->page_elems * 2));
   const int lpages = (S->max_seq + kMaxRows + S->page_size - 1) / S->page_size;
+  S->pages_total = S->page_elems ? (int)(o->kv_pool_bytes / (S->page_elems * 2)) : lpages;   // 0 layers: no KV
   S->page_of.assign(lpages, -1);
   for (int p = S->pages_total - 1; p >= 0; --p) S->free_pages.push_back(p);
   S_TRY(cudaMalloc(&S->d_page_table, (size_t)lpages * 4));
   S_TRY(cudaMemset(S->d_page_table, 0, (size_t)lpages * 4));
   S_TRY(cudaHostAlloc(&S->h_page_table, (size_t)lpages * 4, cudaHostAllocDefault));
   memset(S->h_page_table, 0, (size_t)lpages * 4);
+  S_TRY(cudaMalloc(&S->attn_dbg, (size_t)1024 * 8 * 8));
+  S_TRY(cudaMemset(S->attn_dbg, 0, (size_t)1024 * 8 * 8));
   // --- megakernel phase-completion counters (cumulative; see ps_mega.cuh)
   S_TRY(cudaMalloc(&S->mega_done, (size_t)(6 * sh.n_layers + 8) * 4));
   S_TRY(cudaMemset(S->mega_done, 0, (size_t)(6 * sh.n_layers + 8) * 4));
@@ -914,6 +950,15 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
                            kind, S->stream));
   }
   CU_TRY(cudaStreamSynchronize(S->stream));
+  {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, S->fwd_ev[0], S->fwd_ev[1]) == cudaSuccess) {
+      S->last_fwd_ms = ms;
+      S->sum_fwd_ms += ms;
+      ++S->n_fwd;
+    }
+    cudaGetLastError();
+  }
   const StepOut* r = S->h_out;
   const int a = r->a, nxt = r->next;
   if (a < 0 || a > w || nxt < 0 || nxt >= S->sh.vocab) return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d", a, nxt);
@@ -989,6 +1034,16 @@ ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
   info->launches_per_verify = S->use_mega ? 1 : 1 + 5LL * S->sh.n_layers + 2;
   info->rows_buckets[0] = 16;
   info->rows_buckets[1] = 32;
+  info->last_fwd_ms = S->last_fwd_ms;
+  info->sum_fwd_ms = S->sum_fwd_ms;
+  info->n_fwd = S->n_fwd;
+  return PS_OK;
+}
+
+ps_status ps_stage_reset_timers(ps_stage* S) {
+  if (!S) return fail(PS_E_INVALID, "NULL stage");
+  S->sum_fwd_ms = 0;
+  S->n_fwd = 0;
   return PS_OK;
 }
 
@@ -1172,6 +1227,7 @@ extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t
     case 7: src = S->attn_ml; break;
     case 8: src = S->d_page_table; break;
     case 9: src = S->mega_dbg; break;
+    case 10: src = S->attn_dbg; break;
     default: return fail(PS_E_INVALID, "unknown buffer %d", which);
   }
   CU_TRY(cudaStreamSynchronize(S->stream));

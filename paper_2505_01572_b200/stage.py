@@ -55,7 +55,7 @@ class Stage:
                               weights["final_norm"].data_ptr(),
                               C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
         nbytes = kv_pool_bytes(shape, max_seq, page_size)
-        self.kv_pool = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.kv_pool = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self._pl = abi.Placement(device, None, 0, 1)
         self._opts = abi.StageOpts(max_seq, max_window, page_size, self.kv_pool.data_ptr(), nbytes,
@@ -136,7 +136,11 @@ class Stage:
         i = abi.StageInfo()
         abi.check(abi.lib().ps_stage_get_info(self._h, C.byref(i)))
         return dict(n_tokens=i.n_tokens, kv_len=i.kv_len, pages_in_use=i.pages_in_use,
-                    pages_total=i.pages_total, launches_per_verify=i.launches_per_verify)
+                    pages_total=i.pages_total, launches_per_verify=i.launches_per_verify,
+                    last_fwd_ms=i.last_fwd_ms, sum_fwd_ms=i.sum_fwd_ms, n_fwd=i.n_fwd)
+
+    def reset_timers(self):
+        abi.check(abi.lib().ps_stage_reset_timers(self._h))
 
     def set_synthetic(self, S, n_prompt: int, level: int, top: int, alphas, seed: int):
         s = _i32(S)
