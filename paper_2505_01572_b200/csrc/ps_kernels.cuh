@@ -162,6 +162,45 @@ PS_DEV void epi_prepare(const GemmParams& p, int e, int R, int pos0, float* scra
   named_bar(1, 128);
 }
 
+// Fixed-order sum over the nseg stream-K partials of one tile for the first
+// 4*J rows: ((0 + p_0) + p_1) + ...; NIF segments' loads are in flight at once.
+template <int RP, int J>
+PS_DEV void sk_reduce(const float4* wsp, float* v, int e, int seg, int nseg) {
+  constexpr int V4 = RP / 4;
+  constexpr int JJ = J < V4 ? J : V4;
+  constexpr int NIF = 16 / JJ;
+  float acc[4 * JJ];
+#pragma unroll
+  for (int r = 0; r < 4 * JJ; ++r) acc[r] = 0.f;
+  for (int q0 = 0; q0 < nseg; q0 += NIF) {
+    float4 w4[NIF][JJ];
+#pragma unroll
+    for (int h = 0; h < NIF; ++h) {
+      const int q = q0 + h;
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) {
+        if (q == seg) w4[h][j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        else if (q < nseg) w4[h][j] = __ldcg(&wsp[((size_t)q * 128 + e) * V4 + j]);
+        else w4[h][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < NIF; ++h) {
+      if (q0 + h < nseg) {
+#pragma unroll
+        for (int j = 0; j < JJ; ++j) {
+          acc[4 * j] += w4[h][j].x;
+          acc[4 * j + 1] += w4[h][j].y;
+          acc[4 * j + 2] += w4[h][j].z;
+          acc[4 * j + 3] += w4[h][j].w;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4 * JJ; ++r) v[r] = acc[r];
+}
+
 // One accumulator segment of tile t (units [seg_begin, seg_end) of this CTA c
 // out of G): stream-K fixup (deterministic fixed segment order) then the
 // fused epilogue for the tile if this CTA completes it.  128 epilogue threads.
@@ -181,9 +220,11 @@ PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       const int seg = c - first;
       float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
       constexpr int V4 = RP / 4;
+      const int R4 = (R + 3) >> 2;               // float4s per thread that hold live rows
 #pragma unroll
       for (int j = 0; j < V4; ++j)
-        __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        if (j < R4)
+          __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
       fence_acq_rel_gpu();
       named_bar(1, 128);
       if (e == 0) *flag = (atomicAdd(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
@@ -192,38 +233,11 @@ PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       named_bar(1, 128);
       if (!last) break;
       fence_acq_rel_gpu();
-      float acc_r[RP];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) acc_r[r] = 0.f;
-      constexpr int NIF = RP == 16 ? 2 : 1;   // segments with loads in flight at once
-      for (int q0 = 0; q0 < nseg; q0 += NIF) {
-        float4 w4[NIF][V4];
-#pragma unroll
-        for (int h = 0; h < NIF; ++h) {
-          const int q = q0 + h;
-          if (q == seg) {
-#pragma unroll
-            for (int j = 0; j < V4; ++j) w4[h][j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else if (q < nseg) {
-#pragma unroll
-            for (int j = 0; j < V4; ++j) w4[h][j] = __ldcg(&wsp[((size_t)q * 128 + e) * V4 + j]);
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < NIF; ++h) {
-          if (q0 + h < nseg) {
-#pragma unroll
-            for (int j = 0; j < V4; ++j) {
-              acc_r[4 * j] += w4[h][j].x;
-              acc_r[4 * j + 1] += w4[h][j].y;
-              acc_r[4 * j + 2] += w4[h][j].z;
-              acc_r[4 * j + 3] += w4[h][j].w;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RP; ++r) v[r] = acc_r[r];
+      // reduce: only the live rows, with up to 16 float4 loads in flight
+      if (R4 <= 1) sk_reduce<RP, 1>(wsp, v, e, seg, nseg);
+      else if (R4 <= 2) sk_reduce<RP, 2>(wsp, v, e, seg, nseg);
+      else if (R4 <= 4) sk_reduce<RP, 4>(wsp, v, e, seg, nseg);
+      else sk_reduce<RP, (RP / 4 < 8 ? RP / 4 : 8)>(wsp, v, e, seg, nseg);
       if (e == 0) p.counters[t] = 0u;
     }
 
@@ -244,8 +258,9 @@ PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       for (int r = 0; r < RP; ++r) xo[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
+        if (r >= R) break;
         float sq = 0.f;
-        if (r < R && ok) {
+        if (ok) {
           const float xn = xo[r] + v[r];
           p.x[(size_t)r * p.ld_x + f] = xn;
           p.xg[(size_t)r * p.ld_xg + f] = __float2bfloat16(xn * g);

@@ -53,7 +53,7 @@ struct MegaParams {
 constexpr int kMegaThreads = 192;
 // ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
 template <int RP> constexpr int mega_stages() { return RP == 16 ? 8 : 7; }
-constexpr int kL2Ahead = 24;       // weight tiles (16 KB) per SM prefetched into L2 ahead of the ring
+constexpr int kL2Ahead = 0;        // tiles prefetched into L2 while blocked on a dependency (measured: re-reads, no gain)
 
 template <int RP, int STAGES = mega_stages<RP>()>
 struct MegaSmem {
@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
                 if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
                 else __nanosleep(128);
               }
+              if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
               fence_proxy_async_global();
               ready = true;
               flush();
@@ -282,7 +283,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
           }
           if (!ready) {
             ready = poll_ready(dep, target);
-            if (ready) fence_proxy_async_global();
+            if (ready) {
+              fence_proxy_async_global();
+              if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
+            }
           }
           if (ready) {
             flush();
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
             else __nanosleep(128);
           }
+          if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
           fence_proxy_async_global();
           flush();
         }
@@ -319,12 +324,18 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         if (c >= Gp) continue;
         const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
         long long u = ub;
+        bool first = true;
         while (u < ue) {
           const int t = (int)(u / kbt);
           const long long seg_begin = u;
           const long long seg_end = min(ue, (long long)(t + 1) * kbt);
           const int acc = nacc & 1;
           mbar_wait(&tempty[acc], ((nacc >> 1) & 1) ^ 1);
+          if (first && P.dbg != nullptr) {
+            mbar_wait(&full[it % kMegaStages], (it / kMegaStages) & 1);
+            P.dbg[((size_t)c * P.n_ph + ph) * 8 + 3] = globaltimer();
+          }
+          first = false;
           tc_fence_after();
           const uint32_t dcol = tmem + acc * RP;
           for (; u < seg_end; ++u, ++it) {
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
           mma_commit(&tfull[acc]);
           ++nacc;
         }
+        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 4] = globaltimer();
       }
     }
   } else {
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         if (et == 0) spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
       }
       named_bar(1, 128);
-      if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 2] = globaltimer();
+      if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 0] = globaltimer();
       const MegaPhase& Q = *sph;
       const int kind = Q.kind;
       if (kind == PH_EMBED) {
@@ -396,6 +408,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             const int acc = nacc & 1;
             mbar_wait(&tfull[acc], (nacc >> 1) & 1);
             tc_fence_after();
+            if (P.dbg != nullptr && et == 0) {
+              if (u == ub) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 5] = globaltimer();
+              P.dbg[((size_t)c * P.n_ph + ph) * 8 + 6] = globaltimer();
+            }
             float v[RP];
             load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * RP, v);
             tc_fence_before();
@@ -404,6 +420,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             u = seg_end;
             epi_segment<RP>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch, red,
                             rstd, kvrow, flag);
+            if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 7] = globaltimer();
           }
         }
       }
@@ -413,7 +430,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (et == 0) {
         fence_proxy_async_global();
         red_release_add(P.done + ph, 1u);
-        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 2 + 1] = globaltimer();
+        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 1] = globaltimer();
       }
     }
   }

@@ -481,7 +481,7 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
     if (st != PS_OK) return st;
   }
   if ((g_test_flags & 8) && !S->mega_dbg)
-    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 2 * 8));
+    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 8 * 8));
   MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr,
                 (g_test_flags & 16) ? 0 : kL2Ahead, (g_test_flags & 128) ? 0 : kL2Head};
   cudaLaunchConfig_t cfg = {};
