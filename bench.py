@@ -311,6 +311,20 @@ def main():
     step_ms = 1e3 * dev_s / args.steps
     share = (pass_ms + g * draft_ms) / step_ms if step_ms > 0 else None
 
+    # --- whole-generation runs through ps_pipeline_run (Alg.1) in each mode, wall clock
+    from paper_2505_01572_b200 import pipeline_run
+    from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
+    modes = {}
+    for mname, mode in (("ar", PS_MODE_AR), ("sync_sd", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
+        torch.cuda.synchronize()
+        w0m = time.perf_counter()
+        out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g])
+        torch.cuda.synchronize()
+        dtm = time.perf_counter() - w0m
+        assert out == S[:args.gen], f"{mname}: output differs from M_K autoregressive decoding"
+        modes[mname] = {"tokens_per_s": len(out) / dtm, "decode_s": st_.wall_ns / 1e9,
+                        "tokens_per_s_decode": len(out) / (st_.wall_ns / 1e9) if st_.wall_ns else None,
+                        "verify_steps": int(st_.verify_steps[1]), "rollbacks": int(st_.rollbacks[0])}
     value = tot_tokens / dev_s
     e2e = tot_tokens / wall_s
     fwd_per_step = g + 1
@@ -324,6 +338,7 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs > L2 (16 GB of 8B weights streamed per verify pass)"},
         "speedup_vs_ar": value / ar_tok_s, "ar_tokens_per_s": ar_tok_s,
+        "pipeline_run": modes,
         "tokens_per_step": tot_tokens / world / args.steps,
         "verify_pass": {"ms": pass_ms, "rows": R, "ctx": ctx, "bytes": pass_bytes, "GB/s": pass_gbs,
                         "frac": pass_gbs / peak},
