@@ -205,9 +205,10 @@ PS_DEV void sk_reduce(const float4* wsp, float* v, int e, int seg, int nseg) {
 // out of G): stream-K fixup (deterministic fixed segment order) then the
 // fused epilogue for the tile if this CTA completes it.  128 epilogue threads.
 template <int RP>
-PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long long seg_end, long long U, int G, int c,
+PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long long seg_end, long long U, int G, int c,
                         int kbt, float* v, int e, int lane, int quarter, int R, int pos0, float* scratch,
                         unsigned long long* red, const float* rstd, const long long* kvrow, volatile int* flag) {
+  bool finalized = false;
   do {
     // ---- stream-K fixup: deterministic, fixed segment order ----
     // Partials are laid out [tile][seg][lane e][RP] so every thread moves
@@ -350,8 +351,9 @@ PS_DEV void epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       }
       named_bar(1, 128);
     }
-
+    finalized = true;
   } while (0);
+  return finalized;   // this CTA completed tile t (its outputs are written)
 }
 
 // 192 threads: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-5

@@ -30,6 +30,9 @@ struct MegaPhase {
   int kind;
   int gu;                          // GEMM: gate/up (two 64-row boxes per A tile)
   int head;                        // 1: runs only in forwards with lm_head (counter target gen_head)
+  int tctr;                        // GEMM: base index of this phase's per-tile completion counters
+  int dep_w;                       // GEMM: X columns per producing tile of the previous (GEMM) phase;
+                                   // 0 = the X operand waits for the whole previous phase
   const CUtensorMap* mA0;          // global-memory tensor maps (64-byte aligned)
   const CUtensorMap* mA1;
   const CUtensorMap* mA2;
@@ -45,15 +48,13 @@ struct MegaParams {
   int n_ph;
   const StepIn* step;
   unsigned* done;                  // [n_ph] cumulative CTA completion counters
-  unsigned long long* dbg;         // optional [G][n_ph][2] %globaltimer (phase start, end)
-  int l2_ahead;                    // L2-prefetch depth while blocked on a dependency (tiles)
-  int l2_head;                     // tiles of the next GEMM phase prefetched into L2 at phase start
+  unsigned long long* dbg;         // optional [G][n_ph][8] %globaltimer stamps
+  unsigned* tile_done;             // cumulative per-tile completion counters (all GEMM phases)
 };
 
-constexpr int kMegaThreads = 192;
+constexpr int kMegaThreads = 224;   // 7 warps: W producer, MMA, 4 epilogue, X loader
 // ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
 template <int RP> constexpr int mega_stages() { return RP == 16 ? 8 : 7; }
-constexpr int kL2Ahead = 0;        // tiles prefetched into L2 while blocked on a dependency (measured: re-reads, no gain)
 
 template <int RP, int STAGES = mega_stages<RP>()>
 struct MegaSmem {
@@ -146,170 +147,99 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   const unsigned tgt_body = (unsigned)P.step->gen * (unsigned)G;
   const unsigned tgt_head = (unsigned)P.step->gen_head * (unsigned)G;
 
+  // Unit walk shared by the two TMA warps: fn(ph, Q, u, t, kb) for this CTA's
+  // units of every GEMM phase, in ring order.
+  auto for_units = [&](auto&& fn) {
+    for (int ph = 0; ph < P.n_ph; ++ph) {
+      const MegaPhase& Q = P.ph[ph];
+      if (Q.kind != PH_GEMM) continue;
+      const int kbt = Q.g.kb_total;
+      const long long U = (long long)Q.g.n_tiles * kbt;
+      const int Gp = (int)min((long long)G, U);
+      if (c >= Gp) continue;
+      const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
+      for (long long u = ub; u < ue; ++u) fn(ph, Q, u, (int)(u / kbt), (int)(u % kbt));
+    }
+  };
+
   if (warp == 0) {
-    // ================= TMA producer: all GEMM phases, one ring =================
+    // ================= W producer: weight tiles of every GEMM phase, never waits
+    // on activations (weights do not depend on them), so it streams ahead across
+    // phase boundaries as far as the ring allows.
     if (lane == 0) {
-      // L2 prefetch cursor: runs kL2Ahead weight tiles ahead of the ring --
-      // across phase boundaries -- so the HBM pipe keeps streaming the next
-      // phase's weights into L2 while this phase's tail and the grid-wide
-      // dependency resolve (L2 is the staging buffer smem is too small for).
-      struct Cursor {
-        int ph = -1;
-        long long u = 0, ue = 0;
-        int kbt = 1, gu = 0, qkv = 0, t1 = 0, t2 = 0;
-        const CUtensorMap *m0 = nullptr, *m1 = nullptr, *m2 = nullptr;
-      } pf;
-      auto pf_next_phase = [&]() -> bool {
-        while (++pf.ph < P.n_ph) {
-          const MegaPhase& Q = P.ph[pf.ph];
-          if (Q.kind != PH_GEMM) continue;
-          const long long U = (long long)Q.g.n_tiles * Q.g.kb_total;
-          const int Gp = (int)min((long long)G, U);
-          if (c >= Gp) continue;
-          pf.u = sk_begin(U, Gp, c);
-          pf.ue = sk_begin(U, Gp, c + 1);
-          pf.kbt = Q.g.kb_total;
-          pf.gu = Q.gu;
-          pf.qkv = Q.g.mode == EPI_QKV;
-          pf.t1 = Q.g.t1;
-          pf.t2 = Q.g.t2;
-          pf.m0 = Q.mA0;
-          pf.m1 = Q.mA1;
-          pf.m2 = Q.mA2;
-          if (pf.u < pf.ue) return true;
-        }
-        return false;
-      };
-      // keep the prefetch cursor strictly ahead of the unit being issued
-      auto pf_sync = [&](int ph, long long u) {
-        if (pf.ph < ph || (pf.ph == ph && pf.u <= u)) {
-          const MegaPhase& Q = P.ph[ph];
-          const long long U = (long long)Q.g.n_tiles * Q.g.kb_total;
-          const int Gp = (int)min((long long)G, U);
-          pf.ph = ph;
-          pf.u = u + 1;
-          pf.ue = sk_begin(U, Gp, c + 1);
-          pf.kbt = Q.g.kb_total;
-          pf.gu = Q.gu;
-          pf.qkv = Q.g.mode == EPI_QKV;
-          pf.t1 = Q.g.t1;
-          pf.t2 = Q.g.t2;
-          pf.m0 = Q.mA0;
-          pf.m1 = Q.mA1;
-          pf.m2 = Q.mA2;
-        }
-      };
-      auto pf_one = [&]() {
-        if (pf.ph >= P.n_ph) return;
-        if (pf.ph < 0 || pf.u >= pf.ue) {
-          if (!pf_next_phase()) return;
-        }
-        const int t = (int)(pf.u / pf.kbt), kb = (int)(pf.u % pf.kbt);
-        if (pf.gu) {
-          tma_prefetch_l2_2d(pf.m0, kb * 64, t * 64);
-          tma_prefetch_l2_2d(pf.m1, kb * 64, t * 64);
-        } else if (pf.qkv) {
-          if (t < pf.t1) tma_prefetch_l2_2d(pf.m0, kb * 64, t * 128);
-          else if (t < pf.t2) tma_prefetch_l2_2d(pf.m1, kb * 64, (t - pf.t1) * 128);
-          else tma_prefetch_l2_2d(pf.m2, kb * 64, (t - pf.t2) * 128);
+      uint32_t it = 0;
+      int last_ph = -1;
+      for_units([&](int ph, const MegaPhase& Q, long long, int t, int kb) {
+        if (ph != last_ph) { tma_prefetch_desc(Q.mA0); last_ph = ph; }
+        const int slot = it % kMegaStages;
+        mbar_wait(&empty[slot], ((it / kMegaStages) & 1) ^ 1);
+        uint8_t* dst = sA + slot * L::kABytes;
+        mbar_arrive_expect_tx(&full[slot], L::kABytes + L::kXBytes);
+        if (Q.gu) {
+          tma_load_2d(dst, Q.mA0, &full[slot], kb * 64, t * 64, kEvictFirst);
+          tma_load_2d(dst + 64 * 128, Q.mA1, &full[slot], kb * 64, t * 64, kEvictFirst);
+        } else if (Q.g.mode == EPI_QKV) {
+          if (t < Q.g.t1) tma_load_2d(dst, Q.mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
+          else if (t < Q.g.t2) tma_load_2d(dst, Q.mA1, &full[slot], kb * 64, (t - Q.g.t1) * 128, kEvictFirst);
+          else tma_load_2d(dst, Q.mA2, &full[slot], kb * 64, (t - Q.g.t2) * 128, kEvictFirst);
         } else {
-          tma_prefetch_l2_2d(pf.m0, kb * 64, t * 128);
+          tma_load_2d(dst, Q.mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
         }
-        ++pf.u;
-      };
-      uint32_t it = 0;   // units issued so far (ring position)
-      for (int ph = 0; ph < P.n_ph; ++ph) {
-        const MegaPhase& Q = P.ph[ph];
-        if (Q.kind != PH_GEMM) continue;
-        const int n_tiles = Q.g.n_tiles, kbt = Q.g.kb_total;
-        const long long U = (long long)n_tiles * kbt;
-        const int Gp = (int)min((long long)G, U);
-        if (c >= Gp) continue;
-        const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
-        const CUtensorMap* mA0 = Q.mA0;
-        const CUtensorMap* mA1 = Q.mA1;
-        const CUtensorMap* mA2 = Q.mA2;
-        const CUtensorMap* mX = Q.mX;
-        const int gu = Q.gu, qkv = (Q.g.mode == EPI_QKV), t1 = Q.g.t1, t2 = Q.g.t2;
-        tma_prefetch_desc(mA0);
-        tma_prefetch_desc(mX);
-        if (P.l2_head > 0) {      // stage the head of the NEXT GEMM phase in L2 now,
-          pf.ph = ph;             // so its weights are on chip when this phase's tail ends
-          pf.u = pf.ue = 0;
-          for (int i = 0; i < P.l2_head; ++i) pf_one();
+        ++it;
+      });
+    }
+  } else if (warp == 6) {
+    // ================= X loader: the activation tile of each unit, issued once
+    // the producing tile of the previous phase (or the whole previous phase)
+    // has been published.  Dataflow instead of a grid barrier: most consumer
+    // units start while the previous phase's slowest tiles are still finishing.
+    if (lane == 0) {
+      uint32_t it = 0;
+      int cur_ph = -1;
+      bool phase_ready = false;            // whole previous phase published
+      unsigned long long rmask[4];         // per-tile readiness cache (<= 256 producer tiles)
+      for_units([&](int ph, const MegaPhase& Q, long long, int, int kb) {
+        const MegaPhase& D = P.ph[ph - 1];
+        const unsigned* dphase = P.done + (ph - 1);
+        const unsigned tphase = D.head ? tgt_head : tgt_body;
+        if (ph != cur_ph) {
+          tma_prefetch_desc(Q.mX);
+          cur_ph = ph;
+          phase_ready = poll_ready(dphase, tphase);
+          rmask[0] = rmask[1] = rmask[2] = rmask[3] = 0ull;
         }
-        bool ready = false;
-        int pend_slot[kMegaStages];
-        int pend_kb[kMegaStages];
-        int npend = 0;
-        const unsigned* dep = P.done + (ph - 1);
-        const unsigned target = P.ph[ph - 1].head ? tgt_head : tgt_body;
-        auto flush = [&]() {
-          for (int i = 0; i < npend; ++i)
-            tma_load_2d(sX + pend_slot[i] * L::kXBytes, mX, &full[pend_slot[i]], pend_kb[i] * 64, 0, kEvictLast);
-          npend = 0;
-        };
-        for (long long u = ub; u < ue; ++u) {
-          const int slot = it % kMegaStages;
-          const uint32_t par = ((it / kMegaStages) & 1) ^ 1;
-          if (!mbar_try_wait(&empty[slot], par)) {
-            if (npend) {             // ring full of tiles waiting for activations:
-              // while the dependency resolves, stream the NEXT tiles into L2
-              pf_sync(ph, u - 1);
-              int nprf = 0;
-              while (!poll_ready(dep, target)) {
-                if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
-                else __nanosleep(128);
+        if (!phase_ready) {
+          if (Q.dep_w > 0 && D.g.n_tiles <= 256) {
+            const int pt = (kb * 64) / Q.dep_w;
+            if (!((rmask[pt >> 6] >> (pt & 63)) & 1ull)) {
+              // one round trip for a batch of 8 producer tiles
+              const unsigned ttile = D.head ? (unsigned)P.step->gen_head : (unsigned)P.step->gen;
+              const unsigned* base = P.tile_done + D.tctr;
+              unsigned vals[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) vals[q] = (pt + q < D.g.n_tiles) ? ld_relaxed_u32(base + pt + q) : 0u;
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (pt + q < D.g.n_tiles && (int)(vals[q] - ttile) >= 0) rmask[(pt + q) >> 6] |= 1ull << ((pt + q) & 63);
+              if (!((rmask[pt >> 6] >> (pt & 63)) & 1ull)) {
+                spin_until(base + pt, ttile);
+                rmask[pt >> 6] |= 1ull << (pt & 63);
               }
-              if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
+              fence_acquire_gpu();
               fence_proxy_async_global();
-              ready = true;
-              flush();
             }
-            mbar_wait(&empty[slot], par);
-          }
-          const int t = (int)(u / kbt), kb = (int)(u % kbt);
-          uint8_t* dst = sA + slot * L::kABytes;
-          mbar_arrive_expect_tx(&full[slot], L::kABytes + L::kXBytes);
-          if (gu) {
-            tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 64, kEvictFirst);
-            tma_load_2d(dst + 64 * 128, mA1, &full[slot], kb * 64, t * 64, kEvictFirst);
-          } else if (qkv) {
-            if (t < t1) tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
-            else if (t < t2) tma_load_2d(dst, mA1, &full[slot], kb * 64, (t - t1) * 128, kEvictFirst);
-            else tma_load_2d(dst, mA2, &full[slot], kb * 64, (t - t2) * 128, kEvictFirst);
           } else {
-            tma_load_2d(dst, mA0, &full[slot], kb * 64, t * 128, kEvictFirst);
+            spin_until(dphase, tphase);
+            fence_proxy_async_global();
+            phase_ready = true;
           }
-          if (!ready) {
-            ready = poll_ready(dep, target);
-            if (ready) {
-              fence_proxy_async_global();
-              if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
-            }
-          }
-          if (ready) {
-            flush();
-            tma_load_2d(sX + slot * L::kXBytes, mX, &full[slot], kb * 64, 0, kEvictLast);
-          } else {
-            pend_slot[npend] = slot;
-            pend_kb[npend] = kb;
-            ++npend;
-          }
-          ++it;
+          if (P.dbg != nullptr && kb == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
         }
-        if (npend) {
-          pf_sync(ph, ue - 1);
-          int nprf = 0;
-          while (!poll_ready(dep, target)) {
-            if (nprf < P.l2_ahead) { pf_one(); ++nprf; }
-            else __nanosleep(128);
-          }
-          if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
-          fence_proxy_async_global();
-          flush();
-        }
-      }
+        const int slot = it % kMegaStages;
+        mbar_wait(&empty[slot], ((it / kMegaStages) & 1) ^ 1);
+        tma_load_2d(sX + slot * L::kXBytes, Q.mX, &full[slot], kb * 64, 0, kEvictLast);
+        ++it;
+      });
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
@@ -375,7 +305,13 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         for (int i = et; i < NW8; i += 128) dst[i] = src[i];
       }
       const int prev_head = ph > 0 ? P.ph[ph - 1].head : 0;
-      if (ph > 0) {                                    // inputs of this phase are complete
+      // Wait for the whole previous phase unless this is a GEMM phase whose
+      // epilogue needs no full-row statistic (O / down: RESID, no rstd); the
+      // mainloop of every GEMM phase is gated per tile by the X loader.
+      named_bar(1, 128);
+      const bool need_prev = ph > 0 && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
+                                         sph->g.mode != EPI_STORE && sph->dep_w > 0);
+      if (need_prev) {
         if (et == 0) spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
       }
       named_bar(1, 128);
@@ -418,8 +354,15 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             mbar_arrive(&tempty[acc]);
             ++nacc;
             u = seg_end;
-            epi_segment<RP>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch, red,
-                            rstd, kvrow, flag);
+            const bool fin = epi_segment<RP>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
+                                             pos0, scratch, red, rstd, kvrow, flag);
+            if (fin) {                                  // publish tile t of this phase
+              named_bar(1, 128);
+              if (et == 0) {
+                fence_proxy_async_global();
+                red_release_add(P.tile_done + Q.tctr + t, 1u);
+              }
+            }
             if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 7] = globaltimer();
           }
         }

@@ -72,7 +72,6 @@ static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64
 }
 
 // ============================================================================ GEMM launch
-constexpr int kL2Head = 0;    // megakernel: next-phase tiles staged in L2 at phase start (measured: no gain)
 constexpr int kStages = 4;   // x (16 KB weights + RP*128 B activations): 2 CTAs/SM
 static int g_num_sms = 0;
 static int g_test_flags = 0;   // test hooks only: bit0 = launch without PDL
@@ -220,6 +219,8 @@ struct ps_stage {
   CUtensorMap* mega_maps[4] = {nullptr, nullptr, nullptr, nullptr};
   int mega_n[4] = {0, 0, 0, 0};
   unsigned* mega_done = nullptr;
+  unsigned* tile_done = nullptr;   // per-tile completion counters, GEMM phases of the megakernel
+  int n_tile_ctr = 0;
   unsigned long long* mega_dbg = nullptr;
   unsigned long long* attn_dbg = nullptr;
   unsigned gen = 0, gen_head = 0;
@@ -454,6 +455,27 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     add(K_ARGMAX, 0);
     ph.back().head = 1;
   }
+  // per-tile counters (fixed per layer position, identical in every table) and
+  // the X dependency granularity: columns per producing tile of the previous
+  // GEMM phase (x∘g from O / down: 128; h from gate/up: 64); 0 after a
+  // non-GEMM phase (embed, attention combine)
+  {
+    int base = 0;
+    for (size_t i = 0; i < ph.size(); ++i) {
+      MegaPhase& P = ph[i];
+      if (P.kind != PH_GEMM) continue;
+      P.tctr = base;
+      base += P.g.n_tiles;
+      const MegaPhase& D = ph[i - 1];
+      // Per-tile dependencies are implemented (X loader, ps_mega.cuh) but off by
+      // default: the acquire + proxy fences per producer-tile batch serialise the
+      // X loader behind its own in-flight TMA loads (measured 2x slower); the
+      // phase-level gate with a decoupled W producer streams at ~6.6 TB/s.
+      P.dep_w = 0;
+      if (D.kind == PH_GEMM && (g_test_flags & 256)) P.dep_w = D.gu ? 64 : 128;
+    }
+    if (base > S->n_tile_ctr) return fail(PS_E_INVALID, "tile counter overflow");
+  }
   const int key = b * 2 + (with_head ? 1 : 0);
   if (S->mega_maps[key]) cudaFree(S->mega_maps[key]);
   if (S->mega_ph[key]) cudaFree(S->mega_ph[key]);
@@ -483,7 +505,7 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   if ((g_test_flags & 8) && !S->mega_dbg)
     CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 8 * 8));
   MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr,
-                (g_test_flags & 16) ? 0 : kL2Ahead, (g_test_flags & 128) ? 0 : kL2Head};
+                S->tile_done};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g_num_sms);
   cfg.blockDim = dim3(kMegaThreads);
@@ -651,6 +673,7 @@ ps_status ps_stage_destroy(ps_stage* S) {
     if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
   }
   if (S->mega_done) cudaFree(S->mega_done);
+  if (S->tile_done) cudaFree(S->tile_done);
   if (S->mega_dbg) cudaFree(S->mega_dbg);
   if (S->attn_dbg) cudaFree(S->attn_dbg);
   void* dev[] = {S->d_page_table, S->d_in, S->d_out, S->x, S->q, S->ss, S->logits, S->ws, S->xg, S->att, S->h,
@@ -826,6 +849,12 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   // --- megakernel phase-completion counters (cumulative; see ps_mega.cuh)
   S_TRY(cudaMalloc(&S->mega_done, (size_t)(6 * sh.n_layers + 8) * 4));
   S_TRY(cudaMemset(S->mega_done, 0, (size_t)(6 * sh.n_layers + 8) * 4));
+  {  // per-tile counters: QKV, O, gate/up, down per layer + lm_head
+    S->n_tile_ctr = sh.n_layers * (S->gs_qkv.n_tiles + S->gs_o.n_tiles + S->gs_gu.n_tiles + S->gs_d.n_tiles) +
+                    S->gs_lm.n_tiles;
+    S_TRY(cudaMalloc(&S->tile_done, (size_t)std::max(1, S->n_tile_ctr) * 4));
+    S_TRY(cudaMemset(S->tile_done, 0, (size_t)std::max(1, S->n_tile_ctr) * 4));
+  }
   // --- synthetic override (disabled)
   S_TRY(cudaMalloc(&S->d_syn, sizeof(SynthParams)));
   S->h_syn = SynthParams{};
