@@ -164,6 +164,11 @@ PS_DEV unsigned long long warp_max_u64(unsigned long long v) {
 }
 // Release / acquire at GPU scope (lighter than __threadfence()'s fence.sc.gpu).
 PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+PS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 PS_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 // Greedy key: larger logit wins, equal logits -> lower index wins (reading R12).

@@ -226,14 +226,14 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       for (int j = 0; j < V4; ++j)
         if (j < R4)
           __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-      fence_acq_rel_gpu();
+      // all partial stores of the CTA are ordered before thread 0's release by
+      // the barrier; the acquire side of the same atomic orders the reducer's
+      // loads (grid-sync pattern: one gpu-scope acq_rel atomic per CTA)
       named_bar(1, 128);
-      if (e == 0) *flag = (atomicAdd(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
+      if (e == 0) *flag = (atom_add_acq_rel_gpu(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
       named_bar(1, 128);
-      const int last = *flag;
-      named_bar(1, 128);
+      const int last = *flag;   // rewritten only after the next segment's first barrier
       if (!last) break;
-      fence_acq_rel_gpu();
       // reduce: only the live rows, with up to 16 float4 loads in flight
       if (R4 <= 1) sk_reduce<RP, 1>(wsp, v, e, seg, nseg);
       else if (R4 <= 2) sk_reduce<RP, 2>(wsp, v, e, seg, nseg);
