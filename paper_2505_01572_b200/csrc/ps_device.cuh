@@ -164,6 +164,21 @@ PS_DEV unsigned long long warp_max_u64(unsigned long long v) {
 }
 // Release / acquire at GPU scope (lighter than __threadfence()'s fence.sc.gpu).
 PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+PS_DEV void red_release_add_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Wait until *p >= target (relaxed polls with back-off, then one acquire fence).
+PS_DEV void spin_until_gpu(const unsigned* p, unsigned target) {
+  unsigned ns = 20;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if ((int)(v - target) >= 0) break;
+    __nanosleep(ns);
+    ns = ns < 160 ? ns * 2 : 160;
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 PS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

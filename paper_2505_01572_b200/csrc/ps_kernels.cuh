@@ -222,24 +222,35 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
       constexpr int V4 = RP / 4;
       const int R4 = (R + 3) >> 2;               // float4s per thread that hold live rows
+      if (seg != 0) {
 #pragma unroll
-      for (int j = 0; j < V4; ++j)
-        if (j < R4)
-          __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-      // all partial stores of the CTA are ordered before thread 0's release by
-      // the barrier; the acquire side of the same atomic orders the reducer's
-      // loads (grid-sync pattern: one gpu-scope acq_rel atomic per CTA)
+        for (int j = 0; j < V4; ++j)
+          if (j < R4)
+            __stcg(&wsp[((size_t)seg * 128 + e) * V4 + j], make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+      }
+      // Static reducer: segment 0's CTA (its range ENDS in this tile, so it
+      // reaches this tile last anyway) waits for the other nseg-1 segments;
+      // they publish with a fire-and-forget release add (no round trip) after
+      // a barrier that orders all 128 threads' partial stores before it.
+      if (seg != 0) {
+        named_bar(1, 128);
+        if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+        if (e == 0) red_release_add_gpu(&p.counters[t], 1u);
+        break;
+      }
+      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+      if (e == 0) {
+        spin_until_gpu(&p.counters[t], (unsigned)(nseg - 1));
+        p.counters[t] = 0u;                    // ready for the next forward
+      }
       named_bar(1, 128);
-      if (e == 0) *flag = (atom_add_acq_rel_gpu(&p.counters[t], 1u) == (unsigned)(nseg - 1)) ? 1 : 0;
-      named_bar(1, 128);
-      const int last = *flag;   // rewritten only after the next segment's first barrier
-      if (!last) break;
+      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 1] = globaltimer();
       // reduce: only the live rows, with up to 16 float4 loads in flight
       if (R4 <= 1) sk_reduce<RP, 1>(wsp, v, e, seg, nseg);
       else if (R4 <= 2) sk_reduce<RP, 2>(wsp, v, e, seg, nseg);
       else if (R4 <= 4) sk_reduce<RP, 4>(wsp, v, e, seg, nseg);
       else sk_reduce<RP, (RP / 4 < 8 ? RP / 4 : 8)>(wsp, v, e, seg, nseg);
-      if (e == 0) p.counters[t] = 0u;
+      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 2] = globaltimer();
     }
 
     // ---- fused epilogues (global loads batched ahead of use) ----
@@ -352,6 +363,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       named_bar(1, 128);
     }
     finalized = true;
+    if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 3] = globaltimer();
   } while (0);
   return finalized;   // this CTA completed tile t (its outputs are written)
 }

@@ -222,6 +222,7 @@ struct ps_stage {
   unsigned* tile_done = nullptr;   // per-tile completion counters, GEMM phases of the megakernel
   int n_tile_ctr = 0;
   unsigned long long* mega_dbg = nullptr;
+  unsigned long long* epi_dbg = nullptr;
   unsigned long long* attn_dbg = nullptr;
   unsigned gen = 0, gen_head = 0;
   StepOut* d_out = nullptr;
@@ -481,6 +482,10 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
   if (S->mega_ph[key]) cudaFree(S->mega_ph[key]);
   CU_TRY(cudaMalloc(&S->mega_maps[key], std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
   CU_TRY(cudaMemcpy(S->mega_maps[key], maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  if (g_test_flags & 8) {   // test: per-phase epilogue stamps [phase][cta][4]
+    if (!S->epi_dbg) CU_TRY(cudaMalloc(&S->epi_dbg, (size_t)(6 * S->sh.n_layers + 8) * g_num_sms * 4 * 8));
+    for (size_t i = 0; i < ph.size(); ++i) ph[i].g.dbg = S->epi_dbg + i * g_num_sms * 4;
+  }
   const CUtensorMap* dm = S->mega_maps[key];
   for (auto& P : ph) {
     if (P.kind != PH_GEMM) continue;
@@ -1256,6 +1261,7 @@ extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t
     case 7: src = S->attn_ml; break;
     case 8: src = S->d_page_table; break;
     case 9: src = S->mega_dbg; break;
+    case 11: src = S->epi_dbg; break;
     case 10: src = S->attn_dbg; break;
     default: return fail(PS_E_INVALID, "unknown buffer %d", which);
   }
