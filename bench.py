@@ -106,6 +106,20 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def aggregate(dev_s, wall_s, tokens, world, device="cpu"):
+    """Whole-job numbers over ranks: times are the MAX over ranks (the job ends
+    when its slowest replica does), tokens the SUM (weak scaling)."""
+    if world <= 1:
+        return dev_s, wall_s, float(tokens)
+    import torch
+    import torch.distributed as dist
+    times = torch.tensor([dev_s, wall_s], device=device, dtype=torch.float64)
+    tok = torch.tensor([float(tokens)], device=device, dtype=torch.float64)
+    dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+    return float(times[0]), float(times[1]), float(tok[0])
+
+
 def oracle_sample(draft_shape, target_shape, wd, wt, gamma, alpha, seed, n_rounds, ctx=64, layers=2):
     """The fp64 oracle (as it stands) on the host cores: sync-SD rounds of the
     same two shapes at `layers` of their L layers (full width and vocab), ctx
@@ -270,14 +284,7 @@ def main():
     launches = L.ps_kernel_launch_count() - launches0
     dev_s = t0e.elapsed_time(t1e) / 1e3
     wall_s = w1 - w0
-    if world > 1:
-        t = torch.tensor([dev_s, wall_s, float(tokens)], device="cuda", dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[2:], op=dist.ReduceOp.SUM)
-        dev_s, wall_s, tot_tokens = float(mx[0]), float(mx[1]), float(t[2])
-    else:
-        tot_tokens = float(tokens)
+    dev_s, wall_s, tot_tokens = aggregate(dev_s, wall_s, tokens, world, device="cuda")
 
     # --- dominant kernel: M_1's verify forward = ONE persistent megakernel launch
     # (embed, 32 x {QKV, attention, combine, O, gate/up, down}, lm_head, argmax);

@@ -201,3 +201,37 @@ def test_megakernel_equals_per_kernel_path(name, layers):
     (t1, (a1, n1, l1)), (t2, (a2, n2, l2)) = outs
     assert t1 == t2 and (a1, n1) == (a2, n2)
     assert np.array_equal(l1, l2)
+
+
+@pytest.mark.slow
+def test_bench_config_self_consistency():
+    """BASELINE configs[1] at full size (LLaMA-3.2-1B -> LLaMA-3.1-8B shapes,
+    512-token prompt, bench.py's launch configuration): properties that hold at
+    any size -- sync-SD and async PipeSpec output == M_K autoregressive output,
+    and a verify over w accepted drafts reproduces the AR logits bit-exactly."""
+    from paper_2505_01572_b200 import Stage, pipeline_run
+    from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
+    ds, ts = synth.preset("llama3.2-1b"), synth.preset("llama3.1-8b")
+    wd = synth.make_weights(ds, seed=0, device="cuda")
+    wt = synth.make_weights(ts, seed=1, device="cuda")
+    d = Stage(ds, wd, max_seq=700, max_window=8)
+    t = Stage(ts, wt, max_seq=700, max_window=8)
+    prompt = [int(x) for x in synth.make_prompt(ts.vocab, 512, seed=17)]
+    ar, _ = pipeline_run([d, t], prompt, 48, mode=PS_MODE_AR)
+    d.set_synthetic(ar + [0] * 16, 512, level=0, top=1, alphas=[0.8], seed=1234)
+    sd, st = pipeline_run([d, t], prompt, 48, mode=PS_MODE_SYNC_SD, gammas=[0, 8])
+    assert sd == ar and st.verify_steps[1] >= 1
+    ps, _ = pipeline_run([d, t], prompt, 48, mode=PS_MODE_PIPESPEC, gammas=[0, 8])
+    assert ps == ar
+    # row-bucket invariance at full size: AR rows vs one verify of 8 accepted drafts
+    t.prefill(prompt)
+    rows = []
+    for _ in range(9):
+        a, nxt, lg = t.verify([], want_logits=True)
+        rows.append(lg[0])
+    t.prefill(prompt)
+    a, nxt, lg = t.verify(ar[:8], want_logits=True)
+    assert a == 8 and nxt == ar[8]
+    assert np.array_equal(lg, np.stack(rows))
+    d.close()
+    t.close()
