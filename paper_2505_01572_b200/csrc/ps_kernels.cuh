@@ -662,8 +662,43 @@ PS_DEV uint32_t pack_bf16(float lo, float hi) {
 // NW warps (16 query rows each) of one CTA run the work items
 // item = cta, cta + ncta, ...; `bar` is the named barrier id for the NW*32
 // participating threads (tid in [0, NW*32)).
+// Issue (cp.async, one commit group) the K/V chunk of this CTA's first work
+// item if it lies wholly in the context (positions < pos0: not rewritten by the
+// coming QKV phase).  Returns the prefetched item id, or -1.
+template <int HD, int NW>
+PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* attn_smem, int tid, int cta) {
+  constexpr int kRB = NW * 16, NT = NW * 32, LD = HD + kAttnPad, VPR = HD / 8;
+  const StepIn* st = p.step;
+  const int R = st->R, pos0 = st->pos0;
+  const int rows = R * (p.H / p.hkv);
+  const int n_rb = (rows + kRB - 1) / kRB;
+  const int nchunks = (pos0 + R + kAttnChunk - 1) / kAttnChunk;
+  if (cta >= p.hkv * n_rb * nchunks) return -1;
+  const int c = cta % nchunks, kh = cta / (nchunks * n_rb);
+  const int k0 = c * kAttnChunk;
+  if (k0 + kAttnChunk > pos0) return -1;
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_smem) + kRB * LD;
+  __nv_bfloat16* sV = sK + kAttnChunk * LD;
+  const long long page = p.page_table[k0 / p.page_size];
+  const int slot0 = k0 % p.page_size;
+  const __nv_bfloat16* Kp = p.kv + (size_t)page * p.page_stride +
+                            ((size_t)((p.layer * 2 + 0) * p.hkv + kh) * p.page_size + slot0) * HD;
+  const __nv_bfloat16* Vp = p.kv + (size_t)page * p.page_stride +
+                            ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
+  for (int i = tid; i < kAttnChunk * VPR; i += NT) {
+    const int row = i / VPR, cv = i % VPR;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sK + row * LD + cv * 8)),
+                 "l"(Kp + (size_t)row * HD + cv * 8) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sV + row * LD + cv * 8)),
+                 "l"(Vp + (size_t)row * HD + cv * 8) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  return cta;
+}
+
 template <int HD, int NW, bool kInlineCombine = true>
-PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, int ncta, int bar) {
+PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, int ncta, int bar,
+                     int pref_item = -1) {
   constexpr int kRB = NW * 16;                          // query rows per block
   constexpr int NT = NW * 32;
   constexpr int LD = HD + kAttnPad;                     // smem row stride (elements)
@@ -700,7 +735,8 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
                               ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
     constexpr int VPR = HD / 8;                          // 16-byte vectors per row
     // K/V chunk: cp.async (16 B, zero-fill past nk) -- every copy in flight at once
-    for (int i = tid; i < kAttnChunk * VPR; i += NT) {
+    // (skipped when it was prefetched during the QKV phase)
+    for (int i = (item == pref_item) ? kAttnChunk * VPR : tid; i < kAttnChunk * VPR; i += NT) {
       const int row = i / VPR, cv = i % VPR;
       const int ok = row < nk ? 16 : 0;
       const __nv_bfloat16* ksrc = Kp + (size_t)(row < nk ? row : 0) * HD + cv * 8;

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     const int e = quarter * 32 + lane;
     const int et = threadIdx.x - 64;                   // 0..127 in warp order 2..5
     uint32_t nacc = 0;
+    int pref_item = -1;                                // attention chunk prefetched during QKV
     const StepIn* st = P.step;
     const int R = st->R;
     const int pos0 = st->pos0;
@@ -321,8 +322,9 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1);
-        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1);
+        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        pref_item = -1;
       } else if (kind == PH_ACOMB) {
         if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
         else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
@@ -333,6 +335,13 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const int kbt = gp.kb_total;
         const long long U = (long long)gp.n_tiles * kbt;
         const int Gp = (int)min((long long)G, U);
+        if (gp.mode == EPI_QKV && ph + 1 < P.n_ph && P.ph[ph + 1].kind == PH_ATTN) {
+          // the attention phase's context K/V does not depend on this phase:
+          // stream this CTA's first chunk into smem while QKV runs
+          const AttnParams& an = P.ph[ph + 1].a;
+          pref_item = an.hd == 128 ? attn_prefetch_kv<128, 4>(an, attn_smem, et, c)
+                                   : attn_prefetch_kv<64, 4>(an, attn_smem, et, c);
+        }
         if (c < Gp) {
           epi_prepare<RP>(gp, e, R, pos0, scratch, rstd, kvrow);
           const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
