@@ -235,3 +235,41 @@ def test_bench_config_self_consistency():
     assert np.array_equal(lg, np.stack(rows))
     d.close()
     t.close()
+
+
+def test_long_context_many_attention_items():
+    """LLaMA-68M shape (12 KV heads) at ~2K context: more attention work items
+    than CTAs (strided item loop), 33 chunks per row combined; parity vs oracle."""
+    s, wt, st = make("llama-68m", 3, max_seq=2200)
+    w64 = synth.weights_to_numpy(wt)
+    prompt = list(synth.make_prompt(s.vocab, 2040, seed=4))
+    st.prefill(prompt)
+    stream = st.draft(6)
+    st.prefill(prompt)
+    window = stream[:3] + [(stream[3] + 7) % s.vocab] + stream[4:5]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
+
+
+def test_70b_width_one_layer():
+    """LLaMA-3.1-70B widths (d=8192, 64/8 heads, ffn 28672; vocab cut to 32000
+    to bound the oracle's RAM): GQA g=8 -> 4 attention row blocks at R=32."""
+    from dataclasses import replace
+    s = replace(synth.preset("llama3.1-70b"), n_layers=1, vocab=32000)
+    from paper_2505_01572_b200 import Stage
+    wt = synth.make_weights(s, seed=5, device="cuda")
+    st = Stage(s, wt, max_seq=200)
+    w64 = synth.weights_to_numpy(wt)
+    prompt = list(synth.make_prompt(s.vocab, 80, seed=6))
+    st.prefill(prompt)
+    stream = st.draft(31)
+    st.prefill(prompt)
+    window = stream[:31]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
