@@ -309,10 +309,11 @@ def main():
     except Exception:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
+    traffic, draft_traffic = None, None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get("verify_megakernel_8b_r9", {}).get("dram_bytes_per_launch")
+        traffic = tr.get("verify_megakernel_8b_r5", {}).get("dram_bytes_per_launch")
+        draft_traffic = tr.get("draft_megakernel_1b_r1", {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     step_ms = 1e3 * dev_s / args.steps
@@ -349,7 +350,8 @@ def main():
         "tokens_per_step": tot_tokens / world / args.steps,
         "verify_pass": {"ms": pass_ms, "rows": R, "ctx": ctx, "bytes": pass_bytes, "GB/s": pass_gbs,
                         "frac": pass_gbs / peak},
-        "draft_step": {"ms": draft_ms, "rows": 1, "bytes": draft_bytes, "GB/s": draft_gbs, "frac": draft_gbs / peak},
+        "draft_step": {"ms": draft_ms, "rows": 1, "bytes": draft_bytes, "GB/s": draft_gbs, "frac": draft_gbs / peak,
+                       "traffic": draft_traffic},
         "kernel_share_of_step": share,
         "roofline": {"kernel": "M_1 verify forward: persistent tcgen05/TMA megakernel (1 launch per pass)",
                      "bound": "hbm", "achieved": pass_gbs, "peak": peak, "unit": "GB/s", "frac": pass_gbs / peak,

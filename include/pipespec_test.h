@@ -27,7 +27,15 @@ ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N
  * memory, `iters` back-to-back launches; *avg_ms per launch. */
 ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters, int32_t flags,
                                   float* avg_ms);
-/* Test-only launch flags (bit0: launch GEMMs without programmatic dependent launch). */
+/* Test/profiling flags (process-wide; 0 = production behaviour):
+ *   bit0  per-step path: launch GEMMs without programmatic dependent launch
+ *   bit1  ps_test_gemm*: skip TMA loads        bit2  ps_test_gemm*: skip MMAs
+ *   bit3  megakernel: record %globaltimer phase stamps (ps_test_read 9) and
+ *         stream-K fixup stamps (ps_test_read 11); takes effect for stages
+ *         created / tables built afterwards
+ *   bit5  megakernel: 4-stage ring variant
+ *   bit6  attention: per-item stage stamps (ps_test_read 10)
+ *   bit8  megakernel: per-tile dataflow dependencies (experimental, slower) */
 void ps_test_set_flags(int32_t flags);
 
 /* Re-launch one kernel of the stage's most recent forward configuration
@@ -41,7 +49,8 @@ ps_status ps_time_kernel(ps_stage* stage, int32_t kind, int32_t layer, int32_t i
  * stream).  which: 0 x (fp32 [32,d]), 1 x∘g (bf16 [32,d]), 2 q (fp32 [32,H*hd]),
  * 3 attention out (bf16 [32,H*hd]), 4 SwiGLU out (bf16 [32,ffn]),
  * 5 sumsq slots (fp32 [32,ceil(d/128)]), 6 KV pool, 7 attention (m,l) partials,
- * 8 device page table (int32). */
+ * 8 device page table (int32), 9 megakernel phase stamps, 10 attention stamps,
+ * 11 stream-K fixup stamps. */
 ps_status ps_test_read(ps_stage* stage, int32_t which, void* dst, int64_t bytes);
 
 #ifdef __cplusplus

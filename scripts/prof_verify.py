@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="llama3.1-8b")
 ap.add_argument("--layers", type=int, default=None)
 ap.add_argument("--ctx", type=int, default=512)
-ap.add_argument("--w", type=int, default=8)
+ap.add_argument("--w", type=int, default=4)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--graphs", type=int, default=1)
 a = ap.parse_args()
