@@ -79,11 +79,29 @@ typedef struct ps_weights {
   const void* const* layers;
 } ps_weights;
 
-/* Device placement.  Tensor parallelism (tp_size > 1) is reserved for the
- * multi-GPU build; this build accepts tp_size == 1 only (else PS_E_INVALID). */
+/* Device placement.  Tensor parallelism inside a stage (
+ * the paper only says the 70B was "split across 2 GPUs", reading R18):
+ * tp_size in 1..8 ranks, each a stage of its own (one per GPU, or several on
+ * one GPU with opts.max_ctas partitioning the SMs), created with the FULL
+ * model shape and this rank's weight SHARDS (Megatron layout):
+ *   wq/wk/wv: query / KV heads [r*H/T, (r+1)*H/T) rows;  wg/wu: d_ffn rows
+ *   [r*F/T, ...);  wo, wd: the matching input COLUMNS (row-parallel);
+ *   lm_head: vocabulary rows [r*V/T, (r+1)*V/T);  embed and the norm gains
+ *   replicated.  Requires n_heads, n_kv_heads, vocab divisible by T, d_ffn by
+ *   64*T, d_model by 128, use_megakernel = 1.
+ * The O and down projections each end in an all-reduce of the [R, d] partials
+ * and the lm_head in a max over the ranks' greedy keys; both run INSIDE the
+ * megakernel over peer memory (no NCCL call): every rank publishes its
+ * partial in its exchange buffer, then reads all T in rank order, so every
+ * rank holds bit-identical activations and takes the same (a, next).  The
+ * ranks of a group must run the same call sequence (ps_prefill / ps_verify /
+ * ps_draft / ps_resync / ps_kv_rollback) concurrently, one host thread or
+ * process each.  Before the first forward connect the group with
+ * ps_tp_connect (one process per GPU, CUDA IPC handles) or
+ * ps_tp_connect_local (ranks in one process).  nccl_comm is unused. */
 typedef struct ps_placement {
   int32_t device;           /* CUDA ordinal */
-  void* nccl_comm;          /* NULL, or a torch ProcessGroupNCCL _comm_ptr */
+  void* nccl_comm;          /* reserved, NULL */
   int32_t tp_rank, tp_size;
 } ps_placement;
 
@@ -102,12 +120,16 @@ typedef struct ps_stage_opts {
   int32_t use_graphs;       /* 1: capture one CUDA graph per rows bucket      */
   int32_t use_megakernel;   /* 1: whole forward as one persistent cooperative
                                kernel (ps_mega.cuh); 0: one kernel per step   */
+  int32_t max_ctas;         /* megakernel CTAs (one per SM), 0 = every SM; a
+                               smaller grid leaves SMs to concurrent stages  */
 } ps_stage_opts;
 
 typedef struct ps_stage ps_stage;
 
-/* Bytes of KV pool a stage of this shape needs for max_seq tokens. */
+/* Bytes of KV pool a stage of this shape needs for max_seq tokens
+ * (_tp: one rank of a tp_size group, which holds n_kv_heads / tp_size heads). */
 int64_t ps_kv_pool_bytes(const ps_model_shape* shape, int32_t max_seq, int32_t page_size);
+int64_t ps_kv_pool_bytes_tp(const ps_model_shape* shape, int32_t max_seq, int32_t page_size, int32_t tp_size);
 
 /* Create a stage: validates the shape, builds TMA descriptors over the
  * borrowed weights, allocates scratch, and (optionally) captures graphs.
@@ -116,6 +138,19 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* weights
                           const ps_placement* placement, const ps_stage_opts* opts,
                           ps_stage** out);
 ps_status ps_stage_destroy(ps_stage* stage);
+
+/* Tensor-parallel group wiring (see ps_placement).  PS_TP_HANDLE_BYTES is the
+ * size of one exported handle (a cudaIpcMemHandle_t of the rank's exchange
+ * buffer).  ps_tp_handle writes this rank's handle; ps_tp_connect takes all
+ * tp_size handles in rank order (host array [tp_size][PS_TP_HANDLE_BYTES],
+ * this rank's own entry ignored) and maps the peers' buffers, enabling peer
+ * access; ps_tp_connect_local links n stages created in THIS process (rank
+ * order = array order, n == their tp_size).  A forward on an unconnected
+ * tp_size > 1 stage returns PS_E_INVALID. */
+#define PS_TP_HANDLE_BYTES 64
+ps_status ps_tp_handle(ps_stage* stage, void* handle_out);
+ps_status ps_tp_connect(ps_stage* stage, const void* handles);
+ps_status ps_tp_connect_local(ps_stage* const* stages, int32_t n);
 
 /* O_i := tokens[0:n] (host, n >= 1, every token < vocab, n <= max_seq).
  * Keeps the KV of the longest common prefix with the current O_i, then runs
@@ -150,6 +185,8 @@ ps_status ps_draft(ps_stage* stage, int32_t n_steps, int32_t* out_tokens);
  * opt_logits: NULL, or host/device float [w+1][vocab] receiving the rows'
  * logits.  Errors: w > max_window or token >= vocab -> PS_E_INVALID;
  * n + w > max_seq or no page -> PS_E_CAPACITY; empty O_i -> PS_E_CONTRACT. */
+/* (Tensor parallel: opt_logits receives this rank's [w+1][vocab/tp_size]
+ * vocabulary slice; a and next are the group's.) */
 ps_status ps_verify(ps_stage* stage, const int32_t* window, int32_t w,
                     int32_t* accepted_len, int32_t* next_token, float* opt_logits);
 

@@ -6,4 +6,5 @@ the import of `stage` fails, and without an sm_100a GPU every call raises
 PipeSpecError(PS_E_CUDA).
 """
 from .abi import PipeSpecError  # noqa: F401
-from .stage import Stage, pipeline_run, kv_pool_bytes, model_shape  # noqa: F401
+from .stage import (Stage, pipeline_run, kv_pool_bytes, model_shape, shard_weights,  # noqa: F401
+                    tp_connect_local, tp_connect_group)

@@ -17,6 +17,7 @@ STATUS_NAMES = {0: "PS_OK", -1: "PS_E_INVALID", -2: "PS_E_CONTRACT", -3: "PS_E_C
                 -5: "PS_E_NCCL", -6: "PS_E_STALE"}
 PS_WQ, PS_WK, PS_WV, PS_WO, PS_WG, PS_WU, PS_WD, PS_N_ATTN, PS_N_MLP, PS_LAYER_SLOTS = range(10)
 PS_MODE_AR, PS_MODE_SYNC_SD, PS_MODE_PIPESPEC = 0, 1, 2
+PS_TP_HANDLE_BYTES = 64
 
 
 class PipeSpecError(RuntimeError):
@@ -45,7 +46,7 @@ class Placement(C.Structure):
 class StageOpts(C.Structure):
     _fields_ = [("max_seq", C.c_int32), ("max_window", C.c_int32), ("page_size", C.c_int32),
                 ("kv_pool", C.c_void_p), ("kv_pool_bytes", C.c_int64), ("stream", C.c_void_p),
-                ("use_graphs", C.c_int32), ("use_megakernel", C.c_int32)]
+                ("use_graphs", C.c_int32), ("use_megakernel", C.c_int32), ("max_ctas", C.c_int32)]
 
 
 class StageInfo(C.Structure):
@@ -71,6 +72,10 @@ _PROTOS = {
     "ps_version": (C.c_int32, []),
     "ps_kernel_launch_count": (C.c_int64, []),
     "ps_kv_pool_bytes": (C.c_int64, [C.POINTER(ModelShape), C.c_int32, C.c_int32]),
+    "ps_kv_pool_bytes_tp": (C.c_int64, [C.POINTER(ModelShape), C.c_int32, C.c_int32, C.c_int32]),
+    "ps_tp_handle": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "ps_tp_connect": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "ps_tp_connect_local": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32]),
     "ps_stage_create": (C.c_int32, [C.POINTER(ModelShape), C.POINTER(Weights), C.POINTER(Placement),
                                     C.POINTER(StageOpts), C.POINTER(C.c_void_p)]),
     "ps_stage_destroy": (C.c_int32, [C.c_void_p]),

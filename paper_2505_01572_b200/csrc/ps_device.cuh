@@ -167,17 +167,46 @@ PS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"
 PS_DEV void red_release_add_gpu(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Every in-kernel wait is bounded: a wait that outlives kSpinLimitNs (a peer
+// rank that never arrives, a scheduling deadlock) traps instead of hanging the
+// GPU; the host sees a CUDA error.  Checked once per 1024 polls.
+constexpr unsigned long long kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+PS_DEV void spin_check(unsigned& polls, unsigned long long& t0) {
+  if ((++polls & 1023u) != 0u) return;
+  const unsigned long long now = globaltimer();
+  if (t0 == 0ull) t0 = now;
+  else if (now - t0 > kSpinLimitNs) __trap();
+}
 // Wait until *p >= target (relaxed polls with back-off, then one acquire fence).
 PS_DEV void spin_until_gpu(const unsigned* p, unsigned target) {
-  unsigned ns = 20;
+  unsigned ns = 20, polls = 0;
+  unsigned long long t0 = 0;
   for (;;) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     if ((int)(v - target) >= 0) break;
     __nanosleep(ns);
     ns = ns < 160 ? ns * 2 : 160;
+    spin_check(polls, t0);
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// System scope (tensor-parallel peers on other GPUs, NVLink peer memory).
+PS_DEV void red_release_add_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PS_DEV void spin_until_sys(const unsigned* p, unsigned target) {
+  unsigned ns = 32, polls = 0;
+  unsigned long long t0 = 0;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if ((int)(v - target) >= 0) break;
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+    spin_check(polls, t0);
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 PS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
   unsigned old;

@@ -84,6 +84,8 @@ struct GemmParams {
   // EPI_LMHEAD
   float* logits; int ld_logits;
   unsigned long long* amax; int amax_ld;
+  int vocab_off;                   // tensor parallel: first vocabulary id of this rank's slice
+  int amax_par;                    // 1: amax has two [kMaxRows] slots selected by gen_head parity
   // EPI_STORE
   float* out; int ld_out;
   // stream-K fixup
@@ -350,7 +352,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       for (int r = 0; r < RP; ++r) {
         const float z = v[r] * rstd[r];
         if (want && ok && r < R) p.logits[(size_t)r * p.ld_logits + f] = z;
-        unsigned long long k = ok ? argmax_key(z, (uint32_t)f) : 0ull;
+        unsigned long long k = ok ? argmax_key(z, (uint32_t)(f + p.vocab_off)) : 0ull;
         k = warp_max_u64(k);
         if (lane == 0) red[quarter * RP + r] = k;
       }
@@ -358,7 +360,8 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       if (e < R) {
         unsigned long long k = red[e];
         for (int q = 1; q < 4; ++q) k = red[q * RP + e] > k ? red[q * RP + e] : k;
-        atomicMax(&p.amax[e], k);
+        unsigned long long* am = p.amax_par ? p.amax + (p.step->gen_head & 1) * kMaxRows : p.amax;
+        atomicMax(&am[e], k);
       }
       named_bar(1, 128);
     }
@@ -607,6 +610,43 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Embe
   const int r = blockIdx.x;
   if (r >= p.step->R) return;
   embed_row(p, r, threadIdx.x);
+}
+
+// ------------------------------------------------------------------ tensor-parallel reduce (a14)
+// Row-parallel O / down projections leave each rank a partial [R, d] (fp32, in
+// its exchange buffer).  Every rank sums the T partials in rank order (so all
+// ranks hold bit-identical x), adds the residual, and writes the next RMSNorm
+// operand x∘g and the per-128-column sums of squares -- the EPI_RESID epilogue
+// of the single-GPU path with the all-reduce folded in.
+struct TpParams {
+  const float* part[8];            // rank q's partial [kMaxRows][d] (peer memory for q != rank)
+  int n;                           // tp_size
+  float* x; int ld_x;
+  __nv_bfloat16* xg; int ld_xg; const __nv_bfloat16* gain;
+  float* ss_out; int ss_out_ld;
+  int d;
+};
+
+// One unit = (row r, 128-column tile t), one warp: 4 columns per lane.
+PS_DEV void tp_reduce_unit(const TpParams& p, int r, int t, int lane) {
+  const int f = t * 128 + lane * 4;
+  const size_t off = (size_t)r * p.d + f;
+  const float4 xo = *reinterpret_cast<const float4*>(p.x + (size_t)r * p.ld_x + f);
+  float4 s = __ldcg(reinterpret_cast<const float4*>(p.part[0] + off));
+  for (int q = 1; q < p.n; ++q) {    // rank order: ((p_0 + p_1) + p_2) + ...
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(p.part[q] + off));
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  const float4 xn = make_float4(xo.x + s.x, xo.y + s.y, xo.z + s.z, xo.w + s.w);
+  *reinterpret_cast<float4*>(p.x + (size_t)r * p.ld_x + f) = xn;
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(p.gain + f);
+  const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(p.xg + (size_t)r * p.ld_xg + f);
+  o2[0] = __floats2bfloat162_rn(xn.x * ga.x, xn.y * ga.y);
+  o2[1] = __floats2bfloat162_rn(xn.z * gb.x, xn.w * gb.y);
+  float sq = xn.x * xn.x + xn.y * xn.y + xn.z * xn.z + xn.w * xn.w;
+  sq = warp_sum(sq);
+  if (lane == 0) p.ss_out[(size_t)r * p.ss_out_ld + t] = sq;
 }
 
 // ------------------------------------------------------------------ attention (a6)
@@ -987,6 +1027,10 @@ struct ArgmaxParams {
   StepOut* out;            // device
   StepOut* mirror;         // mapped pinned host memory (zero-copy), may be null
   const SynthParams* syn;  // may be null
+  // tensor parallel (tp_n > 1): every rank's per-row keys, two parity slots
+  // [2][kMaxRows] each (slot = gen_head & 1); amax is this rank's own block
+  int tp_n;
+  const unsigned long long* tp_keys[8];
 };
 
 PS_DEV int synth_token(const SynthParams* sp, int p) {
@@ -1011,9 +1055,27 @@ template <int NT>
 PS_DEV void argmax_run(const ArgmaxParams& p, int tid, int* s_pred, int bar) {
   const StepIn* st = p.step;
   const int R = st->R;
-  for (int row = tid; row < R; row += NT) {
-    s_pred[row] = (int)argmax_key_idx(__ldcg(&p.amax[row]));
-    p.amax[row] = 0ull;                  // reset the atomicMax slot for the next forward
+  if (p.tp_n > 1) {
+    // vocab-parallel lm_head: max over the ranks' keys (exact, order-free); the
+    // other parity slot (previous head forward, read by every peer before this
+    // forward's lm_head could complete on it) is reset for the next forward
+    const int par = st->gen_head & 1;
+    for (int row = tid; row < kMaxRows; row += NT) {
+      if (row < R) {
+        unsigned long long k = 0ull;
+        for (int q = 0; q < p.tp_n; ++q) {
+          const unsigned long long kq = __ldcg(p.tp_keys[q] + par * kMaxRows + row);
+          k = kq > k ? kq : k;
+        }
+        s_pred[row] = (int)argmax_key_idx(k);
+      }
+      p.amax[(par ^ 1) * kMaxRows + row] = 0ull;
+    }
+  } else {
+    for (int row = tid; row < R; row += NT) {
+      s_pred[row] = (int)argmax_key_idx(__ldcg(&p.amax[row]));
+      p.amax[row] = 0ull;                // reset the atomicMax slot for the next forward
+    }
   }
   named_bar(bar, NT);
   if (tid == 0) {

@@ -24,7 +24,7 @@
 
 namespace ps {
 
-enum { PH_EMBED = 0, PH_GEMM = 1, PH_ATTN = 2, PH_ARGMAX = 3, PH_ACOMB = 4 };
+enum { PH_EMBED = 0, PH_GEMM = 1, PH_ATTN = 2, PH_ARGMAX = 3, PH_ACOMB = 4, PH_TPRED = 5 };
 
 struct MegaPhase {
   int kind;
@@ -33,6 +33,8 @@ struct MegaPhase {
   int tctr;                        // GEMM: base index of this phase's per-tile completion counters
   int dep_w;                       // GEMM: X columns per producing tile of the previous (GEMM) phase;
                                    // 0 = the X operand waits for the whole previous phase
+  int xpub;                        // tensor parallel: peers read this phase's output (publish at sys scope)
+  int xwait;                       // tensor parallel: also wait for every peer's previous phase
   const CUtensorMap* mA0;          // global-memory tensor maps (64-byte aligned)
   const CUtensorMap* mA1;
   const CUtensorMap* mA2;
@@ -41,6 +43,7 @@ struct MegaPhase {
   AttnParams a;
   EmbedParams em;
   ArgmaxParams am;
+  TpParams tp;
 };
 
 struct MegaParams {
@@ -50,6 +53,8 @@ struct MegaParams {
   unsigned* done;                  // [n_ph] cumulative CTA completion counters
   unsigned long long* dbg;         // optional [G][n_ph][8] %globaltimer stamps
   unsigned* tile_done;             // cumulative per-tile completion counters (all GEMM phases)
+  int tp_n;                        // tensor-parallel group size (1: none)
+  const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
 };
 
 constexpr int kMegaThreads = 224;   // 7 warps: W producer, MMA, 4 epilogue, X loader
@@ -90,10 +95,12 @@ PS_DEV void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"
 // Poll with relaxed loads and a short back-off (a tight acquire spin from 148
 // SMs hammers one L2 line and invalidates L1 on every poll), then acquire once.
 PS_DEV void spin_until(const unsigned* p, unsigned target) {
-  unsigned ns = 32;
+  unsigned ns = 32, polls = 0;
+  unsigned long long t0 = 0;
   while ((int)(ld_relaxed_u32(p) - target) < 0) {
     __nanosleep(ns);
     ns = ns < 256 ? ns * 2 : 256;
+    spin_check(polls, t0);
   }
   fence_acquire_gpu();
 }
@@ -312,8 +319,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       named_bar(1, 128);
       const bool need_prev = ph > 0 && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
                                          sph->g.mode != EPI_STORE && sph->dep_w > 0);
-      if (need_prev) {
-        if (et == 0) spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
+      if (need_prev && et == 0) {
+        spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
+        if (sph->xwait)           // tensor parallel: every peer's partial is published
+          for (int q = 0; q < P.tp_n; ++q) spin_until_sys(P.peer_done[q] + (ph - 1), prev_head ? tgt_head : tgt_body);
       }
       named_bar(1, 128);
       if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 0] = globaltimer();
@@ -328,6 +337,9 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       } else if (kind == PH_ACOMB) {
         if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
         else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
+      } else if (kind == PH_TPRED) {
+        const int nt = Q.tp.d >> 7;
+        for (int u = c * 4 + (et >> 5); u < R * nt; u += G * 4) tp_reduce_unit(Q.tp, u / nt, u % nt, lane);
       } else if (kind == PH_ARGMAX) {
         if (c == 0) argmax_run<128>(Q.am, et, (int*)scratch, 1);
       } else {
@@ -381,7 +393,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       named_bar(1, 128);
       if (et == 0) {
         fence_proxy_async_global();
-        red_release_add(P.done + ph, 1u);
+        if (Q.xpub) red_release_add_sys(P.done + ph, 1u);
+        else red_release_add(P.done + ph, 1u);
         if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 1] = globaltimer();
       }
     }

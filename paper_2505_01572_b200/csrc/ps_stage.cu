@@ -225,6 +225,17 @@ struct ps_stage {
   unsigned long long* epi_dbg = nullptr;
   unsigned long long* attn_dbg = nullptr;
   unsigned gen = 0, gen_head = 0;
+  int n_ctas = 0;                    // megakernel grid (persistent CTAs, <= #SMs)
+  // tensor parallelism (a14): this rank's exchange buffer = [phase counters |
+  // partial [2][kMaxRows][d] fp32 | argmax keys [2][kMaxRows] u64]; peers[q] is
+  // rank q's buffer as mapped in this process (peer memory for q != tp_rank)
+  int tp_rank = 0, tp_size = 1;
+  int vocab_full = 0, vocab_off = 0;
+  uint8_t* xch = nullptr;
+  size_t off_part = 0, off_keys = 0, xch_bytes = 0;
+  uint8_t* peers[8] = {};
+  bool peer_ipc[8] = {};
+  bool tp_connected = false;
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
   StepOut* h_out_dev = nullptr;      // its device alias
@@ -254,11 +265,14 @@ struct ps_stage {
 static int bucket_rp(int b) { return b == 0 ? 16 : 32; }
 static int bucket_of(int R) { return R <= 16 ? 0 : 1; }
 
-extern "C" int64_t ps_kv_pool_bytes(const ps_model_shape* s, int32_t max_seq, int32_t page_size) {
-  if (!s || page_size <= 0) return -1;
+extern "C" int64_t ps_kv_pool_bytes_tp(const ps_model_shape* s, int32_t max_seq, int32_t page_size, int32_t tp) {
+  if (!s || page_size <= 0 || tp < 1 || s->n_kv_heads % tp) return -1;
   long long pages = (max_seq + page_size - 1) / page_size;
-  long long page_elems = (long long)s->n_layers * 2 * s->n_kv_heads * page_size * s->head_dim;
+  long long page_elems = (long long)s->n_layers * 2 * (s->n_kv_heads / tp) * page_size * s->head_dim;
   return pages * page_elems * 2;
+}
+extern "C" int64_t ps_kv_pool_bytes(const ps_model_shape* s, int32_t max_seq, int32_t page_size) {
+  return ps_kv_pool_bytes_tp(s, max_seq, page_size, 1);
 }
 
 static void rope_table(const ps_model_shape& s, int max_seq, std::vector<float2>& out) {
@@ -287,6 +301,8 @@ static void rope_table(const ps_model_shape& s, int max_seq, std::vector<float2>
 }
 
 // ---------------------------------------------------------------- forward
+// phases per forward: embed + L x {QKV, attn, combine, O, [TPRED], gate/up, down, [TPRED]} + lm_head + argmax
+static int kMaxPhases(int L) { return 8 * L + 8; }
 enum { K_EMBED = 0, K_QKV, K_ATTN, K_O, K_GU, K_DOWN, K_LMHEAD, K_ARGMAX };
 
 // Host-side TMA maps of one GEMM step: A0..A2 (weights) and X (activations).
@@ -348,6 +364,10 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       p.n_tiles = S->gs_o.n_tiles; p.kb_total = S->gs_o.kb_total; p.maxseg = S->gs_o.maxseg;
       p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld; p.gain = W[PS_N_MLP];
       p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
+      if (S->tp_size > 1) {   // row-parallel: partial -> exchange slot 0, reduced by the TPRED phase
+        p.mode = EPI_STORE;
+        p.out = (float*)(S->xch + S->off_part); p.ld_out = d;
+      }
       hm = HostMaps{&M.o, &M.o, &M.o, &S->map_att[b]};
       return;
     }
@@ -370,6 +390,10 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld;
       p.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
       p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
+      if (S->tp_size > 1) {   // row-parallel: partial -> exchange slot 1
+        p.mode = EPI_STORE;
+        p.out = (float*)(S->xch + S->off_part) + (size_t)kMaxRows * d; p.ld_out = d;
+      }
       hm = HostMaps{&M.d, &M.d, &M.d, &S->map_h[b]};
       return;
     }
@@ -379,12 +403,23 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
       p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
+      if (S->tp_size > 1) {   // vocab-parallel: global ids, per-rank keys in the exchange buffer
+        p.vocab_off = S->vocab_off;
+        p.amax = (unsigned long long*)(S->xch + S->off_keys);
+        p.amax_par = 1;
+      }
       hm = HostMaps{&S->map_lm, &S->map_lm, &S->map_lm, &S->map_xg[b]};
       return;
     }
     case K_ARGMAX: {  // argmax + compare + first-mismatch scan (a11)
       P.kind = PH_ARGMAX;
-      P.am = ArgmaxParams{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn};
+      P.am = ArgmaxParams{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn, 0, {}};
+      if (S->tp_size > 1) {
+        P.am.amax = (unsigned long long*)(S->xch + S->off_keys);
+        P.am.tp_n = S->tp_size;
+        for (int q = 0; q < S->tp_size; ++q)
+          P.am.tp_keys[q] = (const unsigned long long*)(S->peers[q] + S->off_keys);
+      }
       return;
     }
   }
@@ -441,6 +476,24 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     }
     ph.push_back(P);
   };
+  const bool tp = S->tp_size > 1;
+  auto add_tpred = [&](int l, bool after_down) {   // all-reduce + residual + next norm operand (a14)
+    ph.back().xpub = 1;
+    const ps_model_shape& sh = S->sh;
+    MegaPhase P;
+    memset(&P, 0, sizeof P);
+    P.kind = PH_TPRED;
+    P.xwait = 1;
+    TpParams& t = P.tp;
+    t.n = S->tp_size;
+    for (int q = 0; q < S->tp_size; ++q)
+      t.part[q] = (const float*)(S->peers[q] + S->off_part) + (after_down ? (size_t)kMaxRows * sh.d_model : 0);
+    t.x = S->x; t.ld_x = sh.d_model; t.xg = S->xg; t.ld_xg = S->xg_ld;
+    t.gain = !after_down ? S->lw[(size_t)l * 9 + PS_N_MLP]
+                         : (l + 1 < sh.n_layers ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm);
+    t.ss_out = S->ss; t.ss_out_ld = S->ss_ld; t.d = sh.d_model;
+    ph.push_back(P);
+  };
   add(K_EMBED, 0);
   for (int l = 0; l < L; ++l)
     for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
@@ -449,13 +502,17 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
         ph.push_back(ph.back());
         ph.back().kind = PH_ACOMB;
       }
+      if (tp && (kind == K_O || kind == K_DOWN)) add_tpred(l, kind == K_DOWN);
     }
   if (with_head) {
     add(K_LMHEAD, 0);
     ph.back().head = 1;
+    ph.back().xpub = tp ? 1 : 0;
     add(K_ARGMAX, 0);
     ph.back().head = 1;
+    ph.back().xwait = tp ? 1 : 0;
   }
+  if ((int)ph.size() > kMaxPhases(L)) return fail(PS_E_INVALID, "phase table overflow");
   // per-tile counters (fixed per layer position, identical in every table) and
   // the X dependency granularity: columns per producing tile of the previous
   // GEMM phase (x∘g from O / down: 128; h from gate/up: 64); 0 after a
@@ -483,7 +540,7 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
   CU_TRY(cudaMalloc(&S->mega_maps[key], std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
   CU_TRY(cudaMemcpy(S->mega_maps[key], maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   if (g_test_flags & 8) {   // test: per-phase epilogue stamps [phase][cta][4]
-    if (!S->epi_dbg) CU_TRY(cudaMalloc(&S->epi_dbg, (size_t)(6 * S->sh.n_layers + 8) * g_num_sms * 4 * 8));
+    if (!S->epi_dbg) CU_TRY(cudaMalloc(&S->epi_dbg, (size_t)kMaxPhases(S->sh.n_layers) * g_num_sms * 4 * 8));
     for (size_t i = 0; i < ph.size(); ++i) ph[i].g.dbg = S->epi_dbg + i * g_num_sms * 4;
   }
   const CUtensorMap* dm = S->mega_maps[key];
@@ -508,18 +565,24 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
     if (st != PS_OK) return st;
   }
   if ((g_test_flags & 8) && !S->mega_dbg)
-    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * (6 * S->sh.n_layers + 8) * 8 * 8));
+    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * kMaxPhases(S->sh.n_layers) * 8 * 8));
   MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr,
-                S->tile_done};
+                S->tile_done, S->tp_size, {}};
+  for (int q = 0; q < S->tp_size; ++q) mp.peer_done[q] = (const unsigned*)S->peers[q];
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g_num_sms);
+  cfg.gridDim = dim3(S->n_ctas);
   cfg.blockDim = dim3(kMegaThreads);
   cfg.stream = S->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  // A cooperative launch guarantees co-residency of the whole grid, but the
+  // driver does not start a second cooperative kernel while one is running:
+  // ranks of a tensor-parallel group sharing one GPU (max_ctas partitions)
+  // would wait on each other forever.  A partial grid (one 200+ KB CTA per
+  // SM, at most the free SMs) is launched as a plain kernel instead.
+  cfg.numAttrs = (S->n_ctas == g_num_sms || (g_test_flags & 512)) ? 1 : 0;
   cudaError_t e;
   if (g_test_flags & 32) {   // test: shallow ring
     if (b == 0) {
@@ -677,7 +740,9 @@ ps_status ps_stage_destroy(ps_stage* S) {
     if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
     if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
   }
-  if (S->mega_done) cudaFree(S->mega_done);
+  for (int q = 0; q < 8; ++q)
+    if (S->peer_ipc[q]) cudaIpcCloseMemHandle(S->peers[q]);
+  if (S->xch) cudaFree(S->xch);
   if (S->tile_done) cudaFree(S->tile_done);
   if (S->mega_dbg) cudaFree(S->mega_dbg);
   if (S->attn_dbg) cudaFree(S->attn_dbg);
@@ -697,19 +762,120 @@ ps_status ps_stage_destroy(ps_stage* S) {
   return PS_OK;
 }
 
+// ---------------------------------------------------------------- tensor-parallel wiring
+static void drop_tables(ps_stage* S) {   // phase tables embed peer pointers: rebuild after (re)connect
+  for (int k = 0; k < 4; ++k) {
+    if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
+    if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
+    S->mega_ph[k] = nullptr;
+    S->mega_maps[k] = nullptr;
+  }
+}
+
+// Build every phase table now: building one lazily inside a forward allocates
+// and copies synchronously, which would wait for a peer rank's running
+// megakernel that is itself waiting for this rank's forward.
+static ps_status build_all_tables(ps_stage* S) {
+  for (int b = 0; b < 2; ++b)
+    for (int h = 0; h < 2; ++h) {
+      ps_status st = build_mega(S, b, h != 0);
+      if (st != PS_OK) return st;
+    }
+  if ((g_test_flags & 8) && !S->mega_dbg)
+    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * kMaxPhases(S->sh.n_layers) * 8 * 8));
+  CU_TRY(cudaDeviceSynchronize());
+  return PS_OK;
+}
+
+ps_status ps_tp_handle(ps_stage* S, void* handle_out) {
+  if (!S || !handle_out) return fail(PS_E_INVALID, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == PS_TP_HANDLE_BYTES, "handle size");
+  CU_TRY(cudaSetDevice(S->device));
+  cudaIpcMemHandle_t h;
+  CU_TRY(cudaIpcGetMemHandle(&h, S->xch));
+  memcpy(handle_out, &h, sizeof h);
+  return PS_OK;
+}
+
+ps_status ps_tp_connect(ps_stage* S, const void* handles) {
+  if (!S || !handles) return fail(PS_E_INVALID, "NULL argument");
+  if (S->tp_size < 2) return fail(PS_E_INVALID, "stage is not tensor parallel");
+  CU_TRY(cudaSetDevice(S->device));
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  drop_tables(S);
+  for (int q = 0; q < S->tp_size; ++q) {
+    if (q == S->tp_rank) continue;
+    if (S->peer_ipc[q]) { cudaIpcCloseMemHandle(S->peers[q]); S->peer_ipc[q] = false; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const uint8_t*)handles + (size_t)q * PS_TP_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    CU_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    S->peers[q] = (uint8_t*)p;
+    S->peer_ipc[q] = true;
+  }
+  ps_status st = build_all_tables(S);
+  if (st != PS_OK) return st;
+  S->tp_connected = true;
+  return PS_OK;
+}
+
+ps_status ps_tp_connect_local(ps_stage* const* stages, int32_t n) {
+  if (!stages || n < 2 || n > 8) return fail(PS_E_INVALID, "need 2..8 stages");
+  for (int r = 0; r < n; ++r) {
+    const ps_stage* A = stages[r];
+    if (!A) return fail(PS_E_INVALID, "NULL stage");
+    if (A->tp_size != n || A->tp_rank != r) return fail(PS_E_INVALID, "stage %d: tp_rank/tp_size mismatch", r);
+    if (A->n_ctas != stages[0]->n_ctas || A->xch_bytes != stages[0]->xch_bytes ||
+        memcmp(&A->sh, &stages[0]->sh, sizeof A->sh) != 0)
+      return fail(PS_E_INVALID, "stage %d: shard shape / grid differs from rank 0", r);
+  }
+  for (int r = 0; r < n; ++r) {
+    ps_stage* A = stages[r];
+    CU_TRY(cudaSetDevice(A->device));
+    CU_TRY(cudaStreamSynchronize(A->stream));
+    drop_tables(A);
+    for (int q = 0; q < n; ++q) {
+      const ps_stage* B = stages[q];
+      if (B->device != A->device) {
+        int ok = 0;
+        CU_TRY(cudaDeviceCanAccessPeer(&ok, A->device, B->device));
+        if (!ok) return fail(PS_E_CUDA, "no peer access %d -> %d", A->device, B->device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(B->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(PS_E_CUDA, "enable peer access: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+      A->peers[q] = B->xch;
+    }
+    ps_status st = build_all_tables(A);
+    if (st != PS_OK) return st;
+    A->tp_connected = true;
+  }
+  return PS_OK;
+}
+
 ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, const ps_placement* pl,
                           const ps_stage_opts* o, ps_stage** out) {
   ps_status st;
   if (!out || !w || !pl || !o) return fail(PS_E_INVALID, "NULL argument");
   if ((st = validate_shape(shape)) != PS_OK) return st;
-  if (pl->tp_size > 1) return fail(PS_E_INVALID, "tensor parallelism is not built in this version");
+  const int tp = pl->tp_size < 1 ? 1 : pl->tp_size;
+  if (tp > 8 || pl->tp_rank < 0 || pl->tp_rank >= tp) return fail(PS_E_INVALID, "tp_rank/tp_size out of range (tp <= 8)");
+  if (tp > 1) {
+    if (shape->n_heads % tp || shape->n_kv_heads % tp || shape->vocab % tp || shape->d_ffn % (64 * tp) ||
+        shape->d_model % 128)
+      return fail(PS_E_INVALID, "tensor parallel needs heads, kv_heads, vocab divisible by tp, d_ffn by 64*tp, "
+                                "d_model by 128");
+    if (!o || !o->use_megakernel) return fail(PS_E_INVALID, "tensor parallel needs use_megakernel = 1");
+  }
+  if (o && o->max_ctas < 0) return fail(PS_E_INVALID, "max_ctas must be >= 0");
   if (o->max_seq < 2) return fail(PS_E_INVALID, "max_seq must be >= 2");
   if (o->max_window < 0 || o->max_window > kMaxRows - 1) return fail(PS_E_INVALID, "max_window must be 0..31");
   if (o->page_size != 64 && o->page_size != 128 && o->page_size != 256)
     return fail(PS_E_INVALID, "page_size must be 64, 128 or 256");
   if (!w->embed || !w->lm_head || !w->final_norm || (shape->n_layers > 0 && !w->layers))
     return fail(PS_E_INVALID, "NULL weight pointer");
-  const int64_t need = ps_kv_pool_bytes(shape, o->max_seq, o->page_size);
+  const int64_t need = ps_kv_pool_bytes_tp(shape, o->max_seq, o->page_size, tp);
   if ((need > 0 && !o->kv_pool) || o->kv_pool_bytes < need)
     return fail(PS_E_INVALID, "kv_pool too small (%lld < %lld bytes)", (long long)o->kv_pool_bytes, (long long)need);
   if ((st = init_device_globals(pl->device)) != PS_OK) return st;
@@ -734,8 +900,17 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
     if (s_ != PS_OK) return bail(s_);                                                           \
   } while (0)
 
-  const ps_model_shape& sh = *shape;
+  // this rank's shard of the model: heads, KV heads, FFN columns, vocabulary
+  ps_model_shape shl = *shape;
+  shl.n_heads /= tp; shl.n_kv_heads /= tp; shl.d_ffn /= tp; shl.vocab /= tp;
+  const ps_model_shape& sh = shl;
   S->sh = sh;
+  S->tp_size = tp;
+  S->tp_rank = pl->tp_rank;
+  S->vocab_full = shape->vocab;
+  S->vocab_off = pl->tp_rank * sh.vocab;
+  S->tp_connected = tp == 1;
+  S->n_ctas = o->max_ctas > 0 ? std::min(o->max_ctas, g_num_sms) : g_num_sms;
   S->device = pl->device;
   S->max_seq = o->max_seq;
   S->max_window = o->max_window;
@@ -801,7 +976,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
     P_TRY(make_map(&S->map_h[b], S->h, kMaxRows, f, bucket_rp(b)));
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
-  const int n = g_num_sms;
+  const int n = S->n_ctas;
   S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n);
   S->gs_o = gemm_shape((d + 127) / 128, hq, n);
   S->gs_gu = gemm_shape((f + 63) / 64, d, n);
@@ -851,9 +1026,15 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   memset(S->h_page_table, 0, (size_t)lpages * 4);
   S_TRY(cudaMalloc(&S->attn_dbg, (size_t)1024 * 8 * 8));
   S_TRY(cudaMemset(S->attn_dbg, 0, (size_t)1024 * 8 * 8));
-  // --- megakernel phase-completion counters (cumulative; see ps_mega.cuh)
-  S_TRY(cudaMalloc(&S->mega_done, (size_t)(6 * sh.n_layers + 8) * 4));
-  S_TRY(cudaMemset(S->mega_done, 0, (size_t)(6 * sh.n_layers + 8) * 4));
+  // --- exchange buffer: megakernel phase-completion counters (cumulative; see
+  // ps_mega.cuh), tensor-parallel partials and argmax keys (read by peers)
+  S->off_part = ((size_t)kMaxPhases(sh.n_layers) * 4 + 255) / 256 * 256;
+  S->off_keys = S->off_part + (size_t)2 * kMaxRows * d * 4;
+  S->xch_bytes = S->off_keys + (size_t)2 * kMaxRows * 8;
+  S_TRY(cudaMalloc(&S->xch, S->xch_bytes));
+  S_TRY(cudaMemset(S->xch, 0, S->xch_bytes));
+  S->mega_done = (unsigned*)S->xch;
+  S->peers[S->tp_rank] = S->xch;
   {  // per-tile counters: QKV, O, gate/up, down per layer + lm_head
     S->n_tile_ctr = sh.n_layers * (S->gs_qkv.n_tiles + S->gs_o.n_tiles + S->gs_gu.n_tiles + S->gs_d.n_tiles) +
                     S->gs_lm.n_tiles;
@@ -876,6 +1057,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
 static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long pos0, int w, bool with_head,
                               bool want_logits, int row0 = 0) {
   ps_status st;
+  if (!S->tp_connected) return fail(PS_E_INVALID, "tensor-parallel stage not connected (ps_tp_connect)");
   if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
   CU_TRY(cudaEventSynchronize(S->in_ev[S->in_slot]));   // slot's previous copy done
   StepIn* in = S->h_in + S->in_slot;
@@ -903,7 +1085,7 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
   if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "prefill length %d not in [1, max_seq]", n);
   for (int i = 0; i < n; ++i)
-    if (tokens[i] < 0 || tokens[i] >= S->sh.vocab) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
+    if (tokens[i] < 0 || tokens[i] >= S->vocab_full) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
   CU_TRY(cudaSetDevice(S->device));
   // keep the KV of the longest common prefix
   long long m = 0;
@@ -947,7 +1129,7 @@ ps_status ps_resync(ps_stage* S, const int32_t* tokens, int32_t n) {
   if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
   if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "resync length %d not in [1, max_seq]", n);
   for (int i = 0; i < n; ++i)
-    if (tokens[i] < 0 || tokens[i] >= S->sh.vocab) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
+    if (tokens[i] < 0 || tokens[i] >= S->vocab_full) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
   long long m = 0;
   while (m < (long long)S->tokens.size() && m < n && S->tokens[m] == tokens[m]) ++m;
   S->kv_len = std::min<long long>(S->kv_len, std::min<long long>(m, n - 1));
@@ -965,7 +1147,7 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
   if (n + w > S->max_seq) return fail(PS_E_CAPACITY, "n + w = %lld exceeds max_seq", n + w);
   if (S->kv_len > n - 1) return fail(PS_E_CONTRACT, "KV covers %lld positions > n-1 = %lld", S->kv_len, n - 1);
   for (int j = 0; j < w; ++j)
-    if (window[j] < 0 || window[j] >= S->sh.vocab) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
+    if (window[j] < 0 || window[j] >= S->vocab_full) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
   ps_status st = catch_up(S, 1 + w);
   if (st != PS_OK) return st;
   const int row0 = (int)(n - 1 - S->kv_len);
@@ -995,7 +1177,7 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
   }
   const StepOut* r = S->h_out;
   const int a = r->a, nxt = r->next;
-  if (a < 0 || a > w || nxt < 0 || nxt >= S->sh.vocab) return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d", a, nxt);
+  if (a < 0 || a > w || nxt < 0 || nxt >= S->vocab_full) return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d", a, nxt);
   for (int j = 0; j < a; ++j) S->tokens.push_back(window[j]);
   S->tokens.push_back(nxt);
   S->kv_len = n + a;
@@ -1105,7 +1287,7 @@ ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_
     S->h_syn.len_S = len_S;
     S->h_syn.level = level;
     S->h_syn.top = top;
-    S->h_syn.vocab = S->sh.vocab;
+    S->h_syn.vocab = S->vocab_full;
     S->h_syn.seed = seed;
     for (int j = level; j < top; ++j) {
       const double a = alphas[j - level];
@@ -1263,6 +1445,7 @@ extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t
     case 9: src = S->mega_dbg; break;
     case 11: src = S->epi_dbg; break;
     case 10: src = S->attn_dbg; break;
+    case 12: src = S->xch + S->off_part; break;
     default: return fail(PS_E_INVALID, "unknown buffer %d", which);
   }
   CU_TRY(cudaStreamSynchronize(S->stream));

@@ -22,9 +22,33 @@ def model_shape(s) -> abi.ModelShape:
                           s.rope_orig_max, int(bool(s.tied)))
 
 
-def kv_pool_bytes(shape, max_seq: int, page_size: int) -> int:
+def kv_pool_bytes(shape, max_seq: int, page_size: int, tp_size: int = 1) -> int:
     sh = model_shape(shape)
-    return int(abi.lib().ps_kv_pool_bytes(C.byref(sh), max_seq, page_size))
+    return int(abi.lib().ps_kv_pool_bytes_tp(C.byref(sh), max_seq, page_size, tp_size))
+
+
+def shard_weights(shape, weights: dict, rank: int, tp_size: int) -> dict:
+    """Rank `rank`'s Megatron shard of a full weight dict (include/pipespec.h,
+    ps_placement): column-parallel Q/K/V (by heads) and gate/up (by FFN rows),
+    row-parallel O and down (matching input columns), vocab-parallel lm_head;
+    embed and norm gains replicated.  Pure slicing (copies where a slice is not
+    contiguous); no arithmetic."""
+    T, r = tp_size, rank
+    hd = shape.head_dim
+    qh, kh, fr, vr = shape.n_heads // T, shape.n_kv_heads // T, shape.d_ffn // T, shape.vocab // T
+    out = {"embed": weights["embed"], "final_norm": weights["final_norm"],
+           "lm_head": weights["lm_head"][r * vr:(r + 1) * vr].contiguous(), "layers": []}
+    for lw in weights["layers"]:
+        out["layers"].append({
+            "wq": lw["wq"][r * qh * hd:(r + 1) * qh * hd].contiguous(),
+            "wk": lw["wk"][r * kh * hd:(r + 1) * kh * hd].contiguous(),
+            "wv": lw["wv"][r * kh * hd:(r + 1) * kh * hd].contiguous(),
+            "wo": lw["wo"][:, r * qh * hd:(r + 1) * qh * hd].contiguous(),
+            "wg": lw["wg"][r * fr:(r + 1) * fr].contiguous(),
+            "wu": lw["wu"][r * fr:(r + 1) * fr].contiguous(),
+            "wd": lw["wd"][:, r * fr:(r + 1) * fr].contiguous(),
+            "n_attn": lw["n_attn"], "n_mlp": lw["n_mlp"]})
+    return out
 
 
 def _i32(a) -> np.ndarray:
@@ -36,7 +60,10 @@ class Stage:
 
     def __init__(self, shape, weights: dict, max_seq: int = 1024, max_window: int = 31,
                  page_size: int = 64, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 use_graphs: bool = True, megakernel: bool = True):
+                 use_graphs: bool = True, megakernel: bool = True, tp_rank: int = 0, tp_size: int = 1,
+                 max_ctas: int = 0):
+        """`weights`: the full model, or with tp_size > 1 this rank's shard
+        (shard_weights); `shape` is always the full model's."""
         self.shape = shape
         self.weights = weights            # keep the borrowed tensors alive
         self._sh = model_shape(shape)
@@ -54,12 +81,13 @@ class Stage:
         self._w = abi.Weights(weights["embed"].data_ptr(), weights["lm_head"].data_ptr(),
                               weights["final_norm"].data_ptr(),
                               C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
-        nbytes = kv_pool_bytes(shape, max_seq, page_size)
+        nbytes = kv_pool_bytes(shape, max_seq, page_size, tp_size)
         self.kv_pool = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
-        self._pl = abi.Placement(device, None, 0, 1)
+        self._pl = abi.Placement(device, None, tp_rank, tp_size)
         self._opts = abi.StageOpts(max_seq, max_window, page_size, self.kv_pool.data_ptr(), nbytes,
-                                   self.stream.cuda_stream, int(use_graphs), int(megakernel))
+                                   self.stream.cuda_stream, int(use_graphs), int(megakernel), max_ctas)
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         h = C.c_void_p()
         abi.check(abi.lib().ps_stage_create(C.byref(self._sh), C.byref(self._w), C.byref(self._pl),
                                             C.byref(self._opts), C.byref(h)))
@@ -115,12 +143,24 @@ class Stage:
         logits = None
         lptr = None
         if want_logits:
-            logits = np.zeros((w + 1, self.shape.vocab), dtype=np.float32)
+            logits = np.zeros((w + 1, self.shape.vocab // self.tp_size), dtype=np.float32)
             lptr = logits.ctypes.data
         abi.check(abi.lib().ps_verify(self._h, ptr if w else None, w, C.byref(a), C.byref(nxt), lptr))
         if want_logits:
             return a.value, nxt.value, logits
         return a.value, nxt.value
+
+    def tp_handle(self) -> bytes:
+        """This rank's exchange-buffer handle (ps_tp_handle)."""
+        buf = (C.c_uint8 * abi.PS_TP_HANDLE_BYTES)()
+        abi.check(abi.lib().ps_tp_handle(self._h, buf))
+        return bytes(buf)
+
+    def tp_connect(self, handles):
+        """Map the peers' exchange buffers: handles = every rank's tp_handle() in rank order."""
+        assert len(handles) == self.tp_size and all(len(h) == abi.PS_TP_HANDLE_BYTES for h in handles)
+        buf = (C.c_uint8 * (abi.PS_TP_HANDLE_BYTES * self.tp_size)).from_buffer_copy(b"".join(handles))
+        abi.check(abi.lib().ps_tp_connect(self._h, buf))
 
     def kv_rollback(self, keep_len: int):
         abi.check(abi.lib().ps_kv_rollback(self._h, keep_len))
@@ -150,6 +190,21 @@ class Stage:
 
     def clear_synthetic(self):
         abi.check(abi.lib().ps_set_synthetic(self._h, None, 0, 0, 0, 0, None, 0))
+
+
+def tp_connect_local(stages):
+    """Link the ranks of one tensor-parallel group created in this process (rank order)."""
+    hs = (C.c_void_p * len(stages))(*[s.handle for s in stages])
+    abi.check(abi.lib().ps_tp_connect_local(hs, len(stages)))
+
+
+def tp_connect_group(stage, group=None):
+    """One process per rank: all-gather the exchange handles over a
+    torch.distributed group (any backend) and connect."""
+    import torch.distributed as dist
+    handles = [None] * stage.tp_size
+    dist.all_gather_object(handles, stage.tp_handle(), group=group)
+    stage.tp_connect(handles)
 
 
 def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PIPESPEC, gammas=None,

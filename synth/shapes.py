@@ -59,6 +59,8 @@ PRESETS = {
     # BASELINE.json configs[0]
     "toy-drafter": ModelShape("toy-drafter", 256, 64, 2, 1, 1, 64, 256, 1e-5, 1e4),
     "toy-verifier": ModelShape("toy-verifier", 256, 128, 4, 2, 1, 64, 512, 1e-5, 1e4),
+    # tensor-parallel toy (heads, KV heads, vocab divisible by 1, 2 and 4; d_ffn by 64*4)
+    "toy-tp": ModelShape("toy-tp", 1024, 512, 2, 8, 4, 64, 1024, 1e-5, 1e4),
     # paper-style LLaMA-2 hierarchy (Tab.2)
     "llama-68m": ModelShape("llama-68m", 32000, 768, 2, 12, 12, 64, 3072, 1e-6, 1e4),
     "llama2-7b": ModelShape("llama2-7b", 32000, 4096, 32, 32, 32, 128, 11008, 1e-5, 1e4),
