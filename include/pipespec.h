@@ -251,6 +251,25 @@ ps_status ps_pipeline_run(ps_stage* const* stages, int32_t k, const int32_t* pro
                           int32_t n_prompt, const ps_run_opts* opts, int32_t* out,
                           int32_t* out_len, ps_run_stats* stats);
 
+/* Alg.1 with ONE PROCESS PER STAGE (the paper's layout: each model on its own
+ * GPU(s)).  The stages share a "board" in POSIX shared
+ * memory (same node) holding the committed buffers O_i, epochs and rollback
+ * targets -- the only cross-stage traffic is these few tokens.
+ * ps_board_create: one process creates board `name` (e.g. "/pipespec-run1")
+ * for k stages and `capacity` >= n_prompt + max_new_tokens + 320 tokens
+ * BEFORE any stage attaches (re-creating resets it); ps_board_unlink removes
+ * it.  ps_pipeline_run_rank: process `rank` (stage M_rank, 0 = first drafter,
+ * k-1 = target) prefills `stage` with the prompt, attaches, waits for all k
+ * stages, runs its Alg.1 loop (PS_MODE_PIPESPEC only) and returns, on every
+ * rank, the generated tokens of O_{k-1} in out[0:*out_len] and the run's
+ * stats.  A stage that fails or a peer that never attaches (120 s) ends the
+ * run on every rank with that status. */
+ps_status ps_board_create(const char* name, int32_t k, int32_t capacity);
+ps_status ps_board_unlink(const char* name);
+ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const char* board,
+                               const int32_t* prompt, int32_t n_prompt, const ps_run_opts* opts,
+                               int32_t* out, int32_t* out_len, ps_run_stats* stats);
+
 /* Device-side timing hook for benchmarks: number of kernels this library has
  * launched (graph launches count their kernels) since process start. */
 int64_t ps_kernel_launch_count(void);

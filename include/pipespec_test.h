@@ -35,7 +35,10 @@ ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, i
  *         created / tables built afterwards
  *   bit5  megakernel: 4-stage ring variant
  *   bit6  attention: per-item stage stamps (ps_test_read 10)
- *   bit8  megakernel: per-tile dataflow dependencies (experimental, slower) */
+ *   bit8  megakernel: per-tile dataflow dependencies (experimental, slower)
+ *   bit9  megakernel: cooperative launch even for a partial grid (max_ctas)
+ *   bit10 attention: always combine inline (last-arriving CTA), no ACOMB phase
+ *   bit11 attention: never combine inline (always a separate ACOMB phase) */
 void ps_test_set_flags(int32_t flags);
 
 /* Re-launch one kernel of the stage's most recent forward configuration
@@ -50,8 +53,23 @@ ps_status ps_time_kernel(ps_stage* stage, int32_t kind, int32_t layer, int32_t i
  * 3 attention out (bf16 [32,H*hd]), 4 SwiGLU out (bf16 [32,ffn]),
  * 5 sumsq slots (fp32 [32,ceil(d/128)]), 6 KV pool, 7 attention (m,l) partials,
  * 8 device page table (int32), 9 megakernel phase stamps, 10 attention stamps,
- * 11 stream-K fixup stamps. */
+ * 11 stream-K fixup stamps, 12 tensor-parallel partials (fp32 [2][32][d]). */
 ps_status ps_test_read(ps_stage* stage, int32_t which, void* dst, int64_t bytes);
+
+/* Protocol test double of the async runtime (no GPU): k stages over a
+ * closed-form host "model" -- stage k-1 emits next(c) = (c[-1]*7919 +
+ * |c|*104729 + 13) mod vocab, stage i < k-1 agrees with stage i+1 with
+ * probability alpha (hash of seed, i, |c|) -- stage i sleeping sleep_us*(1+3i) per step.
+ * _pipeline runs the k stages as threads of this process (as
+ * ps_pipeline_run PS_MODE_PIPESPEC), _run_rank as stage `rank` of a board in
+ * shared memory (as ps_pipeline_run_rank). */
+ps_status ps_test_fake_pipeline(int32_t k, const int32_t* prompt, int32_t n_prompt, const ps_run_opts* opts,
+                                int32_t vocab, double alpha, uint64_t seed, int32_t sleep_us,
+                                int32_t* out, int32_t* out_len, ps_run_stats* stats);
+ps_status ps_test_fake_run_rank(int32_t rank, int32_t k, const char* board, const int32_t* prompt,
+                                int32_t n_prompt, const ps_run_opts* opts, int32_t vocab, double alpha,
+                                uint64_t seed, int32_t sleep_us, int32_t* out, int32_t* out_len,
+                                ps_run_stats* stats);
 
 #ifdef __cplusplus
 }

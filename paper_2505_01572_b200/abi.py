@@ -91,6 +91,16 @@ _PROTOS = {
     "ps_pipeline_run": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.POINTER(RunOpts),
                                     C.c_void_p, _I32P, C.POINTER(RunStats)]),
     "ps_resync": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "ps_board_create": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32]),
+    "ps_board_unlink": (C.c_int32, [C.c_char_p]),
+    "ps_pipeline_run_rank": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_void_p, C.c_int32,
+                                         C.POINTER(RunOpts), C.c_void_p, _I32P, C.POINTER(RunStats)]),
+    "ps_test_fake_pipeline": (C.c_int32, [C.c_int32, C.c_void_p, C.c_int32, C.POINTER(RunOpts), C.c_int32,
+                                          C.c_double, C.c_uint64, C.c_int32, C.c_void_p, _I32P,
+                                          C.POINTER(RunStats)]),
+    "ps_test_fake_run_rank": (C.c_int32, [C.c_int32, C.c_int32, C.c_char_p, C.c_void_p, C.c_int32,
+                                          C.POINTER(RunOpts), C.c_int32, C.c_double, C.c_uint64, C.c_int32,
+                                          C.c_void_p, _I32P, C.POINTER(RunStats)]),
     "ps_time_kernel": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "ps_test_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
     "ps_test_gemm_timed": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

@@ -35,6 +35,8 @@ struct MegaPhase {
                                    // 0 = the X operand waits for the whole previous phase
   int xpub;                        // tensor parallel: peers read this phase's output (publish at sys scope)
   int xwait;                       // tensor parallel: also wait for every peer's previous phase
+  int inline_comb;                 // ATTN/ACOMB: 1 the last CTA of each (kv head, row block) combines (no
+                                   // ACOMB phase); 2 the same when R*g <= kInlineCombRows, else ACOMB
   const CUtensorMap* mA0;          // global-memory tensor maps (64-byte aligned)
   const CUtensorMap* mA1;
   const CUtensorMap* mA2;
@@ -56,6 +58,14 @@ struct MegaParams {
   int tp_n;                        // tensor-parallel group size (1: none)
   const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
 };
+
+// Up to this many query rows per KV head the last-arriver combine inside the
+// attention phase is cheaper than a separate combine phase (measured: 1B draft
+// step R=1 -2.5%; 8B verify R=5, 20 rows: +6%).
+constexpr int kInlineCombRows = 8;
+PS_DEV bool inline_combine(const MegaPhase& Q, int R) {
+  return Q.inline_comb == 1 || (Q.inline_comb == 2 && R * (Q.a.H / Q.a.hkv) <= kInlineCombRows);
+}
 
 constexpr int kMegaThreads = 224;   // 7 warps: W producer, MMA, 4 epilogue, X loader
 // ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
@@ -317,8 +327,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       // epilogue needs no full-row statistic (O / down: RESID, no rstd); the
       // mainloop of every GEMM phase is gated per tile by the X loader.
       named_bar(1, 128);
-      const bool need_prev = ph > 0 && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
-                                         sph->g.mode != EPI_STORE && sph->dep_w > 0);
+      // (A combine phase whose work the attention phase already did inline is
+      // a pass-through: each CTA publishes it as soon as its own attention
+      // items, combines included, are done.)
+      const bool skip = sph->kind == PH_ACOMB && inline_combine(*sph, R);
+      const bool need_prev = ph > 0 && !skip && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
+                                                  sph->g.mode != EPI_STORE && sph->dep_w > 0);
       if (need_prev && et == 0) {
         spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
         if (sph->xwait)           // tensor parallel: every peer's partial is published
@@ -331,10 +345,15 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
-        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        if (inline_combine(Q, R)) {
+          if (Q.a.hd == 128) attn_run<128, 4, true>(Q.a, attn_smem, et, c, G, 1, pref_item);
+          else attn_run<64, 4, true>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        } else {
+          if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+          else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        }
         pref_item = -1;
-      } else if (kind == PH_ACOMB) {
+      } else if (kind == PH_ACOMB && !skip) {
         if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
         else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
       } else if (kind == PH_TPRED) {

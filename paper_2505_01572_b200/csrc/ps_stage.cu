@@ -498,9 +498,15 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
   for (int l = 0; l < L; ++l)
     for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
       add(kind, l);
-      if (kind == K_ATTN) {          // chunk partials, then a separate combine phase
-        ph.push_back(ph.back());
-        ph.back().kind = PH_ACOMB;
+      if (kind == K_ATTN) {
+        // chunk partials, then a combine phase -- or, for few query rows per KV
+        // head, the last-arriving CTA of each (kv head, row block) combines
+        // (test flags: 1024 always inline, 2048 never)
+        ph.back().inline_comb = (g_test_flags & 1024) ? 1 : (g_test_flags & 2048) ? 0 : 2;
+        if (ph.back().inline_comb != 1) {
+          ph.push_back(ph.back());
+          ph.back().kind = PH_ACOMB;
+        }
       }
       if (tp && (kind == K_O || kind == K_DOWN)) add_tpred(l, kind == K_DOWN);
     }

@@ -207,6 +207,34 @@ def tp_connect_group(stage, group=None):
     stage.tp_connect(handles)
 
 
+def _run_opts(k, max_new_tokens, mode, gammas, lookaheads, eos_id, max_lead):
+    g = (C.c_int32 * k)(*(gammas or [0] * k))
+    la = (C.c_int32 * k)(*(lookaheads or [0] * k))
+    return abi.RunOpts(mode, max_new_tokens, eos_id, g, la, max_lead), (g, la)
+
+
+def board_create(name: str, k: int, capacity: int):
+    """Shared-memory board for one process per stage (ps_board_create)."""
+    abi.check(abi.lib().ps_board_create(name.encode(), k, capacity))
+
+
+def board_unlink(name: str):
+    abi.check(abi.lib().ps_board_unlink(name.encode()))
+
+
+def pipeline_run_rank(stage, rank: int, k: int, board: str, prompt, max_new_tokens: int, gammas=None,
+                      lookaheads=None, eos_id: int = -1, max_lead: int = 0):
+    """This process's stage M_rank of a k-stage async PipeSpec run (ps_pipeline_run_rank)."""
+    opts, keep = _run_opts(k, max_new_tokens, abi.PS_MODE_PIPESPEC, gammas, lookaheads, eos_id, max_lead)
+    p = _i32(prompt)
+    out = np.zeros(max_new_tokens, dtype=np.int32)
+    n = C.c_int32()
+    stats = abi.RunStats()
+    abi.check(abi.lib().ps_pipeline_run_rank(stage.handle, rank, k, board.encode(), p.ctypes.data, len(p),
+                                             C.byref(opts), out.ctypes.data, C.byref(n), C.byref(stats)))
+    return out[:n.value].tolist(), stats
+
+
 def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PIPESPEC, gammas=None,
                  lookaheads=None, eos_id: int = -1, max_lead: int = 0):
     k = len(stages)

@@ -88,3 +88,58 @@ def test_async_pipespec_three_stage_and_lookahead():
     assert sd == ar
     for x in st:
         x.close()
+
+
+def _stage_process(rank, board, S, n, q):
+    """One stage per process: M_0 (toy drafter, synthetic alpha 0.8 against S)
+    or M_1 (toy verifier), both on cuda:0, through ps_pipeline_run_rank."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import synth as sy
+    from paper_2505_01572_b200 import Stage, pipeline_run_rank
+    name, seed = ("toy-drafter", 31) if rank == 0 else ("toy-verifier", 32)
+    s = sy.preset(name)
+    w = sy.make_weights(s, seed=seed, device="cuda")
+    st = Stage(s, w, max_seq=256, max_window=8)
+    prompt = [int(x) for x in sy.make_prompt(256, 64, seed=33)]
+    if rank == 0:
+        st.set_synthetic(S, len(prompt), level=0, top=1, alphas=[0.8], seed=78)
+    try:
+        out, stats = pipeline_run_rank(st, rank, 2, board, prompt, n, gammas=[0, 4], lookaheads=[0, 2])
+        q.put((rank, "ok", out, int(stats.verify_steps[1]), int(stats.rollbacks[0])))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), [], 0, 0))
+    st.close()
+
+
+def test_stage_per_process_pipespec_lossless(pair):
+    """The paper's layout -- each model in its own process (its own GPU in a
+    deployment; here both on cuda:0, so the verifier waits for 2 drafts
+    (lookahead 2) instead of racing the time-sliced drafter) -- through the
+    shared-memory board:
+    output == M_K autoregressive decoding, verify steps taken."""
+    import os
+    import torch.multiprocessing as mp
+    from paper_2505_01572_b200 import board_create, board_unlink, pipeline_run
+    from paper_2505_01572_b200.abi import PS_MODE_AR
+    sd_, sv, wd, wv, d, v, prompt = pair
+    n = 40
+    ar, _ = pipeline_run([d, v], prompt, n + 8, mode=PS_MODE_AR)
+    board = f"/pipespec-gpu-{os.getpid()}"
+    board_create(board, 2, 64 + n + 400)
+    try:
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_stage_process, args=(r, board, ar, n, q)) for r in range(2)]
+        for p in procs:
+            p.start()
+        res = sorted(q.get(timeout=240) for _ in range(2))
+        for p in procs:
+            p.join(timeout=60)
+    finally:
+        board_unlink(board)
+    for rank, status, out, vsteps, rb in res:
+        assert status == "ok", (rank, status)
+        assert out == ar[:n], rank
+        assert vsteps > 0
