@@ -38,7 +38,7 @@ ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, i
  *   bit8  megakernel: per-tile dataflow dependencies (experimental, slower)
  *   bit9  megakernel: cooperative launch even for a partial grid (max_ctas)
  *   bit10 attention: always combine inline (last-arriving CTA), no ACOMB phase
- *   bit11 attention: never combine inline (always a separate ACOMB phase) */
+ *   bit11 attention: combine inline only when R*g <= 8 (ACOMB a pass-through) */
 void ps_test_set_flags(int32_t flags);
 
 /* Re-launch one kernel of the stage's most recent forward configuration

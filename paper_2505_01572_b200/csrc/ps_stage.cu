@@ -499,10 +499,12 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
       add(kind, l);
       if (kind == K_ATTN) {
-        // chunk partials, then a combine phase -- or, for few query rows per KV
-        // head, the last-arriving CTA of each (kv head, row block) combines
-        // (test flags: 1024 always inline, 2048 never)
-        ph.back().inline_comb = (g_test_flags & 1024) ? 1 : (g_test_flags & 2048) ? 0 : 2;
+        // chunk partials, then a separate combine phase.  (Test flags: 1024 the
+        // last-arriving CTA of each (kv head, row block) combines inline, no
+        // ACOMB phase: 1B R=1 -2.5%, 8B R=5 +6%; 2048 inline only for
+        // R*g <= 8 with ACOMB as a pass-through otherwise: no gain, the
+        // pass-through phase costs what the inline combine saves.)
+        ph.back().inline_comb = (g_test_flags & 1024) ? 1 : (g_test_flags & 2048) ? 2 : 0;
         if (ph.back().inline_comb != 1) {
           ph.push_back(ph.back());
           ph.back().kind = PH_ACOMB;
