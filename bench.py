@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--alpha", type=float, default=0.8)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--multi-gpu-extras", action="store_true",
+                    help="N>1: also time M_1 tensor-parallel over the N GPUs and the stage-per-GPU async pipeline")
     return ap.parse_args()
 
 
@@ -118,6 +120,70 @@ def aggregate(dev_s, wall_s, tokens, world, device="cpu"):
     dist.all_reduce(times, op=dist.ReduceOp.MAX)
     dist.all_reduce(tok, op=dist.ReduceOp.SUM)
     return float(times[0]), float(times[1]), float(tok[0])
+
+
+def multi_gpu_extras(args, rank, world, ts, wt, drafter, target, prompt, S, g):
+    """N > 1 only (beside the replica line): (1) M_1's verify pass tensor-
+    parallel over all N GPUs -- Megatron shards, the all-reduces and the
+    vocab-parallel argmax inside the megakernel over NVLink peer memory
+    (SURVEY §8(e), a14); (2) the paper's stage-per-GPU layout, M_0 on rank 0's
+    GPU and M_1 on rank 1's, async PipeSpec through the shared-memory board.
+    Each part reports an error string instead of failing the bench."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_01572_b200 import (Stage, board_create, board_unlink, pipeline_run_rank, shard_weights,
+                                       tp_connect_group)
+    out = {}
+    obj = [prompt, S, f"/pipespec-bench-{os.getpid()}"]
+    dist.broadcast_object_list(obj, src=0)        # every rank works on rank 0's prompt and stream
+    p0, S0, board = obj
+    try:
+        tps = Stage(ts, shard_weights(ts, wt, rank, world), max_seq=args.prompt + 64, max_window=g,
+                    tp_rank=rank, tp_size=world)
+        tp_connect_group(tps)
+        tps.prefill(p0)
+        win = S0[:g]
+        res = None
+        for it in range(13):
+            if it == 3:
+                torch.cuda.synchronize()
+                dist.barrier()
+                tps.reset_timers()
+            res = tps.verify(win)
+            tps.kv_rollback(len(p0))
+        inf = tps.info()
+        ms = torch.tensor([inf["sum_fwd_ms"] / max(1, inf["n_fwd"])], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        R = g + 1
+        byts = ts.streamed_bytes_per_pass(R) + (len(p0) + R) * ts.kv_bytes_per_token()
+        out["tp_verify_pass"] = {"tp": world, "ms": float(ms[0]), "rows": R, "ctx": len(p0),
+                                 "accepted": res[0], "agg_GB/s": byts / (float(ms[0]) * 1e-3) / 1e9}
+        tps.close()
+    except Exception as e:  # noqa: BLE001
+        out["tp_verify_pass"] = {"error": repr(e)[:300]}
+    try:
+        if rank == 0:
+            board_create(board, 2, len(p0) + args.gen + 512)
+            drafter.set_synthetic(S0, len(p0), level=0, top=1, alphas=[args.alpha], seed=args.seed + 1234)
+        dist.barrier()
+        if rank < 2:
+            stage = drafter if rank == 0 else target
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            got, st = pipeline_run_rank(stage, rank, 2, board, p0, args.gen, gammas=[0, g])
+            dt = time.perf_counter() - w0
+            ok = got == S0[:args.gen]
+        dist.barrier()
+        if rank == 0:
+            board_unlink(board)
+            out["stage_per_gpu_pipespec"] = {"layout": "M_0 on GPU 0, M_1 on GPU 1, one process each",
+                                             "tokens_per_s": len(got) / dt,
+                                             "tokens_per_s_decode": len(got) / (st.wall_ns / 1e9),
+                                             "lossless": ok, "verify_steps": int(st.verify_steps[1]),
+                                             "rollbacks": int(st.rollbacks[0])}
+    except Exception as e:  # noqa: BLE001
+        out["stage_per_gpu_pipespec"] = {"error": repr(e)[:300]}
+    return out
 
 
 def oracle_sample(draft_shape, target_shape, wd, wt, gamma, alpha, seed, n_rounds, ctx=64, layers=2):
@@ -365,6 +431,8 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if world > 1 and args.multi_gpu_extras:
+        line["multi_gpu"] = multi_gpu_extras(args, rank, world, ts, wt, drafter, target, prompt, S, g)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, times, toks = oracle_sample(ds, ts, wd, wt, g, args.alpha, args.seed + 1234, 2)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
