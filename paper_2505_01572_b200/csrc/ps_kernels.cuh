@@ -90,6 +90,8 @@ struct GemmParams {
   float* out; int ld_out;
   // stream-K fixup
   float* ws; unsigned* counters;
+  int ll;                          // 1: flag-in-data partials (below); 0: release counter + reducer spin
+  int ll_tag;                      // distinct per GEMM of a forward (< 1024); flag = gen << 10 ^ ll_tag
   unsigned long long* dbg;         // optional per-CTA %globaltimer trace [grid][4]
   int test_mode;                   // test hooks: bit0 skip TMA, bit1 skip MMA
 };
@@ -203,10 +205,89 @@ PS_DEV void sk_reduce(const float4* wsp, float* v, int e, int seg, int nseg) {
   for (int r = 0; r < 4 * JJ; ++r) v[r] = acc[r];
 }
 
+// Flag-in-data stream-K partials ("LL" protocol): every fp32 partial travels
+// with a 32-bit flag in one 64-bit word (single-copy atomic), flag = (forward
+// generation << 10) ^ GEMM tag, unique per use of a workspace slot.  The
+// reducer polls the data itself: no store -> release -> acquire chain, no
+// counter, no barrier; a partial is usable the moment it lands in L2.
+PS_DEV void st_ll2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+PS_DEV void ld_ll2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+PS_DEV unsigned long long ll_pack(float v, uint32_t flag) {
+  return ((unsigned long long)flag << 32) | (unsigned long long)__float_as_uint(v);
+}
+PS_DEV bool ll_ok(unsigned long long w, uint32_t flag) { return (uint32_t)(w >> 32) == flag; }
+PS_DEV float ll_val(unsigned long long w) { return __uint_as_float((uint32_t)w); }
+
+// Fixed-order sum over the nseg LL partials of one tile, for row pairs
+// [j0, j0 + JJ): ((0 + p_0) + p_1) + ... (the same order as sk_reduce); NIF
+// segments' loads are issued before any is checked, stragglers re-polled.
+template <int RP, int JJ, int NIF>
+PS_DEV void sk_reduce_ll_group(const unsigned long long* wsp, float* v, int j0, int R2, int e, int seg, int nseg,
+                               uint32_t flag) {
+  float acc[2 * JJ];
+#pragma unroll
+  for (int r = 0; r < 2 * JJ; ++r) acc[r] = 0.f;
+  for (int q0 = 0; q0 < nseg; q0 += NIF) {
+    unsigned long long w[NIF][JJ][2];
+#pragma unroll
+    for (int h = 0; h < NIF; ++h) {
+      const int q = q0 + h;
+      if (q < nseg && q != seg) {
+#pragma unroll
+        for (int j = 0; j < JJ; ++j)
+          if (j0 + j < R2) ld_ll2(wsp + ((size_t)q * 128 + e) * RP + 2 * (j0 + j), w[h][j][0], w[h][j][1]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < NIF; ++h) {
+      const int q = q0 + h;
+      if (q >= nseg) continue;
+      if (q == seg) {
+#pragma unroll
+        for (int r = 0; r < 2 * JJ; ++r) acc[r] += v[2 * j0 + r];
+        continue;
+      }
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) {
+        if (j0 + j >= R2) continue;              // row pairs past R: never published, never used
+        unsigned ns = 32, polls = 0;
+        unsigned long long t0 = 0;
+        while (!ll_ok(w[h][j][0], flag) || !ll_ok(w[h][j][1], flag)) {
+          __nanosleep(ns);
+          ns = ns < 128 ? ns * 2 : 128;
+          spin_check(polls, t0);
+          ld_ll2(wsp + ((size_t)q * 128 + e) * RP + 2 * (j0 + j), w[h][j][0], w[h][j][1]);
+        }
+        acc[2 * j] += ll_val(w[h][j][0]);
+        acc[2 * j + 1] += ll_val(w[h][j][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * JJ; ++r) v[2 * j0 + r] = acc[r];
+}
+
+template <int RP>
+PS_DEV void sk_reduce_ll(const unsigned long long* wsp, float* v, int R2, int e, int seg, int nseg, uint32_t flag) {
+  if (R2 <= 1) sk_reduce_ll_group<RP, 1, 8>(wsp, v, 0, R2, e, seg, nseg, flag);
+  else if (R2 <= 2) sk_reduce_ll_group<RP, 2, 4>(wsp, v, 0, R2, e, seg, nseg, flag);
+  else {
+#pragma unroll
+    for (int j0 = 0; j0 < RP / 2; j0 += 4)
+      if (j0 < R2) sk_reduce_ll_group<RP, 4, 2>(wsp, v, j0, R2, e, seg, nseg, flag);
+  }
+}
+
 // One accumulator segment of tile t (units [seg_begin, seg_end) of this CTA c
 // out of G): stream-K fixup (deterministic fixed segment order) then the
 // fused epilogue for the tile if this CTA completes it.  128 epilogue threads.
-template <int RP>
+// kLL: compile the flag-in-data fixup (p.ll selects it at run time); the
+// 2-CTA/SM standalone GEMM keeps the register-lean release/counter fixup.
+template <int RP, bool kLL = false>
 PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long long seg_end, long long U, int G, int c,
                         int kbt, float* v, int e, int lane, int quarter, int R, int pos0, float* scratch,
                         unsigned long long* red, const float* rstd, const long long* kvrow, volatile int* flag) {
@@ -217,7 +298,28 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
     // RP contiguous floats with 16-byte accesses; the reducing CTA issues all
     // of a segment's loads before using them (latency, not bandwidth, bound).
     const long long tile_u0 = (long long)t * kbt;
-    if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
+    // LL only for R <= 4 (at most 2 row pairs per thread: the reducer keeps 8
+    // segments' loads in flight); wider windows keep the release path, whose
+    // float4 partials batch more segments per round trip (measured: 1B R=1
+    // -2.6%, 8B R=5 +3.5% with LL)
+    if (kLL && p.ll && R <= 4 && !(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
+      const int first = sk_owner(U, G, tile_u0);
+      const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
+      const int seg = c - first;
+      const uint32_t flag = ((uint32_t)p.step->gen << 10) ^ (uint32_t)p.ll_tag;
+      unsigned long long* wsp = reinterpret_cast<unsigned long long*>(p.ws) + (size_t)(t * p.maxseg) * RP * 128;
+      const int R2 = (R + 1) >> 1;               // live row pairs
+      if (seg != 0) {                            // publish: data + flag, nothing else
+#pragma unroll
+        for (int j = 0; j < RP / 2; ++j)
+          if (j < R2) st_ll2(wsp + ((size_t)seg * 128 + e) * RP + 2 * j, ll_pack(v[2 * j], flag), ll_pack(v[2 * j + 1], flag));
+        if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+        break;
+      }
+      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = p.dbg[c * 4 + 1] = globaltimer();
+      sk_reduce_ll<RP>(wsp, v, R2, e, seg, nseg, flag);
+      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 2] = globaltimer();
+    } else if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
       const int first = sk_owner(U, G, tile_u0);
       const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
       const int seg = c - first;

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             mbar_arrive(&tempty[acc]);
             ++nacc;
             u = seg_end;
-            const bool fin = epi_segment<RP>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
+            const bool fin = epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
                                              pos0, scratch, red, rstd, kvrow, flag);
             if (fin) {                                  // publish tile t of this phase
               named_bar(1, 128);

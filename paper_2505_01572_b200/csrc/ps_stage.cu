@@ -323,6 +323,8 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
   p.step = S->d_in;
   p.ws = S->ws;
   p.counters = S->counters;
+  p.ll = (g_test_flags & 4096) ? 0 : 1;
+  p.ll_tag = 1 + kind + 8 * l;     // per-kernel path; the megakernel re-tags by phase index
   switch (kind) {
     case K_EMBED: {
       P.kind = PH_EMBED;
@@ -532,6 +534,7 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
       if (P.kind != PH_GEMM) continue;
       P.tctr = base;
       base += P.g.n_tiles;
+      P.g.ll_tag = 1 + (int)i;       // LL stream-K flag tag: the phase index (< 1024)
       const MegaPhase& D = ph[i - 1];
       // Per-tile dependencies are implemented (X loader, ps_mega.cuh) but off by
       // default: the acquire + proxy fences per producer-tile batch serialise the
@@ -997,7 +1000,10 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
     ws_elems = std::max(ws_elems, (size_t)g->n_tiles * g->maxseg * kMaxRows * 128);
     max_tiles = std::max(max_tiles, g->n_tiles);
   }
-  S_TRY(cudaMalloc(&S->ws, ws_elems * 4));
+  // fp32 partials (release path) or (fp32, flag) words (LL path): 8 bytes each;
+  // zeroed so no stale flag of a freed buffer can match
+  S_TRY(cudaMalloc(&S->ws, ws_elems * 8));
+  S_TRY(cudaMemset(S->ws, 0, ws_elems * 8));
   S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * 4));
   S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
   S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * 8));
@@ -1332,7 +1338,8 @@ static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_
   float* ws;
   unsigned* cnt;
   CU_TRY(cudaMalloc(&din, sizeof(StepIn)));
-  CU_TRY(cudaMalloc(&ws, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 4));
+  CU_TRY(cudaMalloc(&ws, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8));
+  CU_TRY(cudaMemset(ws, 0, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8));
   CU_TRY(cudaMalloc(&cnt, (size_t)gs.n_tiles * 4));
   CU_TRY(cudaMemset(cnt, 0, (size_t)gs.n_tiles * 4));
   CU_TRY(cudaMemcpy(din, &hin, sizeof hin, cudaMemcpyHostToDevice));
@@ -1347,6 +1354,8 @@ static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_
   p.ld_out = N;
   p.ws = ws;
   p.counters = cnt;
+  p.ll = (g_test_flags & 4096) ? 0 : 1;
+  p.ll_tag = 1;
   p.test_mode = g_test_flags >> 1;
   unsigned long long* dbg = nullptr;
   const int nl = iters > 0 ? iters : 1;
@@ -1359,6 +1368,7 @@ static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_
   CU_TRY(cudaEventRecord(e0, s));
   for (int i = 0; i < iters && st == PS_OK; ++i) {
     p.dbg = dbg ? dbg + (size_t)i * gs.grid * 4 : nullptr;
+    p.ll_tag = 2 + i % 1000;          // distinct flags for back-to-back launches
     st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
   }
   CU_TRY(cudaEventRecord(e1, s));
