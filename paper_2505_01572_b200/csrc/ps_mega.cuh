@@ -57,6 +57,7 @@ struct MegaParams {
   unsigned* tile_done;             // cumulative per-tile completion counters (all GEMM phases)
   int tp_n;                        // tensor-parallel group size (1: none)
   const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
+  unsigned spin_cap;               // phase-wait poll back-off cap (ns)
 };
 
 // Up to this many query rows per KV head the last-arriver combine inside the
@@ -104,12 +105,12 @@ PS_DEV unsigned ld_relaxed_u32(const unsigned* p) {
 PS_DEV void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // Poll with relaxed loads and a short back-off (a tight acquire spin from 148
 // SMs hammers one L2 line and invalidates L1 on every poll), then acquire once.
-PS_DEV void spin_until(const unsigned* p, unsigned target) {
+PS_DEV void spin_until(const unsigned* p, unsigned target, unsigned cap = 256) {
   unsigned ns = 32, polls = 0;
   unsigned long long t0 = 0;
   while ((int)(ld_relaxed_u32(p) - target) < 0) {
     __nanosleep(ns);
-    ns = ns < 256 ? ns * 2 : 256;
+    ns = ns < cap ? ns * 2 : cap;
     spin_check(polls, t0);
   }
   fence_acquire_gpu();
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
               fence_proxy_async_global();
             }
           } else {
-            spin_until(dphase, tphase);
+            spin_until(dphase, tphase, P.spin_cap);
             fence_proxy_async_global();
             phase_ready = true;
           }
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       const bool need_prev = ph > 0 && !skip && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
                                                   sph->g.mode != EPI_STORE && sph->dep_w > 0);
       if (need_prev && et == 0) {
-        spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body);
+        spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body, P.spin_cap);
         if (sph->xwait)           // tensor parallel: every peer's partial is published
           for (int q = 0; q < P.tp_n; ++q) spin_until_sys(P.peer_done[q] + (ph - 1), prev_head ? tgt_head : tgt_body);
       }
