@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libpipespec.so")
+# PS_LIB overrides the library path (A/B timing of kernel variants only)
+LIB_PATH = os.environ.get("PS_LIB") or os.path.join(PKG, "libpipespec.so")
 
 PS_OK, PS_E_INVALID, PS_E_CONTRACT, PS_E_CAPACITY, PS_E_CUDA, PS_E_NCCL, PS_E_STALE = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "PS_OK", -1: "PS_E_INVALID", -2: "PS_E_CONTRACT", -3: "PS_E_CAPACITY", -4: "PS_E_CUDA",

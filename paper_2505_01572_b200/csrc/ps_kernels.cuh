@@ -292,6 +292,30 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
                         int kbt, float* v, int e, int lane, int quarter, int R, int pos0, float* scratch,
                         unsigned long long* red, const float* rstd, const long long* kvrow, volatile int* flag) {
   bool finalized = false;
+  // Epilogue operands that do not depend on this tile's result (residual x and
+  // its gain; RoPE cos/sin) are loaded BEFORE the stream-K wait, so their
+  // round trip overlaps the partials' arrival instead of following it.
+  // (Rows bucket 16 only: at 32 rows the extra live registers spill.)
+  constexpr bool kPre = RP <= 16;
+  const long long tile_u00 = (long long)t * kbt;
+  const bool will_fin = kPre && ((seg_begin == tile_u00 && seg_end == tile_u00 + kbt) || sk_owner(U, G, tile_u00) == c);
+  float pre_x[RP];
+  float pre_g = 0.f;
+  float2 pre_cs[RP];
+  if (will_fin && p.mode == EPI_RESID) {
+    const int f = t * 128 + e;
+    const bool ok = f < p.N;
+    pre_g = ok ? __bfloat162float(p.gain[f]) : 0.f;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+  }
+  if (will_fin && p.mode == EPI_QKV && t < p.t2) {
+    const int f = t < p.t1 ? t * 128 + e : (t - p.t1) * 128 + e;
+    const int j = (f % p.hd) & ((p.hd >> 1) - 1);
+#pragma unroll
+    for (int r = 0; r < RP; ++r)
+      pre_cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * (p.hd >> 1) + j] : make_float2(1.f, 0.f);
+  }
   do {
     // ---- stream-K fixup: deterministic, fixed segment order ----
     // Partials are laid out [tile][seg][lane e][RP] so every thread moves
@@ -368,10 +392,13 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
     } else if (p.mode == EPI_RESID) {
       const int f = t * 128 + e;
       const bool ok = f < p.N;
-      const float g = ok ? __bfloat162float(p.gain[f]) : 0.f;
-      float xo[RP];
+      if constexpr (!kPre) {
+        pre_g = ok ? __bfloat162float(p.gain[f]) : 0.f;
 #pragma unroll
-      for (int r = 0; r < RP; ++r) xo[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+        for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+      }
+      const float g = pre_g;
+      const float* xo = pre_x;
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
         if (r >= R) break;
@@ -418,10 +445,12 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       const int hd = p.hd, half = hd >> 1;
       const int i = f % hd;
       if (kind < 2) {   // rotate-half RoPE at absolute positions pos0 + r
-        const int j = i & (half - 1);
-        float2 cs[RP];
+        if constexpr (!kPre) {
+          const int j = i & (half - 1);
 #pragma unroll
-        for (int r = 0; r < RP; ++r) cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * half + j] : make_float2(1.f, 0.f);
+          for (int r = 0; r < RP; ++r) pre_cs[r] = r < R ? p.rope_cs[(size_t)(pos0 + r) * half + j] : make_float2(1.f, 0.f);
+        }
+        const float2* cs = pre_cs;
 #pragma unroll
         for (int r = 0; r < RP; ++r) scratch[e * (RP + 1) + r] = v[r];
         named_bar(1, 128);
@@ -869,6 +898,21 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     const bool stamp = p.dbg != nullptr && tid == 0 && item == cta;
     if (stamp) p.dbg[cta * 8 + 0] = globaltimer();
     // ---- stage K/V chunk (one page run of 64 positions) and the Q rows (bf16, pre-scaled)
+    // Q loads first: they do not depend on the page-table lookup, so their
+    // round trip overlaps it instead of following it.
+    const int nwarps_used = (mrows + 15) / 16;
+    constexpr int QIT = (NW * 16 * (HD / 4) + NT - 1) / NT;   // float4 per thread
+    float4 qv[QIT];
+#pragma unroll
+    for (int k = 0; k < QIT; ++k) {
+      const int i = tid + k * NT;
+      const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
+      qv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < mrows) {
+        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+        qv[k] = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
+      }
+    }
     const long long page = p.page_table[k0 / p.page_size];
     const int slot0 = k0 % p.page_size;
     const __nv_bfloat16* Kp = p.kv + (size_t)page * p.page_stride +
@@ -889,21 +933,8 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
                    "l"(vsrc), "r"(ok) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    // Q rows (fp32 -> bf16, pre-scaled): loads batched ahead of the conversion
-    const int nwarps_used = (mrows + 15) / 16;
+    // Q rows (fp32 -> bf16, pre-scaled), loaded above
     {
-      constexpr int QIT = (NW * 16 * (HD / 4) + NT - 1) / NT;   // float4 per thread
-      float4 qv[QIT];
-#pragma unroll
-      for (int k = 0; k < QIT; ++k) {
-        const int i = tid + k * NT;
-        const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
-        qv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (m < mrows) {
-          const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-          qv[k] = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
-        }
-      }
 #pragma unroll
       for (int k = 0; k < QIT; ++k) {
         const int i = tid + k * NT;
@@ -1078,22 +1109,26 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
     const int kh = item / rows, mg = item % rows;
     const int rb = mg / kRB, m = mg % kRB;
     const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
-    float M = -INFINITY;
-    for (int cc = lane; cc < nchunks; cc += 32)
+    float acc[DPL];
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
+    // chunk `lane`'s (m, l) is loaded once and kept for both M and L (one
+    // round trip less when the context has <= 32 chunks); same arithmetic
+    float2 ml0 = make_float2(-INFINITY, 0.f);
+    if (lane < nchunks) ml0 = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + lane) * kRB + m) * 2));
+    float M = ml0.x;
+    for (int cc = lane + 32; cc < nchunks; cc += 32)
       M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float Lp = 0.f;
-    for (int cc = lane; cc < nchunks; cc += 32) {
+    float Lp = (ml0.x == -INFINITY) ? 0.f : exp2f(ml0.x - M) * ml0.y;
+    for (int cc = lane + 32; cc < nchunks; cc += 32) {
       const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
       Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
     const float invL = 1.0f / Lp;
-    float acc[DPL];
-#pragma unroll
-    for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
 #pragma unroll 8
     for (int cc = 0; cc < nchunks; ++cc) {
       const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2);

@@ -58,6 +58,7 @@ struct MegaParams {
   int tp_n;                        // tensor-parallel group size (1: none)
   const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
   unsigned spin_cap;               // phase-wait poll back-off cap (ns)
+  int tile_pub;                    // publish per-tile completion (read only by the per-tile dataflow X gate)
 };
 
 // Up to this many query rows per KV head the last-arriver combine inside the
@@ -86,7 +87,8 @@ struct MegaSmem {
   static constexpr int kOffBar = kOffAttn + attn_smem_bytes(4);
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
   static constexpr int kOffPhase = (kOffMisc + 64 + 127) / 128 * 128;   // MegaPhase copy (epilogue warps)
-  static constexpr int kBytes = kOffPhase + (int)((sizeof(MegaPhase) + 127) / 128 * 128) + 1024;
+  static constexpr int kOffStep = kOffPhase + (int)((sizeof(MegaPhase) + 127) / 128 * 128);   // StepIn copy
+  static constexpr int kBytes = kOffStep + (int)((sizeof(StepIn) + 127) / 128 * 128) + 1024;
 };
 
 PS_DEV unsigned ld_acquire_u32(const unsigned* p) {
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffMisc);
   volatile int* flag = (volatile int*)(smem + L::kOffMisc + 4);
   MegaPhase* sph = (MegaPhase*)(smem + L::kOffPhase);
+  StepIn* sstep = (StepIn*)(smem + L::kOffStep);
 
   constexpr int kTmemCols = RP == 16 ? 32 : 64;
   constexpr uint32_t kIdesc = idesc_bf16_f32<128, RP>();
@@ -311,6 +314,15 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     const int et = threadIdx.x - 64;                   // 0..127 in warp order 2..5
     uint32_t nacc = 0;
     int pref_item = -1;                                // attention chunk prefetched during QKV
+    // StepIn -> smem once: every later read of the step (rows, positions,
+    // generation, flags) in the epilogues / attention / argmax is a shared-
+    // memory hit instead of a global round trip on a phase's critical path.
+    {
+      static_assert(sizeof(StepIn) % 4 == 0, "StepIn words");
+      const int* src = reinterpret_cast<const int*>(P.step);
+      int* dst = reinterpret_cast<int*>(sstep);
+      for (int i = et; i < (int)(sizeof(StepIn) / 4); i += 128) dst[i] = src[i];
+    }
     const StepIn* st = P.step;
     const int R = st->R;
     const int pos0 = st->pos0;
@@ -328,6 +340,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       // epilogue needs no full-row statistic (O / down: RESID, no rstd); the
       // mainloop of every GEMM phase is gated per tile by the X loader.
       named_bar(1, 128);
+      if (et == 0) {   // the phase's step pointers -> the smem copy (read after the next barrier)
+        sph->g.step = sstep;
+        sph->a.step = sstep;
+        sph->em.step = sstep;
+        sph->am.step = sstep;
+      }
       // (A combine phase whose work the attention phase already did inline is
       // a pass-through: each CTA publishes it as soon as its own attention
       // items, combines included, are done.)
@@ -397,7 +415,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             u = seg_end;
             const bool fin = epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
                                              pos0, scratch, red, rstd, kvrow, flag);
-            if (fin) {                                  // publish tile t of this phase
+            if (fin && P.tile_pub) {                    // publish tile t of this phase
               named_bar(1, 128);
               if (et == 0) {
                 fence_proxy_async_global();
