@@ -172,6 +172,7 @@ static ps_status init_device_globals(int device) {
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 4>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32, 4>::kBytes));
   return PS_OK;
 }
@@ -608,6 +609,15 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
       cfg.dynamicSmemBytes = MegaSmem<32, 4>::kBytes;
       e = cudaLaunchKernelEx(&cfg, mega_kernel<32, 4>, mp);
     }
+  } else if (b == 0 && S->sh.d_model <= 2048) {
+    // Small models: a 6-slot ring.  A deeper ring runs further ahead across
+    // phase boundaries but queues the boundary's latency-critical loads
+    // (stream-K partials, X tiles, attention) behind more weight bytes, and
+    // the short phases of a small model lose more to that than they gain
+    // (measured: 1B draft step 0.943 ms with 6 slots vs 0.958 with 8; the 8B
+    // verify pass prefers 8: 3.597 vs 3.638 ms).
+    cfg.dynamicSmemBytes = MegaSmem<16, 6>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, mega_kernel<16, 6>, mp);
   } else if (b == 0) {
     cfg.dynamicSmemBytes = MegaSmem<16>::kBytes;
     e = cudaLaunchKernelEx(&cfg, mega_kernel<16>, mp);
