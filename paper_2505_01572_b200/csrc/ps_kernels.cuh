@@ -67,6 +67,7 @@ struct GemmParams {
   int t1, t2;                      // QKV: tiles [0,t1) q, [t1,t2) k, [t2,n) v
   int nq, nk;                      // QKV: rows of Wq, Wk (== Wv)
   int maxseg;                      // stream-K segments per tile (workspace stride)
+  int grid;                        // CTAs the stream-K partition spans (<= persistent grid)
   const StepIn* step;
   // deferred RMSNorm scale (nullptr: none)
   const float* ss_in; int ss_n, ss_ld; float inv_d, eps;

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (Q.kind != PH_GEMM) continue;
       const int kbt = Q.g.kb_total;
       const long long U = (long long)Q.g.n_tiles * kbt;
-      const int Gp = (int)min((long long)G, U);
+      const int Gp = (int)min((long long)min(G, Q.g.grid), U);
       if (c >= Gp) continue;
       const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
       for (long long u = ub; u < ue; ++u) fn(ph, Q, u, (int)(u / kbt), (int)(u % kbt));
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         if (Q.kind != PH_GEMM) continue;
         const int kbt = Q.g.kb_total;
         const long long U = (long long)Q.g.n_tiles * kbt;
-        const int Gp = (int)min((long long)G, U);
+        const int Gp = (int)min((long long)min(G, Q.g.grid), U);
         if (c >= Gp) continue;
         const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
         long long u = ub;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const GemmParams& gp = Q.g;
         const int kbt = gp.kb_total;
         const long long U = (long long)gp.n_tiles * kbt;
-        const int Gp = (int)min((long long)G, U);
+        const int Gp = (int)min((long long)min(G, Q.g.grid), U);
         if (gp.mode == EPI_QKV && ph + 1 < P.n_ph && P.ph[ph + 1].kind == PH_ATTN) {
           // the attention phase's context K/V does not depend on this phase:
           // stream this CTA's first chunk into smem while QKV runs

@@ -90,12 +90,26 @@ struct GemmShape {
   int n_tiles, kb_total, grid, maxseg;
 };
 
-static GemmShape gemm_shape(int n_tiles, int K, int num_sms) {
+// Stream-K partition of one GEMM over the persistent grid.  align_pct > 0:
+// if some k | kb_total with n_tiles * k >= align_pct% of the SMs exists, use
+// n_tiles * k CTAs (largest such k): every CTA then owns one tile-aligned
+// segment and each tile exactly k partials.  Small models' phases are latency-
+// bound, where fewer partials per tile beat the lost SMs (1B draft step 0.940
+// -> 0.921 ms at 60%); large models' are bandwidth-bound and keep all SMs (8B:
+// 128-CTA O / down phases cost +1.4%).
+static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) {
   GemmShape g;
   g.n_tiles = n_tiles;
   g.kb_total = K / 64;
   long long U = (long long)n_tiles * g.kb_total;
   g.grid = (int)std::min<long long>(num_sms, U);
+  if (align_pct > 0 && n_tiles <= num_sms) {
+    for (int k = num_sms / n_tiles; k >= 1; --k)
+      if (g.kb_total % k == 0) {
+        if ((long long)n_tiles * k * 100 >= (long long)num_sms * align_pct) g.grid = n_tiles * k;
+        break;
+      }
+  }
   auto owner = [&](long long u) { return (int)(((u + 1) * g.grid - 1) / U); };
   g.maxseg = 1;
   for (int t = 0; t < n_tiles; ++t) {
@@ -339,7 +353,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
       p.mode = EPI_QKV;
       p.N = hq + 2 * hkv;
-      p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg;
+      p.n_tiles = S->gs_qkv.n_tiles; p.kb_total = S->gs_qkv.kb_total; p.maxseg = S->gs_qkv.maxseg; p.grid = S->gs_qkv.grid;
       p.t1 = (hq + 127) / 128; p.t2 = p.t1 + (hkv + 127) / 128;
       p.nq = hq; p.nk = hkv;
       p.q = S->q; p.ld_q = hq;
@@ -364,7 +378,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       const LayerMaps& M = S->maps[l];
       P.kind = PH_GEMM;
       p.mode = EPI_RESID; p.N = d;
-      p.n_tiles = S->gs_o.n_tiles; p.kb_total = S->gs_o.kb_total; p.maxseg = S->gs_o.maxseg;
+      p.n_tiles = S->gs_o.n_tiles; p.kb_total = S->gs_o.kb_total; p.maxseg = S->gs_o.maxseg; p.grid = S->gs_o.grid;
       p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld; p.gain = W[PS_N_MLP];
       p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
       if (S->tp_size > 1) {   // row-parallel: partial -> exchange slot 0, reduced by the TPRED phase
@@ -379,7 +393,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       P.kind = PH_GEMM;
       P.gu = 1;
       p.mode = EPI_SWIGLU; p.N = sh.d_ffn;
-      p.n_tiles = S->gs_gu.n_tiles; p.kb_total = S->gs_gu.kb_total; p.maxseg = S->gs_gu.maxseg;
+      p.n_tiles = S->gs_gu.n_tiles; p.kb_total = S->gs_gu.kb_total; p.maxseg = S->gs_gu.maxseg; p.grid = S->gs_gu.grid;
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
       p.h = S->h; p.ld_h = sh.d_ffn;
       hm = HostMaps{&M.g, &M.u, &M.u, &S->map_xg[b]};
@@ -389,7 +403,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       const LayerMaps& M = S->maps[l];
       P.kind = PH_GEMM;
       p.mode = EPI_RESID; p.N = d;
-      p.n_tiles = S->gs_d.n_tiles; p.kb_total = S->gs_d.kb_total; p.maxseg = S->gs_d.maxseg;
+      p.n_tiles = S->gs_d.n_tiles; p.kb_total = S->gs_d.kb_total; p.maxseg = S->gs_d.maxseg; p.grid = S->gs_d.grid;
       p.x = S->x; p.ld_x = d; p.xg = S->xg; p.ld_xg = S->xg_ld;
       p.gain = (l + 1 < sh.n_layers) ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm;
       p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
@@ -403,7 +417,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
     case K_LMHEAD: {  // final norm + lm_head + argmax partials (a10)
       P.kind = PH_GEMM;
       p.mode = EPI_LMHEAD; p.N = sh.vocab;
-      p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg;
+      p.n_tiles = S->gs_lm.n_tiles; p.kb_total = S->gs_lm.kb_total; p.maxseg = S->gs_lm.maxseg; p.grid = S->gs_lm.grid;
       p.ss_in = S->ss; p.ss_n = ss_n; p.ss_ld = S->ss_ld; p.inv_d = inv_d; p.eps = sh.rms_eps;
       p.logits = S->logits; p.ld_logits = sh.vocab; p.amax = S->amax; p.amax_ld = S->lm_tiles;
       if (S->tp_size > 1) {   // vocab-parallel: global ids, per-rank keys in the exchange buffer
@@ -1003,11 +1017,12 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
   const int n = S->n_ctas;
-  S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n);
-  S->gs_o = gemm_shape((d + 127) / 128, hq, n);
-  S->gs_gu = gemm_shape((f + 63) / 64, d, n);
-  S->gs_d = gemm_shape((d + 127) / 128, f, n);
-  S->gs_lm = gemm_shape((sh.vocab + 127) / 128, d, n);
+  const int align = d <= 2048 ? 60 : 0;        // small models: tile-aligned partitions (gemm_shape)
+  S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n, align);
+  S->gs_o = gemm_shape((d + 127) / 128, hq, n, align);
+  S->gs_gu = gemm_shape((f + 63) / 64, d, n, align);
+  S->gs_d = gemm_shape((d + 127) / 128, f, n, align);
+  S->gs_lm = gemm_shape((sh.vocab + 127) / 128, d, n, align);
   S->lm_tiles = S->gs_lm.n_tiles;
   size_t ws_elems = 0;
   int max_tiles = 0;
@@ -1364,6 +1379,7 @@ static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_
   p.n_tiles = gs.n_tiles;
   p.kb_total = gs.kb_total;
   p.maxseg = gs.maxseg;
+  p.grid = gs.grid;
   p.step = din;
   p.out = out;
   p.ld_out = N;
