@@ -91,12 +91,12 @@ struct GemmShape {
 };
 
 // Stream-K partition of one GEMM over the persistent grid.  align_pct > 0:
-// if some k | kb_total with n_tiles * k >= align_pct% of the SMs exists, use
-// n_tiles * k CTAs (largest such k): every CTA then owns one tile-aligned
-// segment and each tile exactly k partials.  Small models' phases are latency-
-// bound, where fewer partials per tile beat the lost SMs (1B draft step 0.940
-// -> 0.921 ms at 60%); large models' are bandwidth-bound and keep all SMs (8B:
-// 128-CTA O / down phases cost +1.4%).
+// if k = floor(#SMs / n_tiles) CTAs per tile keep >= align_pct% of the SMs
+// busy, use n_tiles * k CTAs: every CTA then owns one tile-aligned segment
+// and each tile exactly k partials.  Small models' phases are latency-bound,
+// where fewer partials per tile beat the lost SMs (1B draft step 0.940 ->
+// 0.919 ms at 60%); large models' are bandwidth-bound and keep >= 95% (8B:
+// QKV on 144 CTAs -0.25%; O / down on 128 CTAs would cost +1.4%).
 static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) {
   GemmShape g;
   g.n_tiles = n_tiles;
@@ -104,11 +104,9 @@ static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) 
   long long U = (long long)n_tiles * g.kb_total;
   g.grid = (int)std::min<long long>(num_sms, U);
   if (align_pct > 0 && n_tiles <= num_sms) {
-    for (int k = num_sms / n_tiles; k >= 1; --k)
-      if (g.kb_total % k == 0) {
-        if ((long long)n_tiles * k * 100 >= (long long)num_sms * align_pct) g.grid = n_tiles * k;
-        break;
-      }
+    // sk_begin splits at kb_total*c/k: tile-aligned for any k (<= kb_total: no empty CTA ranges)
+    const int k = std::min(num_sms / n_tiles, g.kb_total);
+    if ((long long)n_tiles * k * 100 >= (long long)num_sms * align_pct) g.grid = n_tiles * k;
   }
   auto owner = [&](long long u) { return (int)(((u + 1) * g.grid - 1) / U); };
   g.maxseg = 1;
@@ -1017,7 +1015,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
   const int n = S->n_ctas;
-  const int align = d <= 2048 ? 60 : 0;        // small models: tile-aligned partitions (gemm_shape)
+  const int align = d <= 2048 ? 60 : 95;       // tile-aligned partitions where they pay (gemm_shape)
   S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n, align);
   S->gs_o = gemm_shape((d + 127) / 128, hq, n, align);
   S->gs_gu = gemm_shape((f + 63) / 64, d, n, align);
