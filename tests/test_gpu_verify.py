@@ -273,3 +273,37 @@ def test_70b_width_one_layer():
     check_logits(logits, ref["logits"])
     check_verify((a, nxt), ref, len(window))
     st.close()
+
+
+def test_long_context_head_dim_128():
+    """head_dim 128 (the LLaMA-3.1-8B attention geometry: llama3 RoPE, GQA
+    g=4) at a 4.2K context: 66 chunks per row (the combine's > 32-chunk path),
+    264 attention items > 148 CTAs; parity vs the oracle, and a verify over
+    accepted drafts reproduces the AR steps' logits bit-exactly (row-bucket
+    invariance with rows crossing a chunk boundary)."""
+    from paper_2505_01572_b200 import Stage
+    s = replace(synth.preset("llama3.1-8b"), name="hd128-long", n_layers=2, d_model=2048, n_heads=16,
+                n_kv_heads=4, d_ffn=2048, vocab=4096)
+    wt = synth.make_weights(s, seed=9, device="cuda")
+    w64 = synth.weights_to_numpy(wt)
+    n = 4222                                   # rows of the window straddle position 4224 = 66 * 64
+    st = Stage(s, wt, max_seq=n + 64)
+    prompt = list(synth.make_prompt(s.vocab, n, seed=10))
+    st.prefill(prompt)
+    rows = []
+    for _ in range(5):
+        a, nxt, lg = st.verify([], want_logits=True)
+        rows.append(lg[0])
+    stream = st.tokens()[n:]
+    st.prefill(prompt)
+    window = stream[:4]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    assert a == 4 and nxt == stream[4]
+    assert np.array_equal(logits, np.stack(rows))
+    st.prefill(prompt)
+    window = stream[:2] + [(stream[2] + 5) % s.vocab]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
