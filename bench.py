@@ -61,46 +61,87 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks, throttle reasons and power sampled during the timed region
+    (NVML every 10 ms; nvidia-smi every 200 ms if NVML is unavailable), plus
+    the board's energy counter across the region (J per token, P:296 4.5)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []            # (sm_mhz, max_mhz, [reason names], power_w)
+        self.energy_j = None
         self._stop = threading.Event()
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nv = None
         self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _sample_nvml(self):
+        nv, h = self._nv, self._h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        reasons = [n for n, b in zip(self.NAMES, bits) if r & b]
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+        self.samples.append((float(sm), float(mx), reasons, pw))
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            reasons = [self.NAMES[i] for i in range(4) if "Active" in f[2 + i] and not f[2 + i].startswith("Not")]
+            num = lambda x: float(x) if x.replace(".", "").isdigit() else float("nan")
+            self.samples.append((num(f[0]), num(f[1]), reasons, float("nan")))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nv else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nv else 0.2)
+
+    def _energy_mj(self):
+        try:
+            return self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h) if self._nv else None
+        except Exception:
+            return None
 
     def __enter__(self):
+        self._e0 = self._energy_mj()
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        e1 = self._energy_mj()
+        if self._e0 is not None and e1 is not None:
+            self.energy_j = (e1 - self._e0) / 1e3
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
-                          and not s[2 + i].startswith("Not")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples if s[0] == s[0]]
+        mx = [s[1] for s in self.samples if s[1] == s[1]]
+        pw = [s[3] for s in self.samples if s[3] == s[3]]
+        reasons = sorted({n for s in self.samples for n in s[2]})
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self._nv else "nvidia-smi"}
+        if pw:
+            out["power_w_median"] = statistics.median(pw)
+        return out
 
 
 # ----------------------------------------------------------------------------- dist
@@ -398,7 +439,9 @@ def main():
         assert out == S[:args.gen], f"{mname}: output differs from M_K autoregressive decoding"
         modes[mname] = {"tokens_per_s": len(out) / dtm, "decode_s": st_.wall_ns / 1e9,
                         "tokens_per_s_decode": len(out) / (st_.wall_ns / 1e9) if st_.wall_ns else None,
-                        "verify_steps": int(st_.verify_steps[1]), "rollbacks": int(st_.rollbacks[0])}
+                        "verify_steps": int(st_.verify_steps[1]), "rollbacks": int(st_.rollbacks[0]),
+                        # tokens appended per verify step of M_K (Fig.4's histogram)
+                        "accept_hist": {int(k): int(c) for k, c in enumerate(st_.accept_hist) if c}}
     value = tot_tokens / dev_s
     e2e = tot_tokens / wall_s
     fwd_per_step = g + 1
@@ -431,6 +474,10 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if clk.energy_j is not None and tokens > 0:
+        # board energy counter across the timed region (this GPU's tokens; paper 4.5)
+        line["energy"] = {"joules": clk.energy_j, "j_per_token": clk.energy_j / tokens,
+                          "avg_w": clk.energy_j / max(wall_s, 1e-9), "source": "nvmlDeviceGetTotalEnergyConsumption"}
     if world > 1 and args.multi_gpu_extras:
         line["multi_gpu"] = multi_gpu_extras(args, rank, world, ts, wt, drafter, target, prompt, S, g)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
