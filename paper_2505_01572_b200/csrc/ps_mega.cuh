@@ -84,7 +84,8 @@ struct MegaSmem {
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
   static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 127) / 128 * 128;
-  static constexpr int kOffBar = kOffAttn + attn_smem_bytes(4);
+  static constexpr int kAttnBytes = attn_smem_bytes(4);
+  static constexpr int kOffBar = kOffAttn + kAttnBytes;
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
   static constexpr int kOffPhase = (kOffMisc + 64 + 127) / 128 * 128;   // MegaPhase copy (epilogue warps)
   static constexpr int kOffStep = kOffPhase + (int)((sizeof(MegaPhase) + 127) / 128 * 128);   // StepIn copy
@@ -413,8 +414,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             mbar_arrive(&tempty[acc]);
             ++nacc;
             u = seg_end;
+            // (the attention area stages stream-K partials, except in QKV phases:
+            // the next attention phase's K/V chunk is prefetched into it then)
             const bool fin = epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
-                                             pos0, scratch, red, rstd, kvrow, flag);
+                                             pos0, scratch, red, rstd, kvrow, flag,
+                                             gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
+                                             L::kAttnBytes / 16);
             if (fin && P.tile_pub) {                    // publish tile t of this phase
               named_bar(1, 128);
               if (et == 0) {
