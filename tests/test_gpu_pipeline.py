@@ -61,7 +61,11 @@ def test_async_pipespec_lossless_two_stage(pair, alpha):
     ar, _ = pipeline_run([d, v], prompt, 40, mode=PS_MODE_AR)
     d.set_synthetic(ar + [0] * 16, len(prompt), level=0, top=1, alphas=[alpha], seed=5)
     ps, stats = pipeline_run([d, v], prompt, 40, mode=PS_MODE_PIPESPEC, gammas=[0, 6])
-    assert ps == ar
+    i = next((j for j in range(min(len(ps), len(ar))) if ps[j] != ar[j]), None)
+    assert ps == ar, (f"first diff at {i}: ps {ps[i:i + 4] if i is not None else ps[len(ar):]} "
+                      f"ar {ar[i:i + 4] if i is not None else []}; steps {list(stats.steps[:2])} "
+                      f"verify {list(stats.verify_steps[:2])} rollbacks {list(stats.rollbacks[:2])} "
+                      f"hist {[int(x) for x in stats.accept_hist[:8]]}")
     assert stats.tokens == 40
     assert stats.steps[1] >= 1
     if alpha == 1.0:
