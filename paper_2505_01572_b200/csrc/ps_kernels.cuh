@@ -537,8 +537,9 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       const bool want = p.logits != nullptr && (p.step->flags & kFlagLogits);
 #pragma unroll
       for (int r = 0; r < RP; ++r) {
+        if (r >= R) break;                       // live rows only (a warp max per row)
         const float z = v[r] * rstd[r];
-        if (want && ok && r < R) p.logits[(size_t)r * p.ld_logits + f] = z;
+        if (want && ok) p.logits[(size_t)r * p.ld_logits + f] = z;
         unsigned long long k = ok ? argmax_key(z, (uint32_t)(f + p.vocab_off)) : 0ull;
         k = warp_max_u64(k);
         if (lane == 0) red[quarter * RP + r] = k;

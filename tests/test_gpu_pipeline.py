@@ -69,7 +69,13 @@ def test_async_pipespec_lossless_two_stage(pair, alpha):
     assert stats.tokens == 40
     assert stats.steps[1] >= 1
     if alpha == 1.0:
-        assert stats.verify_steps[1] >= 1
+        # With lookahead 0 the verifier takes an AR step whenever no draft is
+        # waiting (reading R7), so on one GPU the schedule may never verify a
+        # window (the two stages' kernels serialise).  Lookahead 1 makes it
+        # wait for a draft: every verifier step is then a verification.
+        ps1, st1 = pipeline_run([d, v], prompt, 40, mode=PS_MODE_PIPESPEC, gammas=[0, 6], lookaheads=[0, 1])
+        assert ps1 == ar
+        assert st1.verify_steps[1] >= 1 and st1.verify_steps[1] == st1.steps[1]
     d.clear_synthetic()
 
 
