@@ -430,10 +430,14 @@ def main():
     from paper_2505_01572_b200 import pipeline_run
     from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
     modes = {}
-    for mname, mode in (("ar", PS_MODE_AR), ("sync_sd", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
+    # async PipeSpec with lookahead 0 (the paper's setting) and, as Fig.5's
+    # lookahead sweep, with the verifier waiting for L >= 1 drafts (reading R7)
+    runs = [("ar", PS_MODE_AR, 0), ("sync_sd", PS_MODE_SYNC_SD, 0), ("pipespec_async", PS_MODE_PIPESPEC, 0)]
+    runs += [(f"pipespec_async_lookahead{la}", PS_MODE_PIPESPEC, la) for la in (1, 2, 4)]
+    for mname, mode, la in runs:
         torch.cuda.synchronize()
         w0m = time.perf_counter()
-        out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g])
+        out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g], lookaheads=[0, la])
         torch.cuda.synchronize()
         dtm = time.perf_counter() - w0m
         assert out == S[:args.gen], f"{mname}: output differs from M_K autoregressive decoding"
