@@ -295,8 +295,12 @@ def run_pipespec(cfgs, model, prompt, max_new, eos=None, seed=0, max_lead=None,
             return
         P = bufs[i - 1]
         n = O.n
-        if P.n >= n and P.t[n - 1] != O.t[n - 1]:
-            rollback_below(i, T)             # drafter disagrees at my pending position
+        if P.n >= n and P.first_mismatch(O) < n:
+            # the drafter's buffer disagrees with mine somewhere in O_i[0:n] (its
+            # token at my pending position, or -- after a higher stage's rollback
+            # left it on a short prefix of O_i -- earlier): resync it to O_i
+            # (Alg.1 P:97 "Rollback O_i", reading R2)
+            rollback_below(i, T)
         m = P.first_mismatch(O)
         avail = P.n - n if m >= n else 0
         w = min(max(avail, 0), cfgs[i].gamma)
