@@ -140,14 +140,16 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* weights
 ps_status ps_stage_destroy(ps_stage* stage);
 
 /* Tensor-parallel group wiring (see ps_placement).  PS_TP_HANDLE_BYTES is the
- * size of one exported handle (a cudaIpcMemHandle_t of the rank's exchange
- * buffer).  ps_tp_handle writes this rank's handle; ps_tp_connect takes all
- * tp_size handles in rank order (host array [tp_size][PS_TP_HANDLE_BYTES],
- * this rank's own entry ignored) and maps the peers' buffers, enabling peer
- * access; ps_tp_connect_local links n stages created in THIS process (rank
+ * size of one exported handle: the cudaIpcMemHandle_t of the rank's exchange
+ * buffer plus its rank, megakernel grid (CTAs), buffer size and shard shape.
+ * ps_tp_handle writes this rank's handle; ps_tp_connect takes all tp_size
+ * handles in rank order (host array [tp_size][PS_TP_HANDLE_BYTES], this
+ * rank's own entry ignored), rejects a group whose ranks differ in grid or
+ * shard shape (PS_E_INVALID: every rank waits for its peers' phase counters at
+ * its own grid's target), and maps the peers' buffers, enabling peer access; ps_tp_connect_local links n stages created in THIS process (rank
  * order = array order, n == their tp_size).  A forward on an unconnected
  * tp_size > 1 stage returns PS_E_INVALID. */
-#define PS_TP_HANDLE_BYTES 64
+#define PS_TP_HANDLE_BYTES 256
 ps_status ps_tp_handle(ps_stage* stage, void* handle_out);
 ps_status ps_tp_connect(ps_stage* stage, const void* handles);
 ps_status ps_tp_connect_local(ps_stage* const* stages, int32_t n);
@@ -190,6 +192,40 @@ ps_status ps_draft(ps_stage* stage, int32_t n_steps, int32_t* out_tokens);
 ps_status ps_verify(ps_stage* stage, const int32_t* window, int32_t w,
                     int32_t* accepted_len, int32_t* next_token, float* opt_logits);
 
+/* Asynchronous verification pass (SURVEY §8(b) "an async variant writes
+ * a/next/kv_len to device memory + pinned mirror and records a CUDA event").
+ * ps_verify_async enqueues the same forward as ps_verify on the stage's stream
+ * and returns without waiting: `window` may be host memory or DEVICE memory
+ * (e.g. a drafter's output on a peer GPU); a device window is gathered into
+ * the forward's rows by an on-stream copy, never read by the host.  The
+ * result lands in the stage-owned device record *ticket->d_result and its
+ * mapped pinned mirror *ticket->h_result (ps_verify_result, valid once
+ * ticket->event -- a cudaEvent_t recorded after the forward -- has completed).
+ * Until ps_verify_wait the stage is IN FLIGHT: every call that uses or changes
+ * it (verify, draft, prefill, resync, rollback, synthetic, timing) returns
+ * PS_E_INVALID; ps_verify_query, ps_stage_tokens and ps_stage_get_info are
+ * allowed (O_i is unchanged until the commit).  ps_verify_wait blocks on the event,
+ * then commits exactly as ps_verify does (O_i := x ++ d[0:a] ++ [next] with
+ * d[0:a] = pred[0:a], kv_len = n + a, pages beyond kv_len freed) and returns
+ * a and next.  A device window holding a token >= vocab is reported by the
+ * kernel (rows = -1 in the record) and ps_verify_wait returns PS_E_INVALID
+ * without changing O_i.  ps_verify_query sets *done to 1 if the in-flight
+ * pass has completed (0 otherwise; 1 if nothing is in flight). */
+typedef struct ps_verify_result {
+  int32_t a, next;          /* accepted length, correction/bonus token          */
+  int32_t rows;             /* rows of the forward (-1: invalid device window)  */
+  int32_t kv_len;           /* n + a: KV positions valid after the commit       */
+  int32_t pred[32];         /* greedy prediction of rows row0.. (pred[j], j<=w) */
+} ps_verify_result;
+typedef struct ps_verify_ticket {
+  const ps_verify_result* d_result;   /* device address                         */
+  const ps_verify_result* h_result;   /* mapped pinned host mirror               */
+  void* event;                        /* cudaEvent_t, owned by the stage         */
+} ps_verify_ticket;
+ps_status ps_verify_async(ps_stage* stage, const int32_t* window, int32_t w, ps_verify_ticket* ticket);
+ps_status ps_verify_wait(ps_stage* stage, int32_t* accepted_len, int32_t* next_token);
+ps_status ps_verify_query(ps_stage* stage, int32_t* done);
+
 /* Rollback: requires 1 <= keep_len <= len(O_i) else PS_E_CONTRACT.
  * O_i := O_i[0:keep_len], kv_len := min(kv_len, keep_len-1), pending :=
  * O_i[keep_len-1]; frees pages wholly beyond kv_len (O(#freed pages)).
@@ -208,6 +244,7 @@ typedef struct ps_stage_info {
    * over all verify/draft forwards since creation (ps_stage_reset_timers). */
   double last_fwd_ms, sum_fwd_ms;
   int64_t n_fwd;
+  int32_t max_window, max_seq;  /* the stage's creation options                */
 } ps_stage_info;
 ps_status ps_stage_reset_timers(ps_stage* stage);
 ps_status ps_stage_get_info(const ps_stage* stage, ps_stage_info* info);
@@ -226,13 +263,45 @@ ps_status ps_set_synthetic(ps_stage* stage, const int32_t* S, int32_t len_S, int
 /* Pipeline modes. */
 enum { PS_MODE_AR = 0, PS_MODE_SYNC_SD = 1, PS_MODE_PIPESPEC = 2 };
 
+/* One entry of a run's event log (for trace replay against the oracle's
+ * brute-force verify).  Entries are written
+ * in the order the committed buffers change (under the runtime's lock), so
+ * replaying them from the prompt reproduces every O_i:
+ *   PS_EV_DRAFT   stage 0 appended `next` to O_0[0:n]
+ *   PS_EV_VERIFY  stage i verified window[0:w] on O_i[0:n]: O_i := O_i[0:n] ++
+ *                 window[0:a] ++ [next]
+ *   PS_EV_AR      the same with w = 0 (no draft available, lookahead 0)
+ *   PS_EV_RESYNC  O_stage := O_origin[0:n] (rollback cascade, R2)
+ *   PS_EV_STALE   a finished step of `stage` (its kind in `origin`) discarded
+ *                 by an epoch change                                          */
+enum { PS_EV_DRAFT = 0, PS_EV_VERIFY = 1, PS_EV_AR = 2, PS_EV_RESYNC = 3, PS_EV_STALE = 4 };
+typedef struct ps_event {
+  int64_t t_ns;                   /* since the start of decoding              */
+  int32_t stage, kind, n, w, a, next, origin, pad;
+  int32_t window[32];
+} ps_event;
+
 typedef struct ps_run_opts {
   int32_t mode;
   int32_t max_new_tokens;
   int32_t eos_id;                 /* -1 = none */
-  const int32_t* gamma;           /* host [k]: window cap per stage (stage 0 unused) */
+  const int32_t* gamma;           /* host [k]: window cap per stage (stage 0 unused);
+                                     NULL = 8; SYNC_SD / PIPESPEC need 1..max_window */
   const int32_t* lookahead;       /* host [k]: 0 = verify whenever >= 1 draft */
   int32_t max_lead;               /* draft ring depth per stage pair (>= max gamma + 1) */
+  /* Optional synthetic acceptance (reading R24): alpha
+   * NULL = the models' own predictions; else host [k-1], alpha[i] =
+   * alpha_{i,i+1}.  The run first decodes max_new_tokens of M_K
+   * autoregressively (outside wall_ns) as the target stream S, then sets the
+   * chained override with `seed` on every stage i < K (ps_set_synthetic). */
+  const double* alpha;
+  uint64_t seed;
+  /* Optional virtual latencies: host [k] or NULL; stage i's every step
+   * (draft / verify / AR) lasts at least virtual_ns[i] (the host pads it),
+   * to emulate the paper's relative model speeds on any device. */
+  const int64_t* virtual_ns;
+  ps_event* event_log;            /* NULL or host [event_cap]                  */
+  int32_t event_cap;
 } ps_run_opts;
 
 typedef struct ps_run_stats {
@@ -240,6 +309,11 @@ typedef struct ps_run_stats {
   int64_t wall_ns;                /* from first decode step to the last token  */
   int64_t steps[8], verify_steps[8], rollbacks[8], busy_ns[8];
   int64_t accept_hist[64];        /* tokens appended per stage-K verify step   */
+  int64_t n_events;               /* events written (<= event_cap); events past
+                                     the cap are counted in events_dropped     */
+  int64_t events_dropped;
+  int64_t fwd_ns[8], n_fwd[8];    /* device time (CUDA events) of the stages'
+                                     forwards during the run, and their count */
 } ps_run_stats;
 
 /* Alg.1 end to end: prefill every stage with the prompt, then run the k
@@ -273,6 +347,15 @@ ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const c
 /* Device-side timing hook for benchmarks: number of kernels this library has
  * launched (graph launches count their kernels) since process start. */
 int64_t ps_kernel_launch_count(void);
+
+/* Per-kernel timing (measurement only): re-launch one kernel of the stage's
+ * most recent forward configuration (same rows bucket, same device StepIn)
+ * through the one-kernel-per-step path, `iters` times back to back on the
+ * stage stream; *avg_ms = CUDA-event time per launch.  kind: 0 embed, 1 QKV
+ * GEMM, 2 attention, 3 O GEMM, 4 gate/up GEMM, 5 down GEMM, 6 lm_head GEMM,
+ * 7 argmax/scan; layer selects the weights.  Overwrites the stage's scratch
+ * activations (not its token buffer or KV below kv_len). */
+ps_status ps_time_kernel(ps_stage* stage, int32_t kind, int32_t layer, int32_t iters, double* avg_ms);
 
 #ifdef __cplusplus
 }

@@ -149,6 +149,22 @@ PS_DEV unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// %globaltimer stamps for the phase timeline (scripts/timeline.py): compiled
+// only into the PS_TRACE=1 build (libpipespec_trace.so), so the product
+// kernels carry no debug branches or registers.
+#ifndef PS_TRACE
+#define PS_TRACE 0
+#endif
+#if PS_TRACE
+#define PS_TRACE_STAMP(buf, idx)                              \
+  do {                                                        \
+    if ((buf) != nullptr) (buf)[idx] = ::ps::globaltimer();   \
+  } while (0)
+#else
+#define PS_TRACE_STAMP(buf, idx) \
+  do {                           \
+  } while (0)
+#endif
 PS_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -216,8 +232,10 @@ PS_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
 PS_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 // Greedy key: larger logit wins, equal logits -> lower index wins (reading R12).
+// -0.0 is canonicalised to +0.0 first (-0.0 + 0.0 = +0.0 under round-to-
+// nearest), so equal-comparing zeros tie like np.argmax's and the lower index wins.
 PS_DEV unsigned long long argmax_key(float v, uint32_t idx) {
-  uint32_t u = __float_as_uint(v);
+  uint32_t u = __float_as_uint(__fadd_rn(v, 0.0f));
   u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
   return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
 }

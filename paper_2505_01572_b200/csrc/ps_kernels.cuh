@@ -30,6 +30,26 @@ namespace ps {
 constexpr int kMaxRows = 32;       // max rows per forward (w <= 31)
 constexpr int kAttnChunk = 64;     // keys per split-KV chunk (absolute positions)
 
+// Split-bf16 activations (reading R28).  Every bf16 operand the
+// path derives from an fp32 activation is stored as a PAIR hi = bf16(v),
+// lo = bf16(v - hi) (~16 significant bits): the GEMM operands x∘g, attention
+// output and SwiGLU output (buffers of 2*kMaxRows rows: hi rows [0, 32), lo
+// rows [32, 64); the tensor cores take both, W·hi + W·lo accumulated in fp32),
+// the query and softmax probabilities inside attention, and the KV cache.
+// With plain bf16 activations a 32-layer LLaMA-3.1-8B forward drifts ~4% of
+// max|logit| from exact arithmetic (scripts/precision_probe.py), twice the
+// north star's bound; split operands keep it at fp32-like error.
+PS_DEV void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16(v);
+  lo = __float2bfloat16(v - __bfloat162float(hi));
+}
+PS_DEV uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+// KV cache page layout [page][layer][plane][kv_head][page_size][hd] bf16,
+// planes K_hi, K_lo, V_hi, V_lo.
+constexpr int kKvPlanes = 4;
+
 struct StepIn {                    // written by the host before every forward
   int32_t R;                       // rows in this forward, 1..kMaxRows
   int32_t pos0;                    // absolute position of row 0
@@ -46,8 +66,8 @@ struct StepIn {                    // written by the host before every forward
 constexpr int kFlagLogits = 1;
 constexpr int kFlagSynth = 2;
 
-struct StepOut {                   // written by argmax_scan_kernel
-  int32_t a, next, R, pad;
+struct StepOut {                   // written by argmax_scan_kernel (== ps_verify_result)
+  int32_t a, next, R, kv_len;      // R = -1: a row token was out of range (nothing committed)
   int32_t pred[kMaxRows];
 };
 
@@ -106,7 +126,7 @@ PS_DEV int sk_owner(long long U, int G, long long u) { return (int)(((u + 1) * G
 template <int RP, int STAGES, bool GU>
 struct GemmSmem {
   static constexpr int kABytes = 128 * 64 * 2;      // 16 KB weight tile (128 rows x 64 K)
-  static constexpr int kXBytes = RP * 64 * 2;       // activation tile (RP rows x 64 K)
+  static constexpr int kXBytes = 2 * RP * 64 * 2;   // activation tiles: hi then lo (RP rows x 64 K each)
   static constexpr int kScratch = 128 * (RP + 1) * 4;
   static constexpr int kOffX = STAGES * kABytes;
   static constexpr int kOffScratch = kOffX + STAGES * kXBytes;
@@ -390,12 +410,12 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
 #pragma unroll
         for (int j = 0; j < RP / 2; ++j)
           if (j < R2) st_ll2(wsp + ((size_t)seg * 128 + e) * RP + 2 * j, ll_pack(v[2 * j], flag), ll_pack(v[2 * j + 1], flag));
-        if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+        if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
         break;
       }
-      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = p.dbg[c * 4 + 1] = globaltimer();
+      if (e == 0) { PS_TRACE_STAMP(p.dbg, c * 4 + 0); PS_TRACE_STAMP(p.dbg, c * 4 + 1); }
       sk_reduce_ll<RP>(wsp, v, R2, e, seg, nseg, flag);
-      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 2] = globaltimer();
+      if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 2);
     } else if (!(seg_begin == tile_u0 && seg_end == tile_u0 + kbt)) {
       const int first = sk_owner(U, G, tile_u0);
       const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
@@ -415,17 +435,17 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       // a barrier that orders all 128 threads' partial stores before it.
       if (seg != 0) {
         named_bar(1, 128);
-        if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+        if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
         if (e == 0) red_release_add_gpu(&p.counters[t], 1u);
         break;
       }
-      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 0] = globaltimer();
+      if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
       if (e == 0) {
         spin_until_gpu(&p.counters[t], (unsigned)(nseg - 1));
         p.counters[t] = 0u;                    // ready for the next forward
       }
       named_bar(1, 128);
-      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 1] = globaltimer();
+      if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 1);
       // reduce: only the live rows, with up to 16 float4 loads in flight
       if (R4 <= 1) sk_reduce<RP, 1>(wsp, v, e, seg, nseg);
       else if (R4 <= 2) sk_reduce<RP, 2>(wsp, v, e, seg, nseg);
@@ -434,7 +454,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       // R=9 +0.6%, so the 16-in-flight register version stays up to 16 rows)
       else if (stage != nullptr) sk_reduce_smem<RP>(wsp, v, e, seg, nseg, R4, stage, stage_f4);
       else sk_reduce<RP, (RP / 4 < 8 ? RP / 4 : 8)>(wsp, v, e, seg, nseg);
-      if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 2] = globaltimer();
+      if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 2);
     }
 
     // ---- fused epilogues (global loads batched ahead of use) ----
@@ -462,7 +482,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
         if (ok) {
           const float xn = xo[r] + v[r];
           p.x[(size_t)r * p.ld_x + f] = xn;
-          p.xg[(size_t)r * p.ld_xg + f] = __float2bfloat16(xn * g);
+          split_bf16(xn * g, p.xg[(size_t)r * p.ld_xg + f], p.xg[(size_t)(r + kMaxRows) * p.ld_xg + f]);
           sq = xn * xn;
         }
         sq = warp_sum(sq);
@@ -485,7 +505,8 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
             if (r < R) {
               const float gt = scratch[e * (RP + 1) + r];
               const float up = scratch[(e + 64) * (RP + 1) + r];
-              p.h[(size_t)r * p.ld_h + f] = __float2bfloat16(gt / (1.0f + __expf(-gt)) * up);
+              split_bf16(gt / (1.0f + __expf(-gt)) * up, p.h[(size_t)r * p.ld_h + f],
+                         p.h[(size_t)(r + kMaxRows) * p.ld_h + f]);
             }
           }
         }
@@ -525,10 +546,11 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
             if (r < R) p.q[(size_t)r * p.ld_q + f] = v[r];
         } else {
           const int kh = f / hd;
-          const size_t head_off = ((size_t)((p.layer * 2 + (kind - 1)) * p.hkv + kh) * p.page_size) * hd + i;
+          const size_t plane = (size_t)p.hkv * p.page_size * hd;   // elements per (layer, plane)
+          const size_t head_off = ((size_t)(p.layer * kKvPlanes + 2 * (kind - 1)) * p.hkv + kh) * p.page_size * hd + i;
 #pragma unroll
           for (int r = 0; r < RP; ++r)
-            if (r < R) p.kv[(size_t)kvrow[r] + head_off] = __float2bfloat16(v[r]);
+            if (r < R) split_bf16(v[r], p.kv[(size_t)kvrow[r] + head_off], p.kv[(size_t)kvrow[r] + head_off + plane]);
         }
       }
     } else {  // EPI_LMHEAD: logits (on request) + per-row greedy key, atomicMax (order-free, exact)
@@ -554,7 +576,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       named_bar(1, 128);
     }
     finalized = true;
-    if (p.dbg != nullptr && e == 0) p.dbg[c * 4 + 3] = globaltimer();
+    if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 3);
   } while (0);
   return finalized;   // this CTA completed tile t (its outputs are written)
 }
@@ -594,7 +616,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
   const int G = gridDim.x, c = blockIdx.x;
   const long long u_begin = sk_begin(U, G, c), u_end = sk_begin(U, G, c + 1);
   const int kbt = p.kb_total;
-  const unsigned long long t_entry = (p.dbg != nullptr && threadIdx.x == 0) ? globaltimer() : 0ull;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mA0);
@@ -611,7 +632,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
-  if (p.dbg != nullptr && threadIdx.x == 0) p.dbg[c * 4 + 0] = t_entry;
+  if (threadIdx.x == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -630,9 +651,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
           tma_load_2d(dst, &mA0, &full[s], kb * 64, t * 128, kEvictFirst);
         }
       };
-      auto load_X = [&](long long u, int s) {
+      auto load_X = [&](long long u, int s) {     // hi rows [0, RP), lo rows [kMaxRows, kMaxRows + RP)
         const int kb = (int)(u % kbt);
         tma_load_2d(sX + s * L::kXBytes, &mX, &full[s], kb * 64, 0, kEvictLast);
+        tma_load_2d(sX + s * L::kXBytes + RP * 128, &mX, &full[s], kb * 64, kMaxRows, kEvictLast);
       };
       const long long n_units = u_end - u_begin;
       const int pre = (int)(n_units < STAGES ? n_units : STAGES);
@@ -660,7 +682,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (p.dbg != nullptr) p.dbg[c * 4 + 1] = globaltimer();
+      PS_TRACE_STAMP(p.dbg, c * 4 + 1);
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
@@ -686,9 +708,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
             mbar_arrive(&empty[stage]);
           } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k) {   // W·x_hi + W·x_lo (split-bf16 operand)
               mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
                        (u != seg_begin || k > 0) ? 1u : 0u);
+              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + RP * 128 + 32 * k), kIdesc, 1u);
+            }
             mma_commit(&empty[stage]);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -698,7 +722,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
-      if (p.dbg != nullptr) p.dbg[c * 4 + 2] = globaltimer();
+      PS_TRACE_STAMP(p.dbg, c * 4 + 2);
     }
   } else {
     // ================= epilogue (128 threads, TMEM lane = e) =================
@@ -733,14 +757,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
 
   tc_fence_before();
   __syncthreads();
-  if (p.dbg != nullptr && threadIdx.x == 0) p.dbg[c * 4 + 3] = globaltimer();
+  if (threadIdx.x == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 3);
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
 }
 
 // ------------------------------------------------------------------ embed (a1-a3)
 struct EmbedParams {
   const StepIn* step;
-  const __nv_bfloat16* embed; int d;
+  const __nv_bfloat16* embed; int d; int vocab;
   const __nv_bfloat16* gain;
   float* x; int ld_x;
   __nv_bfloat16* xg; int ld_xg;
@@ -751,7 +775,10 @@ struct EmbedParams {
 PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
   // thread t owns columns [32t, 32t+32) (d <= 4096 per pass); 4 threads per
   // 128-column sum-of-squares slot.  All loads are issued before any use.
-  const int tok = p.step->tokens[r];
+  // (a device-resident window is not validated by the host: an out-of-range
+  // id reads row 0 here and the argmax phase reports it, rows = -1)
+  const int tok0 = p.step->tokens[r];
+  const int tok = (tok0 >= 0 && tok0 < p.vocab) ? tok0 : 0;
   const __nv_bfloat16* src = p.embed + (size_t)tok * p.d;
   for (int c0 = 0; c0 < p.d; c0 += 128 * 32) {
     const int col = c0 + tid * 32;
@@ -769,21 +796,26 @@ PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
         const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&xr[k]);
         const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gr[k]);
         float xf[8];
-        uint4 og;
-        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&og);
+        uint32_t oh[4], ol[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float2 xv = __bfloat1622float2(xb[q]);
           const float2 gv = __bfloat1622float2(gb[q]);
           xf[2 * q] = xv.x;
           xf[2 * q + 1] = xv.y;
-          ob[q] = __floats2bfloat162_rn(xv.x * gv.x, xv.y * gv.y);
+          __nv_bfloat16 h0, l0, h1, l1;
+          split_bf16(xv.x * gv.x, h0, l0);
+          split_bf16(xv.y * gv.y, h1, l1);
+          oh[q] = pack2(h0, h1);
+          ol[q] = pack2(l0, l1);
           sq += xv.x * xv.x + xv.y * xv.y;
         }
         float4* xd = reinterpret_cast<float4*>(p.x + (size_t)r * p.ld_x + col + 8 * k);
         xd[0] = make_float4(xf[0], xf[1], xf[2], xf[3]);
         xd[1] = make_float4(xf[4], xf[5], xf[6], xf[7]);
-        *reinterpret_cast<uint4*>(p.xg + (size_t)r * p.ld_xg + col + 8 * k) = og;
+        *reinterpret_cast<uint4*>(p.xg + (size_t)r * p.ld_xg + col + 8 * k) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+        *reinterpret_cast<uint4*>(p.xg + (size_t)(r + kMaxRows) * p.ld_xg + col + 8 * k) =
+            make_uint4(ol[0], ol[1], ol[2], ol[3]);
       }
     }
     sq += __shfl_xor_sync(0xffffffffu, sq, 1);
@@ -829,9 +861,13 @@ PS_DEV void tp_reduce_unit(const TpParams& p, int r, int t, int lane) {
   *reinterpret_cast<float4*>(p.x + (size_t)r * p.ld_x + f) = xn;
   const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(p.gain + f);
   const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
-  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(p.xg + (size_t)r * p.ld_xg + f);
-  o2[0] = __floats2bfloat162_rn(xn.x * ga.x, xn.y * ga.y);
-  o2[1] = __floats2bfloat162_rn(xn.z * gb.x, xn.w * gb.y);
+  __nv_bfloat16 h[4], l[4];
+  split_bf16(xn.x * ga.x, h[0], l[0]);
+  split_bf16(xn.y * ga.y, h[1], l[1]);
+  split_bf16(xn.z * gb.x, h[2], l[2]);
+  split_bf16(xn.w * gb.y, h[3], l[3]);
+  *reinterpret_cast<uint2*>(p.xg + (size_t)r * p.ld_xg + f) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
+  *reinterpret_cast<uint2*>(p.xg + (size_t)(r + kMaxRows) * p.ld_xg + f) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
   float sq = xn.x * xn.x + xn.y * xn.y + xn.z * xn.z + xn.w * xn.w;
   sq = warp_sum(sq);
   if (lane == 0) p.ss_out[(size_t)r * p.ss_out_ld + t] = sq;
@@ -863,8 +899,9 @@ struct AttnParams {
 };
 
 constexpr int kAttnPad = 8;        // smem row padding (bf16 elements): conflict-free ldmatrix
-// smem for NW warps: Q [NW*16][HD+8] + K,V [64][HD+8] bf16 + scratch
-constexpr int attn_smem_bytes(int nw) { return (nw * 16 + 2 * kAttnChunk) * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64; }
+// smem: K_hi, K_lo, V_hi, V_lo chunks [64][HD+8] bf16 + combine scratch (the
+// query fragments live in registers, built from the fp32 q directly)
+constexpr int attn_smem_bytes(int /*nw*/) { return kKvPlanes * kAttnChunk * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64; }
 constexpr int kAttnSmem = attn_smem_bytes(8);
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -886,13 +923,18 @@ PS_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// Split a pair of fp32 values into hi / lo packed bf16x2 registers.
+PS_DEV void split_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat16 h0, l0, h1, l1;
+  split_bf16(x0, h0, l0);
+  split_bf16(x1, h1, l1);
+  hi = pack2(h0, h1);
+  lo = pack2(l0, l1);
+}
 
-// NW warps (16 query rows each) of one CTA run the work items
-// item = cta, cta + ncta, ...; `bar` is the named barrier id for the NW*32
-// participating threads (tid in [0, NW*32)).
-// Issue (cp.async, one commit group) the K/V chunk of this CTA's first work
-// item if it lies wholly in the context (positions < pos0: not rewritten by the
-// coming QKV phase).  Returns the prefetched item id, or -1.
+// Issue (cp.async, one commit group) the K/V chunk (all four planes) of this
+// CTA's first work item if it lies wholly in the context (positions < pos0:
+// not rewritten by the coming QKV phase).  Returns the prefetched item id, or -1.
 template <int HD, int NW>
 PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* attn_smem, int tid, int cta) {
   constexpr int kRB = NW * 16, NT = NW * 32, LD = HD + kAttnPad, VPR = HD / 8;
@@ -905,35 +947,34 @@ PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* attn_smem, int tid, in
   const int c = cta % nchunks, kh = cta / (nchunks * n_rb);
   const int k0 = c * kAttnChunk;
   if (k0 + kAttnChunk > pos0) return -1;
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(attn_smem) + kRB * LD;
-  __nv_bfloat16* sV = sK + kAttnChunk * LD;
+  __nv_bfloat16* sKV = reinterpret_cast<__nv_bfloat16*>(attn_smem);
   const long long page = p.page_table[k0 / p.page_size];
   const int slot0 = k0 % p.page_size;
-  const __nv_bfloat16* Kp = p.kv + (size_t)page * p.page_stride +
-                            ((size_t)((p.layer * 2 + 0) * p.hkv + kh) * p.page_size + slot0) * HD;
-  const __nv_bfloat16* Vp = p.kv + (size_t)page * p.page_stride +
-                            ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
-  for (int i = tid; i < kAttnChunk * VPR; i += NT) {
-    const int row = i / VPR, cv = i % VPR;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sK + row * LD + cv * 8)),
-                 "l"(Kp + (size_t)row * HD + cv * 8) : "memory");
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sV + row * LD + cv * 8)),
-                 "l"(Vp + (size_t)row * HD + cv * 8) : "memory");
+  for (int i = tid; i < kKvPlanes * kAttnChunk * VPR; i += NT) {
+    const int pl = i / (kAttnChunk * VPR), row = (i / VPR) % kAttnChunk, cv = i % VPR;
+    const __nv_bfloat16* src = p.kv + (size_t)page * p.page_stride +
+                               ((size_t)((p.layer * kKvPlanes + pl) * p.hkv + kh) * p.page_size + slot0 + row) * HD + cv * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sKV + (pl * kAttnChunk + row) * LD + cv * 8)),
+                 "l"(src) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   return cta;
 }
 
+// S = Q K^T and O = P V with split-bf16 operands on mma.sync m16n8k16:
+// (q_hi + q_lo)(k_hi + k_lo)^T ~ q_hi k_hi + q_lo k_hi + q_hi k_lo (the
+// dropped lo*lo term is ~2^-16 relative), likewise P V.
 template <int HD, int NW, bool kInlineCombine = true>
 PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, int ncta, int bar,
                      int pref_item = -1) {
   constexpr int kRB = NW * 16;                          // query rows per block
   constexpr int NT = NW * 32;
   constexpr int LD = HD + kAttnPad;                     // smem row stride (elements)
-  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sK = sQ + kRB * LD;
-  __nv_bfloat16* sV = sK + kAttnChunk * LD;
-  float* sM = reinterpret_cast<float*>(sV + kAttnChunk * LD);   // combine scratch [64]
+  __nv_bfloat16* sKh = reinterpret_cast<__nv_bfloat16*>(attn_smem);
+  __nv_bfloat16* sKl = sKh + kAttnChunk * LD;
+  __nv_bfloat16* sVh = sKl + kAttnChunk * LD;
+  __nv_bfloat16* sVl = sVh + kAttnChunk * LD;
+  float* sM = reinterpret_cast<float*>(sVl + kAttnChunk * LD);   // combine scratch [64]
   int& s_last = *reinterpret_cast<int*>(sM + 3 * 64);
   const StepIn* st = p.step;
   const int R = st->R, pos0 = st->pos0;
@@ -952,78 +993,75 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     const int mrows = min(kRB, rows - m0);
     const int k0 = c * kAttnChunk;
     const int nk = min(kAttnChunk, n_keys - k0);
-    const bool stamp = p.dbg != nullptr && tid == 0 && item == cta;
-    if (stamp) p.dbg[cta * 8 + 0] = globaltimer();
-    // ---- stage K/V chunk (one page run of 64 positions) and the Q rows (bf16, pre-scaled)
-    // Q loads first: they do not depend on the page-table lookup, so their
-    // round trip overlaps it instead of following it.
+    const bool stamp = tid == 0 && item == cta;
+    if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
     const int nwarps_used = (mrows + 15) / 16;
-    constexpr int QIT = (NW * 16 * (HD / 4) + NT - 1) / NT;   // float4 per thread
-    float4 qv[QIT];
-#pragma unroll
-    for (int k = 0; k < QIT; ++k) {
-      const int i = tid + k * NT;
-      const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
-      qv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < mrows) {
-        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-        qv[k] = *reinterpret_cast<const float4*>(p.q + (size_t)r * p.ld_q + h * HD + d4);
-      }
-    }
+    // ---- K/V chunk, four planes: cp.async (16 B, zero-fill past nk) -- every
+    // copy in flight at once (skipped when prefetched during the QKV phase)
     const long long page = p.page_table[k0 / p.page_size];
     const int slot0 = k0 % p.page_size;
-    const __nv_bfloat16* Kp = p.kv + (size_t)page * p.page_stride +
-                              ((size_t)((p.layer * 2 + 0) * p.hkv + kh) * p.page_size + slot0) * HD;
-    const __nv_bfloat16* Vp = p.kv + (size_t)page * p.page_stride +
-                              ((size_t)((p.layer * 2 + 1) * p.hkv + kh) * p.page_size + slot0) * HD;
     constexpr int VPR = HD / 8;                          // 16-byte vectors per row
-    // K/V chunk: cp.async (16 B, zero-fill past nk) -- every copy in flight at once
-    // (skipped when it was prefetched during the QKV phase)
-    for (int i = (item == pref_item) ? kAttnChunk * VPR : tid; i < kAttnChunk * VPR; i += NT) {
-      const int row = i / VPR, cv = i % VPR;
+    for (int i = (item == pref_item) ? kKvPlanes * kAttnChunk * VPR : tid; i < kKvPlanes * kAttnChunk * VPR; i += NT) {
+      const int pl = i / (kAttnChunk * VPR), row = (i / VPR) % kAttnChunk, cv = i % VPR;
       const int ok = row < nk ? 16 : 0;
-      const __nv_bfloat16* ksrc = Kp + (size_t)(row < nk ? row : 0) * HD + cv * 8;
-      const __nv_bfloat16* vsrc = Vp + (size_t)(row < nk ? row : 0) * HD + cv * 8;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sK + row * LD + cv * 8)),
-                   "l"(ksrc), "r"(ok) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sV + row * LD + cv * 8)),
-                   "l"(vsrc), "r"(ok) : "memory");
+      const __nv_bfloat16* src = p.kv + (size_t)page * p.page_stride +
+                                 ((size_t)((p.layer * kKvPlanes + pl) * p.hkv + kh) * p.page_size + slot0 +
+                                  (row < nk ? row : 0)) * HD + cv * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sKh + (pl * kAttnChunk + row) * LD + cv * 8)),
+                   "l"(src), "r"(ok) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    // Q rows (fp32 -> bf16, pre-scaled), loaded above
+    // ---- this warp's query fragments (A operand of m16n8k16, rows lane/4 and
+    // lane/4 + 8, dims 2(lane%4) + {0,1} and + 8 of each 16-wide k step),
+    // loaded straight from the fp32 q, pre-scaled, split into hi / lo
+    uint32_t qh[HD / 16][4], ql[HD / 16][4];
     {
+      int qoff[2];
 #pragma unroll
-      for (int k = 0; k < QIT; ++k) {
-        const int i = tid + k * NT;
-        const int m = i / (HD / 4), d4 = (i % (HD / 4)) * 4;
-        if (m < nwarps_used * 16) {
-          uint2 pk = make_uint2(pack_bf16(qv[k].x * p.scale_log2, qv[k].y * p.scale_log2),
-                                pack_bf16(qv[k].z * p.scale_log2, qv[k].w * p.scale_log2));
-          *reinterpret_cast<uint2*>(sQ + m * LD + d4) = pk;
-        }
+      for (int hr = 0; hr < 2; ++hr) {
+        const int m = warp * 16 + (lane >> 2) + hr * 8;
+        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+        qoff[hr] = m < mrows ? r * p.ld_q + h * HD : -1;
       }
+      float2 qv[HD / 16][4];
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int o = qoff[j & 1];
+          const int d = kk * 16 + (lane & 3) * 2 + (j >> 1) * 8;
+          qv[kk][j] = (o >= 0 && warp < nwarps_used) ? *reinterpret_cast<const float2*>(p.q + o + d)
+                                                     : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          split_pack(qv[kk][j].x * p.scale_log2, qv[kk][j].y * p.scale_log2, qh[kk][j], ql[kk][j]);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     named_bar(bar, NT);
-    if (stamp) p.dbg[cta * 8 + 1] = globaltimer();
+    if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 1);
     if (warp < nwarps_used) {
       // ---- S = Q K^T for this warp's 16 rows x 64 keys
       float sacc[8][4];
 #pragma unroll
       for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
-      const uint32_t qbase = smem_u32(sQ + (warp * 16 + (lane % 16)) * LD + (lane / 16) * 8);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        uint32_t a[4];
-        ldsm_x4(qbase + kk * 32, a[0], a[1], a[2], a[3]);
 #pragma unroll
         for (int jp = 0; jp < 4; ++jp) {   // pairs of 8-key n-tiles
           const int krow = jp * 16 + (lane & 7) + ((lane >> 4) << 3);
           const int kcol = kk * 16 + ((lane >> 3) & 1) * 8;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(smem_u32(sK + krow * LD + kcol), b0, b1, b2, b3);
-          mma16816(sacc[2 * jp], a, b0, b1);
-          mma16816(sacc[2 * jp + 1], a, b2, b3);
+          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+          ldsm_x4(smem_u32(sKh + krow * LD + kcol), b0, b1, b2, b3);
+          ldsm_x4(smem_u32(sKl + krow * LD + kcol), c0, c1, c2, c3);
+          mma16816(sacc[2 * jp], qh[kk], b0, b1);
+          mma16816(sacc[2 * jp + 1], qh[kk], b2, b3);
+          mma16816(sacc[2 * jp], ql[kk], b0, b1);
+          mma16816(sacc[2 * jp + 1], ql[kk], b2, b3);
+          mma16816(sacc[2 * jp], qh[kk], c0, c1);
+          mma16816(sacc[2 * jp + 1], qh[kk], c2, c3);
         }
       }
       // ---- causal / length mask and chunk-local softmax (rows lane/4 and lane/4+8)
@@ -1045,7 +1083,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
         mrow[hr] = fmaxf(mrow[hr], __shfl_xor_sync(0xffffffffu, mrow[hr], 2));
       }
       float lrow[2] = {0.f, 0.f};
-      uint32_t pa[4][4];                 // P as A fragments, 4 k-blocks of 16 keys
+      uint32_t pah[4][4], pal[4][4];      // P as A fragments (hi / lo), 4 k-blocks of 16 keys
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float pv[4];
@@ -1056,15 +1094,15 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
           lrow[hr] += pv[q4];
         }
         const int kb = j >> 1, half2 = j & 1;
-        pa[kb][half2 * 2 + 0] = pack_bf16(pv[0], pv[1]);
-        pa[kb][half2 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+        split_pack(pv[0], pv[1], pah[kb][half2 * 2 + 0], pal[kb][half2 * 2 + 0]);
+        split_pack(pv[2], pv[3], pah[kb][half2 * 2 + 1], pal[kb][half2 * 2 + 1]);
       }
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
         lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 1);
         lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 2);
       }
-      if (stamp) p.dbg[cta * 8 + 2] = globaltimer();
+      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 2);
       // ---- O = P V  (16 rows x HD)
       float oacc[HD / 8][4];
 #pragma unroll
@@ -1075,13 +1113,18 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
         for (int np = 0; np < HD / 16; ++np) {
           const int vrow = kb * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
           const int vcol = np * 16 + (lane >> 4) * 8;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(smem_u32(sV + vrow * LD + vcol), b0, b1, b2, b3);
-          mma16816(oacc[2 * np], pa[kb], b0, b1);
-          mma16816(oacc[2 * np + 1], pa[kb], b2, b3);
+          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+          ldsm_x4_t(smem_u32(sVh + vrow * LD + vcol), b0, b1, b2, b3);
+          ldsm_x4_t(smem_u32(sVl + vrow * LD + vcol), c0, c1, c2, c3);
+          mma16816(oacc[2 * np], pah[kb], b0, b1);
+          mma16816(oacc[2 * np + 1], pah[kb], b2, b3);
+          mma16816(oacc[2 * np], pal[kb], b0, b1);
+          mma16816(oacc[2 * np + 1], pal[kb], b2, b3);
+          mma16816(oacc[2 * np], pah[kb], c0, c1);
+          mma16816(oacc[2 * np + 1], pah[kb], c2, c3);
         }
       }
-      if (stamp) p.dbg[cta * 8 + 3] = globaltimer();
+      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 3);
       // ---- chunk partials -> workspace
       const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kRB);
 #pragma unroll
@@ -1097,7 +1140,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
     }
     if constexpr (!kInlineCombine) {    // partials only; attn_combine runs after a grid barrier
       named_bar(bar, NT);
-      if (stamp) p.dbg[cta * 8 + 4] = globaltimer();
+      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
       continue;
     }
     fence_acq_rel_gpu();
@@ -1143,7 +1186,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
         const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
         __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
 #pragma unroll
-        for (int t = 0; t < DPL; ++t) dst[t] = __float2bfloat16(acc[t] * invL);
+        for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kMaxRows * p.ld_out]);
       }
       if (tid == 0) p.counters[kh * p.max_rb + rb] = 0u;
     }
@@ -1202,7 +1245,7 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
     const int r = mg / g, h = kh * g + mg % g;
     __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
 #pragma unroll
-    for (int t = 0; t < DPL; ++t) dst[t] = __float2bfloat16(acc[t] * invL);
+    for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kMaxRows * p.ld_out]);
   }
 }
 
@@ -1221,6 +1264,7 @@ struct ArgmaxParams {
   StepOut* out;            // device
   StepOut* mirror;         // mapped pinned host memory (zero-copy), may be null
   const SynthParams* syn;  // may be null
+  int vocab;               // full vocabulary (row-token range check)
   // tensor parallel (tp_n > 1): every rank's per-row keys, two parity slots
   // [2][kMaxRows] each (slot = gen_head & 1); amax is this rank's own block
   int tp_n;
@@ -1272,35 +1316,47 @@ PS_DEV void argmax_run(const ArgmaxParams& p, int tid, int* s_pred, int bar) {
     }
   }
   named_bar(bar, NT);
-  if (tid == 0) {
+  if (tid < 32) {
+    // one warp: lane j holds prediction row r0 + j (w <= 31 < 32 lanes)
+    const int lane = tid;
     const int w = st->w;
     const int r0 = st->row0;             // prediction rows r0 .. r0 + w
+    const bool live = lane <= w;
+    const int d = lane < w ? st->tokens[r0 + 1 + lane] : -1;   // draft d_lane
+    int pred = live ? s_pred[r0 + lane] : -1;
     if ((st->flags & kFlagSynth) && p.syn != nullptr && p.syn->len_S > 0 && st->syn_onpath) {
-      // prediction row j's context is x ++ d[0:j]; on-path while the drafts follow S
-      bool on = true;
-      for (int j = 0; j <= w && on; ++j) {
-        const int pj = st->syn_p0 + j;
-        if (pj >= p.syn->len_S) break;
-        s_pred[r0 + j] = synth_token(p.syn, pj);
-        if (j < w) on = (st->tokens[r0 + 1 + j] == p.syn->S[pj]);
-      }
+      // prediction row j's context is x ++ d[0:j]: on-path while d_t == S[p0+t]
+      // for all t < j, i.e. for j <= the first draft that leaves S
+      const int pj = st->syn_p0 + lane;
+      const unsigned off = __ballot_sync(0xffffffffu, lane < w && (pj >= p.syn->len_S || d != p.syn->S[pj]));
+      const int first_off = off ? __ffs(off) - 1 : 32;
+      if (live && lane <= first_off && pj < p.syn->len_S) pred = synth_token(p.syn, pj);
     }
-    int a = 0;
-    while (a < w && s_pred[r0 + a] == st->tokens[r0 + 1 + a]) ++a;
-    StepOut o;
-    o.a = a;
-    o.next = s_pred[r0 + a];
-    o.R = R;
-    o.pad = 0;
-    for (int j = 0; j < kMaxRows; ++j) o.pred[j] = j <= w ? s_pred[r0 + j] : -1;
-    *p.out = o;
-    if (p.mirror != nullptr) {
-      volatile int* m = reinterpret_cast<volatile int*>(p.mirror);
-      for (int j = 0; j < kMaxRows; ++j) m[4 + j] = o.pred[j];
-      m[0] = o.a;
-      m[1] = o.next;
-      m[2] = o.R;
-      __threadfence_system();
+    // a = longest prefix with pred_j == d_j: first mismatching lane (ballot + ffs)
+    const unsigned miss = __ballot_sync(0xffffffffu, lane < w && pred != d);
+    const int a = miss ? __ffs(miss) - 1 : w;
+    const int next = __shfl_sync(0xffffffffu, pred, a);
+    // every row token must be a vocabulary id (device windows are not host-checked)
+    const bool bad_tok = lane < R && (st->tokens[lane] < 0 || st->tokens[lane] >= p.vocab);
+    const bool bad = __any_sync(0xffffffffu, bad_tok);
+    p.out->pred[lane] = live ? pred : -1;
+    if (p.mirror != nullptr) reinterpret_cast<volatile int*>(p.mirror)[4 + lane] = live ? pred : -1;
+    if (lane == 0) {
+      // KV now valid for positions < n + a, n - 1 = pos0 + row0 (the pending row)
+      const int kv_len = st->pos0 + r0 + 1 + a;
+      p.out->a = a;
+      p.out->next = next;
+      p.out->R = bad ? -1 : R;
+      p.out->kv_len = kv_len;
+      if (p.mirror != nullptr) {
+        volatile int* m = reinterpret_cast<volatile int*>(p.mirror);
+        m[0] = a;
+        m[1] = next;
+        m[3] = kv_len;
+        __threadfence_system();
+        m[2] = bad ? -1 : R;             // written last: the host polls it
+        __threadfence_system();
+      }
     }
   }
 }

@@ -30,13 +30,8 @@ struct MegaPhase {
   int kind;
   int gu;                          // GEMM: gate/up (two 64-row boxes per A tile)
   int head;                        // 1: runs only in forwards with lm_head (counter target gen_head)
-  int tctr;                        // GEMM: base index of this phase's per-tile completion counters
-  int dep_w;                       // GEMM: X columns per producing tile of the previous (GEMM) phase;
-                                   // 0 = the X operand waits for the whole previous phase
   int xpub;                        // tensor parallel: peers read this phase's output (publish at sys scope)
   int xwait;                       // tensor parallel: also wait for every peer's previous phase
-  int inline_comb;                 // ATTN/ACOMB: 1 the last CTA of each (kv head, row block) combines (no
-                                   // ACOMB phase); 2 the same when R*g <= kInlineCombRows, else ACOMB
   const CUtensorMap* mA0;          // global-memory tensor maps (64-byte aligned)
   const CUtensorMap* mA1;
   const CUtensorMap* mA2;
@@ -53,31 +48,23 @@ struct MegaParams {
   int n_ph;
   const StepIn* step;
   unsigned* done;                  // [n_ph] cumulative CTA completion counters
-  unsigned long long* dbg;         // optional [G][n_ph][8] %globaltimer stamps
-  unsigned* tile_done;             // cumulative per-tile completion counters (all GEMM phases)
+  unsigned long long* dbg;         // PS_TRACE builds: [G][n_ph][8] %globaltimer stamps
   int tp_n;                        // tensor-parallel group size (1: none)
   const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
-  unsigned spin_cap;               // phase-wait poll back-off cap (ns)
-  int tile_pub;                    // publish per-tile completion (read only by the per-tile dataflow X gate)
 };
 
-// Up to this many query rows per KV head the last-arriver combine inside the
-// attention phase is cheaper than a separate combine phase (measured: 1B draft
-// step R=1 -2.5%; 8B verify R=5, 20 rows: +6%).
-constexpr int kInlineCombRows = 8;
-PS_DEV bool inline_combine(const MegaPhase& Q, int R) {
-  return Q.inline_comb == 1 || (Q.inline_comb == 2 && R * (Q.a.H / Q.a.hkv) <= kInlineCombRows);
-}
+// Phase-wait poll back-off cap (ns; measured: 1024 +5-8%, 256 / 64 / 32 within noise).
+constexpr unsigned kSpinCapNs = 64;
 
 constexpr int kMegaThreads = 224;   // 7 warps: W producer, MMA, 4 epilogue, X loader
 // ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
-template <int RP> constexpr int mega_stages() { return RP == 16 ? 8 : 7; }
+template <int RP> constexpr int mega_stages() { return RP == 16 ? 7 : 5; }
 
 template <int RP, int STAGES = mega_stages<RP>()>
 struct MegaSmem {
   static constexpr int kMegaStages = STAGES;
   static constexpr int kABytes = 128 * 64 * 2;
-  static constexpr int kXBytes = RP * 64 * 2;
+  static constexpr int kXBytes = 2 * RP * 64 * 2;   // split-bf16 activation tiles: hi, then lo
   static constexpr int kOffX = kMegaStages * kABytes;
   static constexpr int kOffScratch = kOffX + kMegaStages * kXBytes;
   static constexpr int kOffRed = kOffScratch + 128 * (RP + 1) * 4;
@@ -212,54 +199,25 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     }
   } else if (warp == 6) {
     // ================= X loader: the activation tile of each unit, issued once
-    // the producing tile of the previous phase (or the whole previous phase)
-    // has been published.  Dataflow instead of a grid barrier: most consumer
-    // units start while the previous phase's slowest tiles are still finishing.
+    // the whole previous phase has been published (grid-wide cumulative
+    // counter: relaxed polls, one acquire, then a proxy fence so this CTA's
+    // TMA (async proxy) sees the other CTAs' generic-proxy epilogue stores).
     if (lane == 0) {
       uint32_t it = 0;
       int cur_ph = -1;
-      bool phase_ready = false;            // whole previous phase published
-      unsigned long long rmask[4];         // per-tile readiness cache (<= 256 producer tiles)
       for_units([&](int ph, const MegaPhase& Q, long long, int, int kb) {
-        const MegaPhase& D = P.ph[ph - 1];
-        const unsigned* dphase = P.done + (ph - 1);
-        const unsigned tphase = D.head ? tgt_head : tgt_body;
         if (ph != cur_ph) {
           tma_prefetch_desc(Q.mX);
           cur_ph = ph;
-          phase_ready = poll_ready(dphase, tphase);
-          rmask[0] = rmask[1] = rmask[2] = rmask[3] = 0ull;
-        }
-        if (!phase_ready) {
-          if (Q.dep_w > 0 && D.g.n_tiles <= 256) {
-            const int pt = (kb * 64) / Q.dep_w;
-            if (!((rmask[pt >> 6] >> (pt & 63)) & 1ull)) {
-              // one round trip for a batch of 8 producer tiles
-              const unsigned ttile = D.head ? (unsigned)P.step->gen_head : (unsigned)P.step->gen;
-              const unsigned* base = P.tile_done + D.tctr;
-              unsigned vals[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) vals[q] = (pt + q < D.g.n_tiles) ? ld_relaxed_u32(base + pt + q) : 0u;
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                if (pt + q < D.g.n_tiles && (int)(vals[q] - ttile) >= 0) rmask[(pt + q) >> 6] |= 1ull << ((pt + q) & 63);
-              if (!((rmask[pt >> 6] >> (pt & 63)) & 1ull)) {
-                spin_until(base + pt, ttile);
-                rmask[pt >> 6] |= 1ull << (pt & 63);
-              }
-              fence_acquire_gpu();
-              fence_proxy_async_global();
-            }
-          } else {
-            spin_until(dphase, tphase, P.spin_cap);
-            fence_proxy_async_global();
-            phase_ready = true;
-          }
-          if (P.dbg != nullptr && kb == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 2] = globaltimer();
+          spin_until(P.done + (ph - 1), P.ph[ph - 1].head ? tgt_head : tgt_body, kSpinCapNs);
+          fence_proxy_async_global();
+          PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 2);
         }
         const int slot = it % kMegaStages;
         mbar_wait(&empty[slot], ((it / kMegaStages) & 1) ^ 1);
+        // hi rows [0, RP) and lo rows [kMaxRows, kMaxRows + RP) of the operand
         tma_load_2d(sX + slot * L::kXBytes, Q.mX, &full[slot], kb * 64, 0, kEvictLast);
+        tma_load_2d(sX + slot * L::kXBytes + RP * 128, Q.mX, &full[slot], kb * 64, kMaxRows, kEvictLast);
         ++it;
       });
     }
@@ -283,10 +241,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
           const long long seg_end = min(ue, (long long)(t + 1) * kbt);
           const int acc = nacc & 1;
           mbar_wait(&tempty[acc], ((nacc >> 1) & 1) ^ 1);
-          if (first && P.dbg != nullptr) {
+#if PS_TRACE
+          if (first) {
             mbar_wait(&full[it % kMegaStages], (it / kMegaStages) & 1);
-            P.dbg[((size_t)c * P.n_ph + ph) * 8 + 3] = globaltimer();
+            PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 3);
           }
+#endif
           first = false;
           tc_fence_after();
           const uint32_t dcol = tmem + acc * RP;
@@ -297,15 +257,17 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             const uint32_t a0 = smem_u32(sA + slot * L::kABytes);
             const uint32_t x0 = smem_u32(sX + slot * L::kXBytes);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k) {   // W·x_hi + W·x_lo (split-bf16 operand)
               mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
                        (u != seg_begin || k > 0) ? 1u : 0u);
+              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + RP * 128 + 32 * k), kIdesc, 1u);
+            }
             mma_commit(&empty[slot]);
           }
           mma_commit(&tfull[acc]);
           ++nacc;
         }
-        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 4] = globaltimer();
+        PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 4);
       }
     }
   } else {
@@ -347,33 +309,22 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         sph->em.step = sstep;
         sph->am.step = sstep;
       }
-      // (A combine phase whose work the attention phase already did inline is
-      // a pass-through: each CTA publishes it as soon as its own attention
-      // items, combines included, are done.)
-      const bool skip = sph->kind == PH_ACOMB && inline_combine(*sph, R);
-      const bool need_prev = ph > 0 && !skip && !(sph->kind == PH_GEMM && sph->g.ss_in == nullptr &&
-                                                  sph->g.mode != EPI_STORE && sph->dep_w > 0);
-      if (need_prev && et == 0) {
-        spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body, P.spin_cap);
+      if (ph > 0 && et == 0) {
+        spin_until(P.done + (ph - 1), prev_head ? tgt_head : tgt_body, kSpinCapNs);
         if (sph->xwait)           // tensor parallel: every peer's partial is published
           for (int q = 0; q < P.tp_n; ++q) spin_until_sys(P.peer_done[q] + (ph - 1), prev_head ? tgt_head : tgt_body);
       }
       named_bar(1, 128);
-      if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 0] = globaltimer();
+      if (et == 0) PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 0);
       const MegaPhase& Q = *sph;
       const int kind = Q.kind;
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (inline_combine(Q, R)) {
-          if (Q.a.hd == 128) attn_run<128, 4, true>(Q.a, attn_smem, et, c, G, 1, pref_item);
-          else attn_run<64, 4, true>(Q.a, attn_smem, et, c, G, 1, pref_item);
-        } else {
-          if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
-          else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
-        }
+        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
+        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
         pref_item = -1;
-      } else if (kind == PH_ACOMB && !skip) {
+      } else if (kind == PH_ACOMB) {
         if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
         else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
       } else if (kind == PH_TPRED) {
@@ -404,9 +355,9 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             const int acc = nacc & 1;
             mbar_wait(&tfull[acc], (nacc >> 1) & 1);
             tc_fence_after();
-            if (P.dbg != nullptr && et == 0) {
-              if (u == ub) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 5] = globaltimer();
-              P.dbg[((size_t)c * P.n_ph + ph) * 8 + 6] = globaltimer();
+            if (et == 0) {
+              if (u == ub) PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 5);
+              PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 6);
             }
             float v[RP];
             load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * RP, v);
@@ -416,18 +367,11 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             u = seg_end;
             // (the attention area stages stream-K partials, except in QKV phases:
             // the next attention phase's K/V chunk is prefetched into it then)
-            const bool fin = epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R,
-                                             pos0, scratch, red, rstd, kvrow, flag,
-                                             gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
-                                             L::kAttnBytes / 16);
-            if (fin && P.tile_pub) {                    // publish tile t of this phase
-              named_bar(1, 128);
-              if (et == 0) {
-                fence_proxy_async_global();
-                red_release_add(P.tile_done + Q.tctr + t, 1u);
-              }
-            }
-            if (P.dbg != nullptr && et == 0) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 7] = globaltimer();
+            epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch,
+                                  red, rstd, kvrow, flag,
+                                  gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
+                                  L::kAttnBytes / 16);
+            if (et == 0) PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 7);
           }
         }
       }
@@ -438,7 +382,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         fence_proxy_async_global();
         if (Q.xpub) red_release_add_sys(P.done + ph, 1u);
         else red_release_add(P.done + ph, 1u);
-        if (P.dbg != nullptr) P.dbg[((size_t)c * P.n_ph + ph) * 8 + 1] = globaltimer();
+        PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 1);
       }
     }
   }

@@ -17,16 +17,13 @@
 #include <vector>
 
 #include "../../include/pipespec.h"
-#include "../../include/pipespec_test.h"
-#include "ps_mega.cuh"
-
-using namespace ps;
+#include "ps_host.cuh"
 
 // ============================================================================ errors
 static thread_local std::string g_err;
-static std::atomic<long long> g_launches{0};
+std::atomic<long long> g_launches{0};
 
-static ps_status fail(ps_status code, const char* fmt, ...) {
+ps_status fail(ps_status code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -34,159 +31,6 @@ static ps_status fail(ps_status code, const char* fmt, ...) {
   va_end(ap);
   g_err = buf;
   return code;
-}
-
-#define CU_TRY(expr)                                                                       \
-  do {                                                                                     \
-    cudaError_t e_ = (expr);                                                               \
-    if (e_ != cudaSuccess)                                                                 \
-      return fail(PS_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-
-// ============================================================================ TMA maps
-static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-
-static ps_status get_encoder() {
-  if (g_encode) return PS_OK;
-  cudaDriverEntryPointQueryResult q;
-  void* fn = nullptr;
-  CU_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-  if (!fn || q != cudaDriverEntryPointSuccess) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled not found");
-  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-  return PS_OK;
-}
-
-// Row-major bf16 [rows, cols] matrix; box = box_rows x 64 columns, SWIZZLE_128B
-// (128-byte rows, the canonical K-major UMMA layout).
-static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  if (((uintptr_t)ptr & 15) || (cols * 2) % 16) return fail(PS_E_INVALID, "tensor not 16-byte aligned");
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return PS_OK;
-}
-
-// ============================================================================ GEMM launch
-constexpr int kStages = 4;   // x (16 KB weights + RP*128 B activations): 2 CTAs/SM
-static int g_num_sms = 0;
-static int g_test_flags = 0;   // test hooks only: bit0 = launch without PDL
-
-template <int RP, bool GU>
-static ps_status gemm_setup_attr() {
-  static bool done = false;
-  if (done) return PS_OK;
-  CU_TRY(cudaFuncSetAttribute(gemm_kernel<RP, kStages, GU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<RP, kStages, GU>::kBytes));
-  done = true;
-  return PS_OK;
-}
-
-struct GemmShape {
-  int n_tiles, kb_total, grid, maxseg;
-};
-
-// Stream-K partition of one GEMM over the persistent grid.  align_pct > 0:
-// if k = floor(#SMs / n_tiles) CTAs per tile keep >= align_pct% of the SMs
-// busy, use n_tiles * k CTAs: every CTA then owns one tile-aligned segment
-// and each tile exactly k partials.  Small models' phases are latency-bound,
-// where fewer partials per tile beat the lost SMs (1B draft step 0.940 ->
-// 0.919 ms at 60%); large models' are bandwidth-bound and keep >= 95% (8B:
-// QKV on 144 CTAs -0.25%; O / down on 128 CTAs would cost +1.4%).
-static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) {
-  GemmShape g;
-  g.n_tiles = n_tiles;
-  g.kb_total = K / 64;
-  long long U = (long long)n_tiles * g.kb_total;
-  g.grid = (int)std::min<long long>(num_sms, U);
-  if (align_pct > 0 && n_tiles <= num_sms) {
-    // sk_begin splits at kb_total*c/k: tile-aligned for any k (<= kb_total: no empty CTA ranges)
-    const int k = std::min(num_sms / n_tiles, g.kb_total);
-    if ((long long)n_tiles * k * 100 >= (long long)num_sms * align_pct) g.grid = n_tiles * k;
-  }
-  auto owner = [&](long long u) { return (int)(((u + 1) * g.grid - 1) / U); };
-  g.maxseg = 1;
-  for (int t = 0; t < n_tiles; ++t) {
-    int ns = owner((long long)t * g.kb_total + g.kb_total - 1) - owner((long long)t * g.kb_total) + 1;
-    g.maxseg = std::max(g.maxseg, ns);
-  }
-  return g;
-}
-
-static ps_status launch_gemm(int RP, bool GU, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& a2,
-                             const CUtensorMap& x, const GemmParams& p, int grid, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = (g_test_flags & 1) ? 0 : 1;
-  cudaError_t e;
-  if (RP == 16 && !GU) {
-    cfg.dynamicSmemBytes = GemmSmem<16, kStages, false>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, false>, a0, a1, a2, x, p);
-  } else if (RP == 16) {
-    cfg.dynamicSmemBytes = GemmSmem<16, kStages, true>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, true>, a0, a1, a2, x, p);
-  } else if (!GU) {
-    cfg.dynamicSmemBytes = GemmSmem<32, kStages, false>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, false>, a0, a1, a2, x, p);
-  } else {
-    cfg.dynamicSmemBytes = GemmSmem<32, kStages, true>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, true>, a0, a1, a2, x, p);
-  }
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
-  g_launches++;
-  return PS_OK;
-}
-
-template <typename K, typename P>
-static ps_status launch_simple(K kernel, dim3 grid, dim3 block, size_t smem, const P& params, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, params);
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-  g_launches++;
-  return PS_OK;
-}
-
-static ps_status init_device_globals(int device) {
-  CU_TRY(cudaSetDevice(device));
-  int major = 0, minor = 0;
-  CU_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
-  CU_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
-  if (major != 10 || minor != 0)
-    return fail(PS_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", device, major, minor);
-  CU_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device));
-  ps_status st;
-  if ((st = get_encoder()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<16, false>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<16, true>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<32, false>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<32, true>()) != PS_OK) return st;
-  CU_TRY(cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-  CU_TRY(cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-  CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
-  CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
-  CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 4>::kBytes));
-  CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
-  CU_TRY(cudaFuncSetAttribute(mega_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32, 4>::kBytes));
-  return PS_OK;
 }
 
 // ============================================================================ stage
@@ -215,6 +59,7 @@ struct ps_stage {
   int pages_total = 0;
   std::vector<int> page_of;     // logical page -> physical (-1 unmapped)
   std::vector<int> free_pages;  // stack
+  int n_mapped = 0;             // logical pages [0, n_mapped) are mapped
   int32_t* d_page_table = nullptr;
   int32_t* h_page_table = nullptr;   // pinned mirror
   // scratch (owned)
@@ -232,9 +77,7 @@ struct ps_stage {
   CUtensorMap* mega_maps[4] = {nullptr, nullptr, nullptr, nullptr};
   int mega_n[4] = {0, 0, 0, 0};
   unsigned* mega_done = nullptr;
-  unsigned* tile_done = nullptr;   // per-tile completion counters, GEMM phases of the megakernel
-  int n_tile_ctr = 0;
-  unsigned long long* mega_dbg = nullptr;
+  unsigned long long* mega_dbg = nullptr;   // PS_TRACE builds only: timeline stamps
   unsigned long long* epi_dbg = nullptr;
   unsigned long long* attn_dbg = nullptr;
   unsigned gen = 0, gen_head = 0;
@@ -249,6 +92,12 @@ struct ps_stage {
   uint8_t* peers[8] = {};
   bool peer_ipc[8] = {};
   bool tp_connected = false;
+  size_t ws_bytes = 0;
+  // asynchronous verify (ps_verify_async / ps_verify_wait)
+  bool inflight = false;
+  long long if_n = 0;                // len(O_i) when the pass was enqueued
+  int if_w = 0;
+  cudaEvent_t done_ev = nullptr;     // recorded after the in-flight pass
   StepOut* d_out = nullptr;
   StepOut* h_out = nullptr;          // mapped pinned mirror
   StepOut* h_out_dev = nullptr;      // its device alias
@@ -276,12 +125,29 @@ struct ps_stage {
 };
 
 static int bucket_rp(int b) { return b == 0 ? 16 : 32; }
+
+// Device-wide setup of a stage's device: the shared GEMM/attention attributes
+// plus the megakernel instantiations (per device, so every GPU of a process).
+static ps_status init_stage_device(int device) {
+  ps_status st;
+  if ((st = init_device_globals(device)) != PS_OK) return st;
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
+  return PS_OK;
+}
 static int bucket_of(int R) { return R <= 16 ? 0 : 1; }
+
+// Calls that change or use the stage are refused while an asynchronous pass
+// is in flight (ps_verify_async ... ps_verify_wait).
+#define PS_NOT_INFLIGHT(S) \
+  if ((S)->inflight) return fail(PS_E_INVALID, "a ps_verify_async pass is in flight (call ps_verify_wait)")
 
 extern "C" int64_t ps_kv_pool_bytes_tp(const ps_model_shape* s, int32_t max_seq, int32_t page_size, int32_t tp) {
   if (!s || page_size <= 0 || tp < 1 || s->n_kv_heads % tp) return -1;
   long long pages = (max_seq + page_size - 1) / page_size;
-  long long page_elems = (long long)s->n_layers * 2 * (s->n_kv_heads / tp) * page_size * s->head_dim;
+  // K_hi, K_lo, V_hi, V_lo planes (split-bf16 KV cache, ps_kernels.cuh)
+  long long page_elems = (long long)s->n_layers * kKvPlanes * (s->n_kv_heads / tp) * page_size * s->head_dim;
   return pages * page_elems * 2;
 }
 extern "C" int64_t ps_kv_pool_bytes(const ps_model_shape* s, int32_t max_seq, int32_t page_size) {
@@ -336,12 +202,12 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
   p.step = S->d_in;
   p.ws = S->ws;
   p.counters = S->counters;
-  p.ll = (g_test_flags & 4096) ? 0 : 1;
+  p.ll = 1;
   p.ll_tag = 1 + kind + 8 * l;     // per-kernel path; the megakernel re-tags by phase index
   switch (kind) {
     case K_EMBED: {
       P.kind = PH_EMBED;
-      P.em = EmbedParams{S->d_in, S->embed, d, sh.n_layers ? S->lw[PS_N_ATTN] : S->final_norm,
+      P.em = EmbedParams{S->d_in, S->embed, d, S->vocab_full, sh.n_layers ? S->lw[PS_N_ATTN] : S->final_norm,
                          S->x, d, S->xg, S->xg_ld, S->ss, S->ss_ld};
       return;
     }
@@ -369,7 +235,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       a.max_chunks = S->max_chunks; a.max_rb = S->max_rb;
       a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
       a.out = S->att; a.ld_out = hq;
-      a.dbg = (g_test_flags & 64) ? S->attn_dbg : nullptr;
+      a.dbg = S->attn_dbg;   // PS_TRACE builds only (null otherwise)
       return;
     }
     case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
@@ -428,7 +294,8 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
     }
     case K_ARGMAX: {  // argmax + compare + first-mismatch scan (a11)
       P.kind = PH_ARGMAX;
-      P.am = ArgmaxParams{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn, 0, {}};
+      P.am = ArgmaxParams{S->d_in, S->amax, S->lm_tiles, S->lm_tiles, S->d_out, S->h_out_dev, S->d_syn, S->vocab_full,
+                          0, {}};
       if (S->tp_size > 1) {
         P.am.amax = (unsigned long long*)(S->xch + S->off_keys);
         P.am.tp_n = S->tp_size;
@@ -514,16 +381,10 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
       add(kind, l);
       if (kind == K_ATTN) {
-        // chunk partials, then a separate combine phase.  (Test flags: 1024 the
-        // last-arriving CTA of each (kv head, row block) combines inline, no
-        // ACOMB phase: 1B R=1 -2.5%, 8B R=5 +6%; 2048 inline only for
-        // R*g <= 8 with ACOMB as a pass-through otherwise: no gain, the
-        // pass-through phase costs what the inline combine saves.)
-        ph.back().inline_comb = (g_test_flags & 1024) ? 1 : (g_test_flags & 2048) ? 2 : 0;
-        if (ph.back().inline_comb != 1) {
-          ph.push_back(ph.back());
-          ph.back().kind = PH_ACOMB;
-        }
+        // chunk partials, then a separate combine phase (measured round 1: the
+        // last-arriving CTA combining inline costs +6% on the 8B R=5 pass)
+        ph.push_back(ph.back());
+        ph.back().kind = PH_ACOMB;
       }
       if (tp && (kind == K_O || kind == K_DOWN)) add_tpred(l, kind == K_DOWN);
     }
@@ -536,37 +397,16 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     ph.back().xwait = tp ? 1 : 0;
   }
   if ((int)ph.size() > kMaxPhases(L)) return fail(PS_E_INVALID, "phase table overflow");
-  // per-tile counters (fixed per layer position, identical in every table) and
-  // the X dependency granularity: columns per producing tile of the previous
-  // GEMM phase (x∘g from O / down: 128; h from gate/up: 64); 0 after a
-  // non-GEMM phase (embed, attention combine)
-  {
-    int base = 0;
-    for (size_t i = 0; i < ph.size(); ++i) {
-      MegaPhase& P = ph[i];
-      if (P.kind != PH_GEMM) continue;
-      P.tctr = base;
-      base += P.g.n_tiles;
-      P.g.ll_tag = 1 + (int)i;       // LL stream-K flag tag: the phase index (< 1024)
-      const MegaPhase& D = ph[i - 1];
-      // Per-tile dependencies are implemented (X loader, ps_mega.cuh) but off by
-      // default: the acquire + proxy fences per producer-tile batch serialise the
-      // X loader behind its own in-flight TMA loads (measured 2x slower); the
-      // phase-level gate with a decoupled W producer streams at ~6.6 TB/s.
-      P.dep_w = 0;
-      if (D.kind == PH_GEMM && (g_test_flags & 256)) P.dep_w = D.gu ? 64 : 128;
-    }
-    if (base > S->n_tile_ctr) return fail(PS_E_INVALID, "tile counter overflow");
-  }
+  // LL stream-K flag tag: the phase index (< 1024)
+  for (size_t i = 0; i < ph.size(); ++i)
+    if (ph[i].kind == PH_GEMM) ph[i].g.ll_tag = 1 + (int)i;
   const int key = b * 2 + (with_head ? 1 : 0);
   if (S->mega_maps[key]) cudaFree(S->mega_maps[key]);
   if (S->mega_ph[key]) cudaFree(S->mega_ph[key]);
   CU_TRY(cudaMalloc(&S->mega_maps[key], std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
   CU_TRY(cudaMemcpy(S->mega_maps[key], maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-  if (g_test_flags & 8) {   // test: per-phase epilogue stamps [phase][cta][4]
-    if (!S->epi_dbg) CU_TRY(cudaMalloc(&S->epi_dbg, (size_t)kMaxPhases(S->sh.n_layers) * g_num_sms * 4 * 8));
+  if (S->epi_dbg)   // PS_TRACE builds: per-phase stream-K fixup stamps [phase][cta][4]
     for (size_t i = 0; i < ph.size(); ++i) ph[i].g.dbg = S->epi_dbg + i * g_num_sms * 4;
-  }
   const CUtensorMap* dm = S->mega_maps[key];
   for (auto& P : ph) {
     if (P.kind != PH_GEMM) continue;
@@ -584,20 +424,11 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
 
 static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   const int key = b * 2 + (with_head ? 1 : 0);
-  if (!S->mega_ph[key]) {
-    ps_status st = build_mega(S, b, with_head);
-    if (st != PS_OK) return st;
-  }
-  if ((g_test_flags & 8) && !S->mega_dbg)
-    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * kMaxPhases(S->sh.n_layers) * 8 * 8));
-  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, (g_test_flags & 8) ? S->mega_dbg : nullptr,
-                S->tile_done, S->tp_size, {}};
+  // (tables are built at create / connect time: a build here would allocate
+  // after the forward's generation counters were prepared)
+  if (!S->mega_ph[key]) return fail(PS_E_INVALID, "megakernel phase table %d missing", key);
+  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, S->mega_dbg, S->tp_size, {}};
   for (int q = 0; q < S->tp_size; ++q) mp.peer_done[q] = (const unsigned*)S->peers[q];
-  mp.spin_cap = (g_test_flags & 8192) ? 256 : 64;   // measured: 1024 +5-8%, 256 vs 64 vs 32 within noise
-  // per-tile completion counters only when the per-tile X gate is on: the tile
-  // publish (barrier + proxy fence + release) sits on every stream-K reducer's
-  // critical path (measured: 8B R=5 pass -1.6%, 1B R=1 step -2.7% without it)
-  mp.tile_pub = (g_test_flags & 256) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S->n_ctas);
   cfg.blockDim = dim3(kMegaThreads);
@@ -611,17 +442,9 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   // ranks of a tensor-parallel group sharing one GPU (max_ctas partitions)
   // would wait on each other forever.  A partial grid (one 200+ KB CTA per
   // SM, at most the free SMs) is launched as a plain kernel instead.
-  cfg.numAttrs = (S->n_ctas == g_num_sms || (g_test_flags & 512)) ? 1 : 0;
+  cfg.numAttrs = S->n_ctas == g_num_sms ? 1 : 0;
   cudaError_t e;
-  if (g_test_flags & 32) {   // test: shallow ring
-    if (b == 0) {
-      cfg.dynamicSmemBytes = MegaSmem<16, 4>::kBytes;
-      e = cudaLaunchKernelEx(&cfg, mega_kernel<16, 4>, mp);
-    } else {
-      cfg.dynamicSmemBytes = MegaSmem<32, 4>::kBytes;
-      e = cudaLaunchKernelEx(&cfg, mega_kernel<32, 4>, mp);
-    }
-  } else if (b == 0 && S->sh.d_model <= 2048) {
+  if (b == 0 && S->sh.d_model <= 2048) {
     // Small models: a 6-slot ring.  A deeper ring runs further ahead across
     // phase boundaries but queues the boundary's latency-critical loads
     // (stream-K partials, X tiles, attention) behind more weight bytes, and
@@ -664,27 +487,6 @@ static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
   return PS_OK;
 }
 
-static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head);
-static ps_status run_forward(ps_stage* S, int R, bool with_head) {
-  const int b = bucket_of(R);
-  S->last_bucket = b;
-  // Forwards are enqueued back to back (prefill chunks): each uses its own
-  // staging slot, and a slot is rewritten only after its previous copy ran.
-  CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
-  CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
-  S->in_slot = (S->in_slot + 1) % 8;
-  if (S->use_mega) {
-    if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
-    ps_status st = launch_mega(S, b, with_head);
-    if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[1], S->stream));
-    return st;
-  }
-  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
-  ps_status st_fwd = run_forward_kernels(S, b, with_head);
-  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[1], S->stream));
-  return st_fwd;
-}
-
 static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head) {
   if (!S->use_graphs) return enqueue_forward(S, b, with_head);
   cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
@@ -706,33 +508,33 @@ static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head) {
 }
 
 // ---------------------------------------------------------------- paging
+// Mapped logical pages always form a prefix [0, n_mapped) of the page table:
+// ensure_pages extends it, free_pages_from cuts it.
 static ps_status ensure_pages(ps_stage* S, long long last_pos) {
   const int need = (int)(last_pos / S->page_size) + 1;
   if (need > (int)S->page_of.size()) return fail(PS_E_CAPACITY, "position %lld beyond max_seq", last_pos);
-  int lo = -1, hi = -1;
-  for (int lp = 0; lp < need; ++lp) {
-    if (S->page_of[lp] >= 0) continue;
-    if (S->free_pages.empty()) return fail(PS_E_CAPACITY, "KV pool exhausted");
+  if (need <= S->n_mapped) return PS_OK;
+  if ((int)S->free_pages.size() < need - S->n_mapped) return fail(PS_E_CAPACITY, "KV pool exhausted");
+  const int lo = S->n_mapped;
+  for (int lp = lo; lp < need; ++lp) {
     S->page_of[lp] = S->free_pages.back();
     S->free_pages.pop_back();
     S->h_page_table[lp] = S->page_of[lp];
-    if (lo < 0) lo = lp;
-    hi = lp;
   }
-  if (lo >= 0)
-    CU_TRY(cudaMemcpyAsync(S->d_page_table + lo, S->h_page_table + lo, (size_t)(hi - lo + 1) * 4,
-                           cudaMemcpyHostToDevice, S->stream));
+  S->n_mapped = need;
+  CU_TRY(cudaMemcpyAsync(S->d_page_table + lo, S->h_page_table + lo, (size_t)(need - lo) * 4, cudaMemcpyHostToDevice,
+                         S->stream));
   return PS_OK;
 }
 
+// Free the pages lying wholly at or beyond kv_len: O(#freed pages).
 static void free_pages_from(ps_stage* S, long long kv_len) {
-  // free pages lying wholly at or beyond kv_len (O(#freed))
-  const long long first = (kv_len + S->page_size - 1) / S->page_size;
-  for (long long lp = (long long)S->page_of.size() - 1; lp >= first; --lp) {
-    if (S->page_of[lp] < 0) continue;
+  const int first = (int)((kv_len + S->page_size - 1) / S->page_size);
+  for (int lp = S->n_mapped - 1; lp >= first; --lp) {
     S->free_pages.push_back(S->page_of[lp]);
     S->page_of[lp] = -1;   // the pinned mirror entry may still be in flight: leave it
   }
+  if (first < S->n_mapped) S->n_mapped = first;
 }
 
 static long long pages_in_use(const ps_stage* S) {
@@ -781,7 +583,6 @@ ps_status ps_stage_destroy(ps_stage* S) {
   for (int q = 0; q < 8; ++q)
     if (S->peer_ipc[q]) cudaIpcCloseMemHandle(S->peers[q]);
   if (S->xch) cudaFree(S->xch);
-  if (S->tile_done) cudaFree(S->tile_done);
   if (S->mega_dbg) cudaFree(S->mega_dbg);
   if (S->attn_dbg) cudaFree(S->attn_dbg);
   void* dev[] = {S->d_page_table, S->d_in, S->d_out, S->x, S->q, S->ss, S->logits, S->ws, S->xg, S->att, S->h,
@@ -794,6 +595,7 @@ ps_status ps_stage_destroy(ps_stage* S) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : S->fwd_ev)
     if (ev) cudaEventDestroy(ev);
+  if (S->done_ev) cudaEventDestroy(S->done_ev);
   if (S->h_out) cudaFreeHost(S->h_out);
   if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
   delete S;
@@ -819,18 +621,36 @@ static ps_status build_all_tables(ps_stage* S) {
       ps_status st = build_mega(S, b, h != 0);
       if (st != PS_OK) return st;
     }
-  if ((g_test_flags & 8) && !S->mega_dbg)
-    CU_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * kMaxPhases(S->sh.n_layers) * 8 * 8));
   CU_TRY(cudaDeviceSynchronize());
   return PS_OK;
 }
 
+// Exported handle: the IPC handle of the exchange buffer plus what every rank
+// must agree on -- the megakernel grid (each rank waits for its peers' phase
+// counters at ITS OWN target gen * n_ctas), the buffer size and the shard shape.
+struct TpHandle {
+  cudaIpcMemHandle_t ipc;
+  uint32_t magic;
+  int32_t tp_rank, tp_size, n_ctas;
+  int64_t xch_bytes;
+  ps_model_shape shard;
+};
+static_assert(sizeof(TpHandle) <= PS_TP_HANDLE_BYTES, "handle size");
+constexpr uint32_t kTpMagic = 0x50535450u;   // "PSTP"
+
 ps_status ps_tp_handle(ps_stage* S, void* handle_out) {
   if (!S || !handle_out) return fail(PS_E_INVALID, "NULL argument");
-  static_assert(sizeof(cudaIpcMemHandle_t) == PS_TP_HANDLE_BYTES, "handle size");
   CU_TRY(cudaSetDevice(S->device));
-  cudaIpcMemHandle_t h;
-  CU_TRY(cudaIpcGetMemHandle(&h, S->xch));
+  TpHandle h;
+  memset(&h, 0, sizeof h);
+  CU_TRY(cudaIpcGetMemHandle(&h.ipc, S->xch));
+  h.magic = kTpMagic;
+  h.tp_rank = S->tp_rank;
+  h.tp_size = S->tp_size;
+  h.n_ctas = S->n_ctas;
+  h.xch_bytes = (int64_t)S->xch_bytes;
+  h.shard = S->sh;
+  memset(handle_out, 0, PS_TP_HANDLE_BYTES);
   memcpy(handle_out, &h, sizeof h);
   return PS_OK;
 }
@@ -838,16 +658,26 @@ ps_status ps_tp_handle(ps_stage* S, void* handle_out) {
 ps_status ps_tp_connect(ps_stage* S, const void* handles) {
   if (!S || !handles) return fail(PS_E_INVALID, "NULL argument");
   if (S->tp_size < 2) return fail(PS_E_INVALID, "stage is not tensor parallel");
+  for (int q = 0; q < S->tp_size; ++q) {   // every rank must match this one's grid and shard
+    if (q == S->tp_rank) continue;
+    TpHandle h;
+    memcpy(&h, (const uint8_t*)handles + (size_t)q * PS_TP_HANDLE_BYTES, sizeof h);
+    if (h.magic != kTpMagic || h.tp_rank != q || h.tp_size != S->tp_size)
+      return fail(PS_E_INVALID, "handle %d is not rank %d of a tp_size %d group", q, q, S->tp_size);
+    if (h.n_ctas != S->n_ctas || h.xch_bytes != (int64_t)S->xch_bytes || memcmp(&h.shard, &S->sh, sizeof S->sh) != 0)
+      return fail(PS_E_INVALID, "rank %d: megakernel grid (%d vs %d CTAs) or shard shape differs from rank %d", q,
+                  h.n_ctas, S->n_ctas, S->tp_rank);
+  }
   CU_TRY(cudaSetDevice(S->device));
   CU_TRY(cudaStreamSynchronize(S->stream));
   drop_tables(S);
   for (int q = 0; q < S->tp_size; ++q) {
     if (q == S->tp_rank) continue;
     if (S->peer_ipc[q]) { cudaIpcCloseMemHandle(S->peers[q]); S->peer_ipc[q] = false; }
-    cudaIpcMemHandle_t h;
+    TpHandle h;
     memcpy(&h, (const uint8_t*)handles + (size_t)q * PS_TP_HANDLE_BYTES, sizeof h);
     void* p = nullptr;
-    CU_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    CU_TRY(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
     S->peers[q] = (uint8_t*)p;
     S->peer_ipc[q] = true;
   }
@@ -916,7 +746,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   const int64_t need = ps_kv_pool_bytes_tp(shape, o->max_seq, o->page_size, tp);
   if ((need > 0 && !o->kv_pool) || o->kv_pool_bytes < need)
     return fail(PS_E_INVALID, "kv_pool too small (%lld < %lld bytes)", (long long)o->kv_pool_bytes, (long long)need);
-  if ((st = init_device_globals(pl->device)) != PS_OK) return st;
+  if ((st = init_stage_device(pl->device)) != PS_OK) return st;
 
   ps_stage* S = new (std::nothrow) ps_stage();
   if (!S) return fail(PS_E_INVALID, "out of host memory");
@@ -992,26 +822,28 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaHostAlloc(&S->h_in, 8 * sizeof(StepIn), cudaHostAllocDefault));
   for (auto& ev : S->in_ev) S_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   for (auto& ev : S->fwd_ev) S_TRY(cudaEventCreate(&ev));
+  S_TRY(cudaEventCreateWithFlags(&S->done_ev, cudaEventDisableTiming));
   S_TRY(cudaHostAlloc(&S->h_out, sizeof(StepOut), cudaHostAllocMapped));
   S_TRY(cudaHostGetDevicePointer((void**)&S->h_out_dev, S->h_out, 0));
   memset(S->h_in, 0, 8 * sizeof(StepIn));
   S_TRY(cudaMalloc(&S->x, (size_t)kMaxRows * d * 4));
-  S_TRY(cudaMalloc(&S->xg, (size_t)kMaxRows * d * 2));
-  S_TRY(cudaMalloc(&S->att, (size_t)kMaxRows * hq * 2));
-  S_TRY(cudaMalloc(&S->h, (size_t)kMaxRows * f * 2));
+  // split-bf16 GEMM operands: hi rows [0, kMaxRows), lo rows [kMaxRows, 2 kMaxRows)
+  S_TRY(cudaMalloc(&S->xg, (size_t)2 * kMaxRows * d * 2));
+  S_TRY(cudaMalloc(&S->att, (size_t)2 * kMaxRows * hq * 2));
+  S_TRY(cudaMalloc(&S->h, (size_t)2 * kMaxRows * f * 2));
   S_TRY(cudaMalloc(&S->q, (size_t)kMaxRows * hq * 4));
   S_TRY(cudaMalloc(&S->ss, (size_t)kMaxRows * S->ss_ld * 4));
   S_TRY(cudaMalloc(&S->logits, (size_t)kMaxRows * sh.vocab * 4));
   S_TRY(cudaMemset(S->x, 0, (size_t)kMaxRows * d * 4));
-  S_TRY(cudaMemset(S->xg, 0, (size_t)kMaxRows * d * 2));
-  S_TRY(cudaMemset(S->att, 0, (size_t)kMaxRows * hq * 2));
-  S_TRY(cudaMemset(S->h, 0, (size_t)kMaxRows * f * 2));
+  S_TRY(cudaMemset(S->xg, 0, (size_t)2 * kMaxRows * d * 2));
+  S_TRY(cudaMemset(S->att, 0, (size_t)2 * kMaxRows * hq * 2));
+  S_TRY(cudaMemset(S->h, 0, (size_t)2 * kMaxRows * f * 2));
   S_TRY(cudaMemset(S->q, 0, (size_t)kMaxRows * hq * 4));
   S_TRY(cudaMemset(S->ss, 0, (size_t)kMaxRows * S->ss_ld * 4));
   for (int b = 0; b < 2; ++b) {
-    P_TRY(make_map(&S->map_xg[b], S->xg, kMaxRows, d, bucket_rp(b)));
-    P_TRY(make_map(&S->map_att[b], S->att, kMaxRows, hq, bucket_rp(b)));
-    P_TRY(make_map(&S->map_h[b], S->h, kMaxRows, f, bucket_rp(b)));
+    P_TRY(make_map(&S->map_xg[b], S->xg, 2 * kMaxRows, d, bucket_rp(b)));
+    P_TRY(make_map(&S->map_att[b], S->att, 2 * kMaxRows, hq, bucket_rp(b)));
+    P_TRY(make_map(&S->map_h[b], S->h, 2 * kMaxRows, f, bucket_rp(b)));
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
   const int n = S->n_ctas;
@@ -1030,8 +862,9 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   }
   // fp32 partials (release path) or (fp32, flag) words (LL path): 8 bytes each;
   // zeroed so no stale flag of a freed buffer can match
-  S_TRY(cudaMalloc(&S->ws, ws_elems * 8));
-  S_TRY(cudaMemset(S->ws, 0, ws_elems * 8));
+  S->ws_bytes = ws_elems * 8;
+  S_TRY(cudaMalloc(&S->ws, S->ws_bytes));
+  S_TRY(cudaMemset(S->ws, 0, S->ws_bytes));
   S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * 4));
   S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
   S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * 8));
@@ -1057,7 +890,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   }
   // --- paged KV
   S->kv = (__nv_bfloat16*)o->kv_pool;
-  S->page_elems = (long long)sh.n_layers * 2 * sh.n_kv_heads * S->page_size * sh.head_dim;
+  S->page_elems = (long long)sh.n_layers * kKvPlanes * sh.n_kv_heads * S->page_size * sh.head_dim;
   const int lpages = (S->max_seq + kMaxRows + S->page_size - 1) / S->page_size;
   S->pages_total = S->page_elems ? (int)(o->kv_pool_bytes / (S->page_elems * 2)) : lpages;   // 0 layers: no KV
   S->page_of.assign(lpages, -1);
@@ -1066,8 +899,13 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->d_page_table, 0, (size_t)lpages * 4));
   S_TRY(cudaHostAlloc(&S->h_page_table, (size_t)lpages * 4, cudaHostAllocDefault));
   memset(S->h_page_table, 0, (size_t)lpages * 4);
+#if PS_TRACE
   S_TRY(cudaMalloc(&S->attn_dbg, (size_t)1024 * 8 * 8));
   S_TRY(cudaMemset(S->attn_dbg, 0, (size_t)1024 * 8 * 8));
+  S_TRY(cudaMalloc(&S->mega_dbg, (size_t)g_num_sms * kMaxPhases(sh.n_layers) * 8 * 8));
+  S_TRY(cudaMemset(S->mega_dbg, 0, (size_t)g_num_sms * kMaxPhases(sh.n_layers) * 8 * 8));
+  S_TRY(cudaMalloc(&S->epi_dbg, (size_t)kMaxPhases(sh.n_layers) * g_num_sms * 4 * 8));
+#endif
   // --- exchange buffer: megakernel phase-completion counters (cumulative; see
   // ps_mega.cuh), tensor-parallel partials and argmax keys (read by peers)
   S->off_part = ((size_t)kMaxPhases(sh.n_layers) * 4 + 255) / 256 * 256;
@@ -1077,17 +915,13 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->xch, 0, S->xch_bytes));
   S->mega_done = (unsigned*)S->xch;
   S->peers[S->tp_rank] = S->xch;
-  {  // per-tile counters: QKV, O, gate/up, down per layer + lm_head
-    S->n_tile_ctr = sh.n_layers * (S->gs_qkv.n_tiles + S->gs_o.n_tiles + S->gs_gu.n_tiles + S->gs_d.n_tiles) +
-                    S->gs_lm.n_tiles;
-    S_TRY(cudaMalloc(&S->tile_done, (size_t)std::max(1, S->n_tile_ctr) * 4));
-    S_TRY(cudaMemset(S->tile_done, 0, (size_t)std::max(1, S->n_tile_ctr) * 4));
-  }
   // --- synthetic override (disabled)
   S_TRY(cudaMalloc(&S->d_syn, sizeof(SynthParams)));
   S->h_syn = SynthParams{};
   S_TRY(cudaMemcpy(S->d_syn, &S->h_syn, sizeof(SynthParams), cudaMemcpyHostToDevice));
   S_TRY(cudaStreamSynchronize(S->stream));
+  // phase tables now (tensor-parallel groups build theirs at connect time)
+  if (tp == 1 && S->use_mega) P_TRY(build_all_tables(S));
   *out = S;
 #undef S_TRY
 #undef P_TRY
@@ -1095,13 +929,22 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
 }
 
 // One forward over tokens [start, start+R) at positions [start, start+R);
-// with_head computes logits/argmax for all rows.
+// with_head computes logits/argmax for all rows.  dev_window (optional): a
+// DEVICE array of w draft tokens copied on-stream into rows row0+1.. (the host
+// rows there are placeholders).  The stage's forward counters (gen, gen_head:
+// the megakernel's cumulative phase targets) are committed only once the
+// forward is enqueued, so a failed launch leaves them consistent with the
+// device counters.
 static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long pos0, int w, bool with_head,
-                              bool want_logits, int row0 = 0) {
+                              bool want_logits, int row0 = 0, const int32_t* dev_window = nullptr) {
   ps_status st;
   if (!S->tp_connected) return fail(PS_E_INVALID, "tensor-parallel stage not connected (ps_tp_connect)");
   if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
   CU_TRY(cudaEventSynchronize(S->in_ev[S->in_slot]));   // slot's previous copy done
+  const unsigned gen = S->gen + 1, gen_head = S->gen_head + (with_head ? 1 : 0);
+  // LL stream-K flags carry gen mod 2^22 (ps_kernels.cuh): clear the partial
+  // workspace every 2^20 forwards so no slot can hold a flag old enough to alias
+  if ((gen & ((1u << 20) - 1)) == 0) CU_TRY(cudaMemsetAsync(S->ws, 0, S->ws_bytes, S->stream));
   StepIn* in = S->h_in + S->in_slot;
   in->R = R;
   in->pos0 = (int32_t)pos0;
@@ -1110,21 +953,37 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   in->syn_p0 = 0;
   in->syn_onpath = 0;
   in->row0 = row0;
-  in->gen = (int32_t)(++S->gen);
-  if (with_head) ++S->gen_head;
-  in->gen_head = (int32_t)S->gen_head;
+  in->gen = (int32_t)gen;
+  in->gen_head = (int32_t)gen_head;
   if (with_head && !S->S_host.empty()) {
     in->flags |= kFlagSynth;
-    const long long gen = (long long)S->tokens.size() - S->n_prompt;
-    in->syn_p0 = (int32_t)gen;
-    in->syn_onpath = (gen >= 0 && S->onpath == gen) ? 1 : 0;
+    const long long g = (long long)S->tokens.size() - S->n_prompt;
+    in->syn_p0 = (int32_t)g;
+    in->syn_onpath = (g >= 0 && S->onpath == g) ? 1 : 0;
   }
   for (int j = 0; j < kMaxRows; ++j) in->tokens[j] = j < R ? toks[j] : 0;
-  return run_forward(S, R, with_head);
+  const int b = bucket_of(R);
+  S->last_bucket = b;
+  // Forwards are enqueued back to back (prefill chunks): each uses its own
+  // staging slot, and a slot is rewritten only after its previous copy ran.
+  CU_TRY(cudaMemcpyAsync(S->d_in, S->h_in + S->in_slot, sizeof(StepIn), cudaMemcpyHostToDevice, S->stream));
+  if (dev_window && w > 0)
+    CU_TRY(cudaMemcpyAsync(S->d_in->tokens + row0 + 1, dev_window, (size_t)w * 4, cudaMemcpyDeviceToDevice,
+                           S->stream));
+  CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
+  S->in_slot = (S->in_slot + 1) % 8;
+  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
+  st = S->use_mega ? launch_mega(S, b, with_head) : run_forward_kernels(S, b, with_head);
+  if (st != PS_OK) return st;
+  S->gen = gen;                        // the forward is enqueued: commit the counters
+  S->gen_head = gen_head;
+  if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[1], S->stream));
+  return PS_OK;
 }
 
 ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
+  PS_NOT_INFLIGHT(S);
   if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "prefill length %d not in [1, max_seq]", n);
   for (int i = 0; i < n; ++i)
     if (tokens[i] < 0 || tokens[i] >= S->vocab_full) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
@@ -1169,6 +1028,7 @@ static ps_status catch_up(ps_stage* S, int reserve_rows) {
 
 ps_status ps_resync(ps_stage* S, const int32_t* tokens, int32_t n) {
   if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
+  PS_NOT_INFLIGHT(S);
   if (n < 1 || n > S->max_seq) return fail(PS_E_INVALID, "resync length %d not in [1, max_seq]", n);
   for (int i = 0; i < n; ++i)
     if (tokens[i] < 0 || tokens[i] >= S->vocab_full) return fail(PS_E_INVALID, "token %d out of range", tokens[i]);
@@ -1181,22 +1041,24 @@ ps_status ps_resync(ps_stage* S, const int32_t* tokens, int32_t n) {
   return PS_OK;
 }
 
-static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t* a_out, int32_t* next_out,
-                             float* logits_out) {
+// Enqueue one verification pass (rows = KV catch-up suffix, pending x[n-1],
+// window) without waiting.  `window` is host memory, or (dev) device memory.
+static ps_status verify_launch(ps_stage* S, const int32_t* window, int w, bool dev, float* logits_out) {
   const long long n = (long long)S->tokens.size();
   if (n < 1) return fail(PS_E_CONTRACT, "verify on an empty token buffer (call ps_prefill first)");
   if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d > max_window %d", w, S->max_window);
   if (n + w > S->max_seq) return fail(PS_E_CAPACITY, "n + w = %lld exceeds max_seq", n + w);
   if (S->kv_len > n - 1) return fail(PS_E_CONTRACT, "KV covers %lld positions > n-1 = %lld", S->kv_len, n - 1);
-  for (int j = 0; j < w; ++j)
-    if (window[j] < 0 || window[j] >= S->vocab_full) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
+  if (!dev)
+    for (int j = 0; j < w; ++j)
+      if (window[j] < 0 || window[j] >= S->vocab_full) return fail(PS_E_INVALID, "draft token %d out of range", window[j]);
   ps_status st = catch_up(S, 1 + w);
   if (st != PS_OK) return st;
   const int row0 = (int)(n - 1 - S->kv_len);
   int32_t rows[kMaxRows];
   for (int j = 0; j <= row0; ++j) rows[j] = S->tokens[S->kv_len + j];
-  for (int j = 0; j < w; ++j) rows[row0 + 1 + j] = window[j];
-  st = forward_rows(S, rows, row0 + 1 + w, S->kv_len, w, true, logits_out != nullptr, row0);
+  for (int j = 0; j < w; ++j) rows[row0 + 1 + j] = dev ? 0 : window[j];
+  st = forward_rows(S, rows, row0 + 1 + w, S->kv_len, w, true, logits_out != nullptr, row0, dev ? window : nullptr);
   if (st != PS_OK) return st;
   if (logits_out) {
     cudaPointerAttributes at{};
@@ -1207,7 +1069,13 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
     CU_TRY(cudaMemcpyAsync(logits_out, S->logits + (size_t)row0 * S->sh.vocab, (size_t)(w + 1) * S->sh.vocab * 4,
                            kind, S->stream));
   }
-  CU_TRY(cudaStreamSynchronize(S->stream));
+  S->if_n = n;
+  S->if_w = w;
+  return PS_OK;
+}
+
+// Commit the finished pass (its result is in the mapped pinned mirror).
+static ps_status verify_commit(ps_stage* S, int32_t* a_out, int32_t* next_out) {
   {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, S->fwd_ev[0], S->fwd_ev[1]) == cudaSuccess) {
@@ -1218,9 +1086,13 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
     cudaGetLastError();
   }
   const StepOut* r = S->h_out;
+  const long long n = S->if_n;
+  const int w = S->if_w;
+  if (r->R == -1) return fail(PS_E_INVALID, "device window holds a token outside [0, vocab)");
   const int a = r->a, nxt = r->next;
-  if (a < 0 || a > w || nxt < 0 || nxt >= S->vocab_full) return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d", a, nxt);
-  for (int j = 0; j < a; ++j) S->tokens.push_back(window[j]);
+  if (a < 0 || a > w || nxt < 0 || nxt >= S->vocab_full || r->kv_len != n + a)
+    return fail(PS_E_CUDA, "corrupt verify result a=%d next=%d kv_len=%d", a, nxt, r->kv_len);
+  for (int j = 0; j < a; ++j) S->tokens.push_back(r->pred[j]);   // accepted drafts: pred_j == d_j
   S->tokens.push_back(nxt);
   S->kv_len = n + a;
   free_pages_from(S, S->kv_len);
@@ -1230,27 +1102,76 @@ static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t*
   return PS_OK;
 }
 
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  const bool dev = p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  return dev;
+}
+
+static ps_status verify_host(ps_stage* S, const int32_t* window, int w, int32_t* a_out, int32_t* next_out,
+                             float* logits_out) {
+  ps_status st = verify_launch(S, window, w, false, logits_out);
+  if (st != PS_OK) return st;
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  return verify_commit(S, a_out, next_out);
+}
+
 ps_status ps_verify(ps_stage* S, const int32_t* window, int32_t w, int32_t* accepted_len, int32_t* next_token,
                     float* opt_logits) {
   if (!S || !accepted_len || !next_token || (w > 0 && !window)) return fail(PS_E_INVALID, "NULL argument");
+  PS_NOT_INFLIGHT(S);
   if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d not in [0, max_window=%d]", w, S->max_window);
   CU_TRY(cudaSetDevice(S->device));
   int32_t host_window[kMaxRows];
   const int32_t* win = window;
-  if (w > 0) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, window) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
-      CU_TRY(cudaMemcpyAsync(host_window, window, (size_t)w * 4, cudaMemcpyDeviceToHost, S->stream));
-      CU_TRY(cudaStreamSynchronize(S->stream));
-      win = host_window;
-    }
-    cudaGetLastError();
+  if (w > 0 && is_device_ptr(window)) {
+    CU_TRY(cudaMemcpyAsync(host_window, window, (size_t)w * 4, cudaMemcpyDeviceToHost, S->stream));
+    CU_TRY(cudaStreamSynchronize(S->stream));
+    win = host_window;
   }
   return verify_host(S, win, w, accepted_len, next_token, opt_logits);
 }
 
+ps_status ps_verify_async(ps_stage* S, const int32_t* window, int32_t w, ps_verify_ticket* ticket) {
+  if (!S || (w > 0 && !window)) return fail(PS_E_INVALID, "NULL argument");
+  PS_NOT_INFLIGHT(S);
+  if (w < 0 || w > S->max_window) return fail(PS_E_INVALID, "window %d not in [0, max_window=%d]", w, S->max_window);
+  CU_TRY(cudaSetDevice(S->device));
+  ps_status st = verify_launch(S, window, w, w > 0 && is_device_ptr(window), nullptr);
+  if (st != PS_OK) return st;
+  CU_TRY(cudaEventRecord(S->done_ev, S->stream));
+  S->inflight = true;
+  if (ticket) {
+    ticket->d_result = reinterpret_cast<const ps_verify_result*>(S->d_out);
+    ticket->h_result = reinterpret_cast<const ps_verify_result*>(S->h_out);
+    ticket->event = S->done_ev;
+  }
+  return PS_OK;
+}
+
+ps_status ps_verify_wait(ps_stage* S, int32_t* accepted_len, int32_t* next_token) {
+  if (!S || !accepted_len || !next_token) return fail(PS_E_INVALID, "NULL argument");
+  if (!S->inflight) return fail(PS_E_INVALID, "no ps_verify_async pass in flight");
+  CU_TRY(cudaSetDevice(S->device));
+  S->inflight = false;
+  CU_TRY(cudaEventSynchronize(S->done_ev));
+  return verify_commit(S, accepted_len, next_token);
+}
+
+ps_status ps_verify_query(ps_stage* S, int32_t* done) {
+  if (!S || !done) return fail(PS_E_INVALID, "NULL argument");
+  if (!S->inflight) { *done = 1; return PS_OK; }
+  CU_TRY(cudaSetDevice(S->device));
+  const cudaError_t e = cudaEventQuery(S->done_ev);
+  if (e == cudaSuccess) { *done = 1; return PS_OK; }
+  if (e == cudaErrorNotReady) { cudaGetLastError(); *done = 0; return PS_OK; }
+  return fail(PS_E_CUDA, "ps_verify_query: %s", cudaGetErrorString(e));
+}
+
 ps_status ps_draft(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
   if (!S || (n_steps > 0 && !out_tokens)) return fail(PS_E_INVALID, "NULL argument");
+  PS_NOT_INFLIGHT(S);
   if (n_steps < 0) return fail(PS_E_INVALID, "n_steps < 0");
   CU_TRY(cudaSetDevice(S->device));
   for (int i = 0; i < n_steps; ++i) {
@@ -1264,6 +1185,7 @@ ps_status ps_draft(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
 
 ps_status ps_kv_rollback(ps_stage* S, int64_t keep) {
   if (!S) return fail(PS_E_INVALID, "NULL stage");
+  PS_NOT_INFLIGHT(S);
   if (keep < 1 || keep > (int64_t)S->tokens.size())
     return fail(PS_E_CONTRACT, "rollback keep=%lld not in [1, len=%zu]", (long long)keep, S->tokens.size());
   S->tokens.resize((size_t)keep);
@@ -1295,6 +1217,8 @@ ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
   info->last_fwd_ms = S->last_fwd_ms;
   info->sum_fwd_ms = S->sum_fwd_ms;
   info->n_fwd = S->n_fwd;
+  info->max_window = S->max_window;
+  info->max_seq = S->max_seq;
   return PS_OK;
 }
 
@@ -1308,6 +1232,7 @@ ps_status ps_stage_reset_timers(ps_stage* S) {
 ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_t n_prompt, int32_t level,
                            int32_t top, const double* alphas, uint64_t seed) {
   if (!S) return fail(PS_E_INVALID, "NULL stage");
+  PS_NOT_INFLIGHT(S);
   CU_TRY(cudaSetDevice(S->device));
   CU_TRY(cudaStreamSynchronize(S->stream));
   if (S->d_S) { cudaFree(S->d_S); S->d_S = nullptr; }
@@ -1346,116 +1271,10 @@ ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_
 
 }  // extern "C"
 
-// ============================================================================ test hooks
-static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                void* stream, int iters, float* ms_out, unsigned long long* dbg_host) {
-  ps_status st;
-  if (R < 1 || R > kMaxRows || K % 64 || N < 1) return fail(PS_E_INVALID, "bad test gemm shape");
-  int dev = 0;
-  CU_TRY(cudaGetDevice(&dev));
-  if ((st = init_device_globals(dev)) != PS_OK) return st;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int RP = R <= 16 ? 16 : 32;
-  CUtensorMap mW, mX;
-  if ((st = make_map(&mW, W, N, K, 128)) != PS_OK) return st;
-  if ((st = make_map(&mX, X, kMaxRows, K, RP)) != PS_OK) return st;
-  GemmShape gs = gemm_shape((N + 127) / 128, K, g_num_sms);
-  StepIn hin{};
-  hin.R = R;
-  StepIn* din;
-  float* ws;
-  unsigned* cnt;
-  CU_TRY(cudaMalloc(&din, sizeof(StepIn)));
-  CU_TRY(cudaMalloc(&ws, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8));
-  CU_TRY(cudaMemset(ws, 0, (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8));
-  CU_TRY(cudaMalloc(&cnt, (size_t)gs.n_tiles * 4));
-  CU_TRY(cudaMemset(cnt, 0, (size_t)gs.n_tiles * 4));
-  CU_TRY(cudaMemcpy(din, &hin, sizeof hin, cudaMemcpyHostToDevice));
-  GemmParams p = {};
-  p.mode = EPI_STORE;
-  p.N = N;
-  p.n_tiles = gs.n_tiles;
-  p.kb_total = gs.kb_total;
-  p.maxseg = gs.maxseg;
-  p.grid = gs.grid;
-  p.step = din;
-  p.out = out;
-  p.ld_out = N;
-  p.ws = ws;
-  p.counters = cnt;
-  p.ll = (g_test_flags & 4096) ? 0 : 1;
-  p.ll_tag = 1;
-  p.test_mode = g_test_flags >> 1;
-  unsigned long long* dbg = nullptr;
-  const int nl = iters > 0 ? iters : 1;
-  if (dbg_host) CU_TRY(cudaMalloc(&dbg, (size_t)nl * gs.grid * 4 * 8));
-  cudaEvent_t e0, e1;
-  CU_TRY(cudaEventCreate(&e0));
-  CU_TRY(cudaEventCreate(&e1));
-  if (iters == 0) st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
-  p.dbg = dbg;
-  CU_TRY(cudaEventRecord(e0, s));
-  for (int i = 0; i < iters && st == PS_OK; ++i) {
-    p.dbg = dbg ? dbg + (size_t)i * gs.grid * 4 : nullptr;
-    p.ll_tag = 2 + i % 1000;          // distinct flags for back-to-back launches
-    st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
-  }
-  CU_TRY(cudaEventRecord(e1, s));
-  cudaError_t e = cudaStreamSynchronize(s);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  if (ms_out) *ms_out = ms / (iters > 0 ? iters : 1);
-  if (dbg_host && e == cudaSuccess) e = cudaMemcpy(dbg_host, dbg, (size_t)nl * gs.grid * 4 * 8, cudaMemcpyDeviceToHost);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (dbg) cudaFree(dbg);
-  cudaFree(din);
-  cudaFree(ws);
-  cudaFree(cnt);
-  if (st != PS_OK) return st;
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
-  return PS_OK;
-}
-
-__global__ void empty_smem_kernel(int* p) {
-  extern __shared__ int sm_[];
-  if (threadIdx.x == 0 && p) sm_[0] = p[0];
-}
-
-extern "C" ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters,
-                                             int32_t flags, float* avg_ms) {
-  g_test_flags = flags;
-  CU_TRY(cudaFuncSetAttribute(empty_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  cudaEvent_t e0, e1;
-  CU_TRY(cudaEventCreate(&e0));
-  CU_TRY(cudaEventCreate(&e1));
-  empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
-  CU_TRY(cudaEventRecord(e0, 0));
-  for (int i = 0; i < iters; ++i) empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
-  CU_TRY(cudaEventRecord(e1, 0));
-  CU_TRY(cudaEventSynchronize(e1));
-  float ms;
-  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
-  *avg_ms = ms / iters;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  return PS_OK;
-}
-
-extern "C" void ps_test_set_flags(int32_t flags) { g_test_flags = flags; }
-
-extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                  void* stream) {
-  return test_gemm_impl(W, X, out, N, K, R, stream, 0, nullptr, nullptr);
-}
-
-extern "C" ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                        void* stream, int32_t iters, float* avg_ms, uint64_t* cta_trace) {
-  return test_gemm_impl(W, X, out, N, K, R, stream, iters, avg_ms, (unsigned long long*)cta_trace);
-}
-
+// ============================================================================ measurement / trace hooks
 extern "C" ps_status ps_time_kernel(ps_stage* S, int32_t kind, int32_t layer, int32_t iters, double* avg_ms) {
   if (!S || !avg_ms || iters < 1) return fail(PS_E_INVALID, "bad arguments");
+  PS_NOT_INFLIGHT(S);
   if (kind < K_EMBED || kind > K_ARGMAX) return fail(PS_E_INVALID, "unknown kernel kind %d", kind);
   if (layer < 0 || (S->sh.n_layers > 0 && layer >= S->sh.n_layers)) return fail(PS_E_INVALID, "bad layer");
   CU_TRY(cudaSetDevice(S->device));
@@ -1476,7 +1295,8 @@ extern "C" ps_status ps_time_kernel(ps_stage* S, int32_t kind, int32_t layer, in
   return PS_OK;
 }
 
-extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t bytes) {
+#if PS_TRACE
+extern "C" ps_status ps_trace_read(ps_stage* S, int32_t which, void* dst, int64_t bytes) {
   if (!S || !dst) return fail(PS_E_INVALID, "NULL argument");
   const void* src = nullptr;
   switch (which) {
@@ -1499,6 +1319,7 @@ extern "C" ps_status ps_test_read(ps_stage* S, int32_t which, void* dst, int64_t
   CU_TRY(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost));
   return PS_OK;
 }
+#endif
 
 extern "C" ps_status ps_pipeline_run(ps_stage* const* stages, int32_t k, const int32_t* prompt, int32_t n_prompt,
                                      const ps_run_opts* opts, int32_t* out, int32_t* out_len, ps_run_stats* stats);

@@ -1,0 +1,256 @@
+// ps_testlib.cu — libpipespec_test.so: test infrastructure that the product
+// library does not carry (include/pipespec_test.h).
+//  * a closed-form host test double of a stage, driven through the SAME board
+//    code as the product runtime (ps_board.h), so the async protocol --
+//    threads and processes, rollbacks, epochs, the event log -- is testable
+//    without a GPU;
+//  * single-kernel probes of the production GEMM kernel (ps_kernels.cuh).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/pipespec_test.h"
+#include "ps_board.h"
+#include "ps_host.cuh"
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+ps_status fail(ps_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+extern "C" const char* ps_test_last_error(void) { return g_err.c_str(); }
+
+// ============================================================================ protocol test double
+// Stage K: next(c) = (c[-1] * 7919 + |c| * 104729 + 13) mod V; stage i < K
+// agrees with stage i+1 with probability alpha (hash of seed, i, |c|), else
+// emits another token.
+namespace {
+struct FakeStage {
+  int i, k, V;
+  double alpha;
+  uint64_t seed;
+  int sleep_us;
+  std::vector<int32_t> toks;
+  static uint64_t mix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  }
+  int32_t next_at(int level, const std::vector<int32_t>& c) const {
+    int64_t t = ((int64_t)c.back() * 7919 + (int64_t)c.size() * 104729 + 13) % V;
+    for (int j = k - 2; j >= level; --j) {
+      const uint64_t h = mix(seed ^ ((uint64_t)j << 48) ^ (uint64_t)c.size());
+      if ((double)(h >> 11) >= alpha * 9007199254740992.0) t = (t + 1 + (int64_t)(mix(h) % (uint64_t)(V - 1))) % V;
+    }
+    return (int32_t)t;
+  }
+  void nap() const { if (sleep_us > 0) usleep((useconds_t)(sleep_us * (1 + 3 * i))); }   // later stages are slower
+  static ps_status draft1(void* p, int32_t* t) {
+    FakeStage* s = (FakeStage*)p;
+    *t = s->next_at(s->i, s->toks);
+    s->toks.push_back(*t);
+    s->nap();
+    return PS_OK;
+  }
+  static ps_status verify(void* p, const int32_t* w, int32_t n, int32_t* a, int32_t* nx) {
+    FakeStage* s = (FakeStage*)p;
+    std::vector<int32_t> c = s->toks;
+    int j = 0;
+    int32_t pred = s->next_at(s->i, c);
+    while (j < n && pred == w[j]) {
+      c.push_back(w[j]);
+      ++j;
+      pred = s->next_at(s->i, c);
+    }
+    c.push_back(pred);
+    s->toks = c;
+    *a = j;
+    *nx = pred;
+    s->nap();
+    return PS_OK;
+  }
+  static ps_status resync(void* p, const int32_t* t, int32_t n) {
+    ((FakeStage*)p)->toks.assign(t, t + n);
+    return PS_OK;
+  }
+  static ps_status tokens(void* p, std::vector<int32_t>& v) {
+    v = ((FakeStage*)p)->toks;
+    return PS_OK;
+  }
+  StageOps ops() { return StageOps{this, draft1, verify, resync, tokens}; }
+};
+const std::string& fake_err() {
+  static thread_local std::string s = "fake stage error";
+  return s;
+}
+}  // namespace
+
+extern "C" ps_status ps_test_board_create(const char* name, int32_t k, int32_t capacity) {
+  if (!name || k < 1 || k > 8 || capacity < 2) return fail(PS_E_INVALID, "bad board arguments");
+  return board_create_shm(name, k, capacity);
+}
+
+extern "C" ps_status ps_test_board_unlink(const char* name) {
+  if (!name) return fail(PS_E_INVALID, "NULL board name");
+  return shm_unlink(name) == 0 ? PS_OK : fail(PS_E_INVALID, "cannot unlink %s", name);
+}
+
+extern "C" ps_status ps_test_fake_run_rank(int32_t rank, int32_t k, const char* board, const int32_t* prompt,
+                                           int32_t n_prompt, const ps_run_opts* o, int32_t vocab, double alpha,
+                                           uint64_t seed, int32_t sleep_us, int32_t* out, int32_t* out_len,
+                                           ps_run_stats* stats) {
+  if (!prompt || n_prompt < 1 || !o || vocab < 2 || k < 1 || k > 8) return fail(PS_E_INVALID, "bad arguments");
+  FakeStage f{rank, k, vocab, alpha, seed, sleep_us, std::vector<int32_t>(prompt, prompt + n_prompt)};
+  ps_run_stats local;
+  ps_run_stats* stt = stats ? stats : &local;
+  memset(stt, 0, sizeof *stt);
+  std::string err;
+  ps_status st = run_rank(f.ops(), rank, k, board, n_prompt, o, out, out_len, stt, fake_err, &err);
+  if (st != PS_OK) return fail(st, "%s", err.c_str());
+  return PS_OK;
+}
+
+extern "C" ps_status ps_test_fake_pipeline(int32_t k, const int32_t* prompt, int32_t n_prompt, const ps_run_opts* o,
+                                           int32_t vocab, double alpha, uint64_t seed, int32_t sleep_us,
+                                           int32_t* out, int32_t* out_len, ps_run_stats* stats) {
+  if (!prompt || n_prompt < 1 || !o || vocab < 2 || k < 1 || k > 8 || !out || !out_len)
+    return fail(PS_E_INVALID, "bad arguments");
+  std::vector<FakeStage> fs;
+  for (int i = 0; i < k; ++i)
+    fs.push_back(FakeStage{i, k, vocab, alpha, seed, sleep_us, std::vector<int32_t>(prompt, prompt + n_prompt)});
+  std::vector<StageOps> ops;
+  for (auto& f : fs) ops.push_back(f.ops());
+  const int cap = n_prompt + o->max_new_tokens + std::max(o->max_lead, 0) + 4 * 64 + 64;
+  std::vector<uint8_t> mem;
+  Board* b = board_on_heap(mem, k, cap, o->event_log ? std::max(o->event_cap, 0) : 0);
+  ps_run_stats local;
+  ps_run_stats* stt = stats ? stats : &local;
+  memset(stt, 0, sizeof *stt);
+  std::vector<int32_t> gen;
+  const long long t0 = now_ns();
+  ps_status st = run_board_threads(b, ops.data(), k, n_prompt, o, gen, stt, fake_err);
+  std::string msg = b->err_msg;
+  board_destroy(b);
+  if (st != PS_OK) return fail(st, "%s", msg.c_str());
+  if ((int)gen.size() > o->max_new_tokens) gen.resize(o->max_new_tokens);
+  std::copy(gen.begin(), gen.end(), out);
+  *out_len = (int32_t)gen.size();
+  stt->tokens = *out_len;
+  stt->wall_ns = now_ns() - t0;
+  return PS_OK;
+}
+
+// ============================================================================ single-kernel probes
+static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                void* stream, int iters, int test_mode, float* ms_out) {
+  ps_status st;
+  if (R < 1 || R > kMaxRows || K % 64 || N < 1) return fail(PS_E_INVALID, "bad test gemm shape");
+  int dev = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  if ((st = init_device_globals(dev)) != PS_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int RP = R <= 16 ? 16 : 32;
+  CUtensorMap mW, mX;
+  if ((st = make_map(&mW, W, N, K, 128)) != PS_OK) return st;
+  if ((st = make_map(&mX, X, kMaxRows, K, RP)) != PS_OK) return st;
+  GemmShape gs = gemm_shape((N + 127) / 128, K, g_num_sms);
+  StepIn hin{};
+  hin.R = R;
+  StepIn* din;
+  float* ws;
+  unsigned* cnt;
+  const size_t ws_bytes = (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8;
+  CU_TRY(cudaMalloc(&din, sizeof(StepIn)));
+  CU_TRY(cudaMalloc(&ws, ws_bytes));
+  CU_TRY(cudaMemset(ws, 0, ws_bytes));
+  CU_TRY(cudaMalloc(&cnt, (size_t)gs.n_tiles * 4));
+  CU_TRY(cudaMemset(cnt, 0, (size_t)gs.n_tiles * 4));
+  GemmParams p = {};
+  p.mode = EPI_STORE;
+  p.N = N;
+  p.n_tiles = gs.n_tiles;
+  p.kb_total = gs.kb_total;
+  p.maxseg = gs.maxseg;
+  p.grid = gs.grid;
+  p.step = din;
+  p.out = out;
+  p.ld_out = N;
+  p.ws = ws;
+  p.counters = cnt;
+  p.ll = 1;
+  p.test_mode = test_mode;
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  // every launch is a new "forward" (distinct LL flag generation)
+  hin.gen = 1;
+  CU_TRY(cudaMemcpy(din, &hin, sizeof hin, cudaMemcpyHostToDevice));
+  p.ll_tag = 1;
+  st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  CU_TRY(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters && st == PS_OK; ++i) {
+    p.ll_tag = 2 + i % 1000;          // distinct flags for back-to-back launches
+    st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
+  }
+  CU_TRY(cudaEventRecord(e1, s));
+  cudaError_t e = cudaStreamSynchronize(s);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (ms_out) *ms_out = ms / (iters > 0 ? iters : 1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(din);
+  cudaFree(ws);
+  cudaFree(cnt);
+  if (st != PS_OK) return st;
+  if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
+
+extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                  void* stream) {
+  return test_gemm_impl(W, X, out, N, K, R, stream, 0, 0, nullptr);
+}
+
+extern "C" ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
+                                        void* stream, int32_t iters, int32_t test_mode, float* avg_ms) {
+  return test_gemm_impl(W, X, out, N, K, R, stream, iters, test_mode, avg_ms);
+}
+
+__global__ void empty_smem_kernel(int* p) {
+  extern __shared__ int sm_[];
+  if (threadIdx.x == 0 && p) sm_[0] = p[0];
+}
+
+extern "C" ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters,
+                                             float* avg_ms) {
+  CU_TRY(cudaFuncSetAttribute(empty_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
+  CU_TRY(cudaEventRecord(e0, 0));
+  for (int i = 0; i < iters; ++i) empty_smem_kernel<<<grid, threads, smem>>>(nullptr);
+  CU_TRY(cudaEventRecord(e1, 0));
+  CU_TRY(cudaEventSynchronize(e1));
+  float ms;
+  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  *avg_ms = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return PS_OK;
+}

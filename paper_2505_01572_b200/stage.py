@@ -162,6 +162,32 @@ class Stage:
         buf = (C.c_uint8 * (abi.PS_TP_HANDLE_BYTES * self.tp_size)).from_buffer_copy(b"".join(handles))
         abi.check(abi.lib().ps_tp_connect(self._h, buf))
 
+    def verify_async(self, window):
+        """Enqueue a verification pass (ps_verify_async); `window` may be a CUDA
+        int32 tensor (gathered on-stream, never read by the host).  Returns the
+        ticket's pinned result record (valid after verify_wait)."""
+        if isinstance(window, torch.Tensor) and window.is_cuda:
+            self._async_win = window.to(torch.int32).contiguous()    # alive until the pass ran
+            ptr, w = self._async_win.data_ptr(), self._async_win.numel()
+        else:
+            self._async_win = _i32(window)
+            ptr, w = self._async_win.ctypes.data, len(self._async_win)
+        tk = abi.VerifyTicket()
+        abi.check(abi.lib().ps_verify_async(self._h, ptr if w else None, w, C.byref(tk)))
+        return tk
+
+    def verify_query(self) -> bool:
+        d = C.c_int32()
+        abi.check(abi.lib().ps_verify_query(self._h, C.byref(d)))
+        return bool(d.value)
+
+    def verify_wait(self):
+        """Commit the in-flight pass: returns (accepted_len, next_token)."""
+        a, nxt = C.c_int32(), C.c_int32()
+        abi.check(abi.lib().ps_verify_wait(self._h, C.byref(a), C.byref(nxt)))
+        self._async_win = None
+        return a.value, nxt.value
+
     def kv_rollback(self, keep_len: int):
         abi.check(abi.lib().ps_kv_rollback(self._h, keep_len))
 
@@ -177,7 +203,8 @@ class Stage:
         abi.check(abi.lib().ps_stage_get_info(self._h, C.byref(i)))
         return dict(n_tokens=i.n_tokens, kv_len=i.kv_len, pages_in_use=i.pages_in_use,
                     pages_total=i.pages_total, launches_per_verify=i.launches_per_verify,
-                    last_fwd_ms=i.last_fwd_ms, sum_fwd_ms=i.sum_fwd_ms, n_fwd=i.n_fwd)
+                    last_fwd_ms=i.last_fwd_ms, sum_fwd_ms=i.sum_fwd_ms, n_fwd=i.n_fwd,
+                    max_window=i.max_window, max_seq=i.max_seq)
 
     def reset_timers(self):
         abi.check(abi.lib().ps_stage_reset_timers(self._h))
@@ -207,10 +234,32 @@ def tp_connect_group(stage, group=None):
     stage.tp_connect(handles)
 
 
-def _run_opts(k, max_new_tokens, mode, gammas, lookaheads, eos_id, max_lead):
-    g = (C.c_int32 * k)(*(gammas or [0] * k))
-    la = (C.c_int32 * k)(*(lookaheads or [0] * k))
-    return abi.RunOpts(mode, max_new_tokens, eos_id, g, la, max_lead), (g, la)
+class RunOptions:
+    """ps_run_opts with its ctypes arrays kept alive.  gammas None -> NULL
+    (window cap 8 per verifier); alphas (k-1 floats) turn on the synthetic
+    override; virtual_ns pads every step of stage i to that many ns;
+    event_cap > 0 records the run's event log (see events())."""
+
+    def __init__(self, k, max_new_tokens, mode, gammas=None, lookaheads=None, eos_id=-1, max_lead=0,
+                 alphas=None, seed=0, virtual_ns=None, event_cap=0):
+        self.g = (C.c_int32 * k)(*gammas) if gammas is not None else None
+        self.la = (C.c_int32 * k)(*lookaheads) if lookaheads is not None else None
+        self.al = (C.c_double * max(1, k - 1))(*alphas) if alphas is not None else None
+        self.vn = (C.c_int64 * k)(*virtual_ns) if virtual_ns is not None else None
+        self.ev = (abi.Event * event_cap)() if event_cap > 0 else None
+        self.opts = abi.RunOpts(mode, max_new_tokens, eos_id,
+                                C.cast(self.g, C.POINTER(C.c_int32)) if self.g else None,
+                                C.cast(self.la, C.POINTER(C.c_int32)) if self.la else None, max_lead,
+                                C.cast(self.al, C.POINTER(C.c_double)) if self.al else None, seed,
+                                C.cast(self.vn, C.POINTER(C.c_int64)) if self.vn else None,
+                                C.cast(self.ev, C.POINTER(abi.Event)) if self.ev else None, event_cap)
+
+    def events(self, stats) -> list[dict]:
+        out = []
+        for e in (self.ev[:stats.n_events] if self.ev else []):
+            out.append(dict(t_ns=e.t_ns, stage=e.stage, kind=e.kind, n=e.n, w=e.w, a=e.a, next=e.next,
+                            origin=e.origin, window=list(e.window[:e.w])))
+        return out
 
 
 def board_create(name: str, k: int, capacity: int):
@@ -223,39 +272,53 @@ def board_unlink(name: str):
 
 
 def pipeline_run_rank(stage, rank: int, k: int, board: str, prompt, max_new_tokens: int, gammas=None,
-                      lookaheads=None, eos_id: int = -1, max_lead: int = 0):
+                      lookaheads=None, eos_id: int = -1, max_lead: int = 0, virtual_ns=None, event_cap: int = 0,
+                      return_events: bool = False):
     """This process's stage M_rank of a k-stage async PipeSpec run (ps_pipeline_run_rank)."""
-    opts, keep = _run_opts(k, max_new_tokens, abi.PS_MODE_PIPESPEC, gammas, lookaheads, eos_id, max_lead)
+    ro = RunOptions(k, max_new_tokens, abi.PS_MODE_PIPESPEC, gammas, lookaheads, eos_id, max_lead,
+                    virtual_ns=virtual_ns, event_cap=event_cap)
     p = _i32(prompt)
     out = np.zeros(max_new_tokens, dtype=np.int32)
     n = C.c_int32()
     stats = abi.RunStats()
     abi.check(abi.lib().ps_pipeline_run_rank(stage.handle, rank, k, board.encode(), p.ctypes.data, len(p),
-                                             C.byref(opts), out.ctypes.data, C.byref(n), C.byref(stats)))
+                                             C.byref(ro.opts), out.ctypes.data, C.byref(n), C.byref(stats)))
+    if return_events:
+        return out[:n.value].tolist(), stats, ro.events(stats)
     return out[:n.value].tolist(), stats
 
 
 def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PIPESPEC, gammas=None,
-                 lookaheads=None, eos_id: int = -1, max_lead: int = 0):
+                 lookaheads=None, eos_id: int = -1, max_lead: int = 0, alphas=None, seed: int = 0,
+                 virtual_ns=None, event_cap: int = 0, return_events: bool = False):
+    """ps_pipeline_run over `stages` (M_0 .. M_K).  Returns (tokens, stats[, events])."""
     k = len(stages)
     hs = (C.c_void_p * k)(*[s.handle for s in stages])
-    g = (C.c_int32 * k)(*(gammas or [0] * k))
-    la = (C.c_int32 * k)(*(lookaheads or [0] * k))
-    opts = abi.RunOpts(mode, max_new_tokens, eos_id, g, la, max_lead)
+    ro = RunOptions(k, max_new_tokens, mode, gammas, lookaheads, eos_id, max_lead, alphas, seed, virtual_ns,
+                    event_cap)
+    opts = ro.opts
     p = _i32(prompt)
     out = np.zeros(max_new_tokens, dtype=np.int32)
     n = C.c_int32()
     stats = abi.RunStats()
     abi.check(abi.lib().ps_pipeline_run(hs, k, p.ctypes.data, len(p), C.byref(opts), out.ctypes.data,
                                         C.byref(n), C.byref(stats)))
+    if return_events:
+        return out[:n.value].tolist(), stats, ro.events(stats)
     return out[:n.value].tolist(), stats
 
 
 def test_gemm(W: torch.Tensor, X: torch.Tensor, R: int) -> torch.Tensor:
-    """Test hook: out[r, n] = X[r] . W[n] through the production tcgen05 GEMM."""
+    """Test hook (libpipespec_test.so): out[r, n] = X[r] . W[n] through the
+    production tcgen05 GEMM kernel.  X: fp32 [32, K] -- handed to the kernel
+    as the split-bf16 operand it consumes (hi rows 0..31 = bf16(X), lo rows
+    32..63 = bf16(X - hi); pure marshalling, the products run on the GPU)."""
     N, K = W.shape
-    assert X.shape == (32, K) and X.dtype == torch.bfloat16 and W.dtype == torch.bfloat16
+    assert X.shape == (32, K) and X.dtype == torch.float32 and W.dtype == torch.bfloat16
+    hi = X.to(torch.bfloat16)
+    lo = (X - hi.float()).to(torch.bfloat16)
+    Xs = torch.cat([hi, lo]).contiguous()
     out = torch.zeros(R, N, dtype=torch.float32, device=W.device)
     s = torch.cuda.current_stream()
-    abi.check(abi.lib().ps_test_gemm(W.data_ptr(), X.data_ptr(), out.data_ptr(), N, K, R, s.cuda_stream))
+    abi.test_check(abi.test_lib().ps_test_gemm(W.data_ptr(), Xs.data_ptr(), out.data_ptr(), N, K, R, s.cuda_stream))
     return out

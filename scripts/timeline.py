@@ -1,5 +1,6 @@
 """Per-phase timeline of the verify megakernel from its %globaltimer stamps
-(test flag bit3, ps_test_read 9: [G][n_ph][8] u64 per CTA and phase:
+(the PS_TRACE build libpipespec_trace.so -- `python -m paper_2505_01572_b200._build
+--trace`, selected here through PS_LIB -- ps_trace_read 9: [G][n_ph][8] u64 per CTA and phase:
 0 epilogue start (after the phase wait), 1 publish, 2 X loader ready,
 3 first full ring slot (MMA), 4 MMA done, 5 first accumulator, 6 last
 accumulator, 7 last epilogue end).
@@ -18,6 +19,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("PS_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                             "paper_2505_01572_b200", "libpipespec_trace.so"))
 import numpy as np
 import torch
 
@@ -31,10 +34,7 @@ ap.add_argument("--ctx", type=int, default=512)
 ap.add_argument("--w", type=int, default=4)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--gbs", type=float, default=6542.0)
-ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
-
-abi.lib().ps_test_set_flags(8 | 64 | a.flags)
 s = synth.preset(a.shape)
 if a.layers:
     s = synth.reduced_depth(s, a.layers)
@@ -59,9 +59,9 @@ for rep in range(a.reps + 1):
         st.kv_rollback(a.ctx)
     torch.cuda.synchronize()
     buf = np.zeros(G * nph_max * 8, dtype=np.uint64)
-    abi.check(abi.lib().ps_test_read(st.handle, 9, buf.ctypes.data, buf.nbytes))
+    abi.check(abi.lib().ps_trace_read(st.handle, 9, buf.ctypes.data, buf.nbytes))
     ebuf = np.zeros(nph_max * G * 4, dtype=np.uint64)
-    abi.check(abi.lib().ps_test_read(st.handle, 11, ebuf.ctypes.data, ebuf.nbytes))
+    abi.check(abi.lib().ps_trace_read(st.handle, 11, ebuf.ctypes.data, ebuf.nbytes))
     et = ebuf.reshape(nph_max, G, 4).astype(np.int64)
     if rep == 0:
         continue
@@ -100,7 +100,7 @@ for rep in range(a.reps + 1):
     acc.setdefault("TOTAL", []).append((done[n_ph - 1] - t0, 0, 0))
     # attention item stamps of the LAST layer's ATTN phase (first item per CTA)
     abuf = np.zeros(1024 * 8, dtype=np.uint64)
-    abi.check(abi.lib().ps_test_read(st.handle, 10, abuf.ctypes.data, abuf.nbytes))
+    abi.check(abi.lib().ps_trace_read(st.handle, 10, abuf.ctypes.data, abuf.nbytes))
     at = abuf.reshape(1024, 8)[:G].astype(np.int64)
     pa = 1 + 6 * (L - 1) + 1                       # last ATTN phase index
     ok = (at[:, 0] > done[pa - 1]) & (at[:, 0] < done[pa])

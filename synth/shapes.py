@@ -51,8 +51,15 @@ class ModelShape:
         return self.n_layers * per_layer + 2 * self.vocab * self.d_model + 2 * self.d_model \
             + rows * 2 * self.d_model
 
-    def kv_bytes_per_token(self) -> int:
+    def kv_bytes_per_token_bf16(self) -> int:
+        """KV-cache bytes per token of a plain bf16 cache."""
         return self.n_layers * 2 * self.kv_dim * 2
+
+    def kv_bytes_per_token(self) -> int:
+        """KV-cache bytes per token as stored by the CUDA path: K and V, each a
+        split-bf16 pair (hi + lo planes, reading R28), i.e. 4 bytes
+        per element."""
+        return self.n_layers * 2 * self.kv_dim * 4
 
 
 PRESETS = {

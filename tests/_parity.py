@@ -1,11 +1,43 @@
-"""Shared parity helpers for the -m gpu tests (compare CUDA path vs oracle)."""
+"""Shared parity helpers for the -m gpu tests (compare CUDA path vs oracle).
+
+Tolerances (BASELINE.json north_star):
+  * logits: max|dlogit| <= 2e-2 * max|logit| against the oracle on the same
+    bf16-rounded weights;
+  * decisions (accepted length, next token, emitted tokens) bit-exact, except
+    where the oracle's top-2 logit gap is below 1e-2.
+
+The north star gives the gap bound no unit.  DESIGN.md reading R25: where the
+row's max|logit| <= 2 (toy, LLaMA-68M, LLaMA-3.2-1B widths) the bound is
+ABSOLUTE, 1e-2, and asserted as such; above that scale (7B/8B/13B/70B widths,
+max|logit| up to ~6) it is read relative to the row's max|logit| -- the same
+unit as the logit tolerance beside it, since a bf16-operand path's allowed
+logit error (2e-2 * max|logit|) exceeds an absolute 1e-2 there.  Every
+exemption taken is RECORDED (absolute gap, relative gap, scale, where) and
+reported at the end of the session (tests/conftest.py), so the bar's use is
+auditable.
+"""
 import numpy as np
 
 from oracle import llama as L
 
 REL_LOGIT_TOL = 2e-2      # north star: max|dlogit| <= 2e-2 * max|logit|
-TIE_GAP = 1e-2            # north star: decisions exempt where oracle top-2 gap < 1e-2,
-                          # read relative to the row's max|logit| (reading R25)
+TIE_GAP = 1e-2            # north star: decisions exempt where the oracle's top-2 gap < 1e-2
+ABS_SCALE_LIMIT = 2.0     # R25: at max|logit| <= this, the gap bound is absolute
+
+EXEMPTIONS: list[dict] = []   # every exemption taken in this session
+
+
+def _exempt(where: str, gap: float, z: np.ndarray):
+    """Assert a decision difference is a near-tie under R25 and record it."""
+    scale = float(np.abs(z).max())
+    rel = gap / scale
+    absolute = scale <= ABS_SCALE_LIMIT
+    EXEMPTIONS.append(dict(where=where, abs_gap=float(gap), rel_gap=float(rel), scale=scale,
+                           criterion="absolute" if absolute else "relative"))
+    if absolute:
+        assert gap < TIE_GAP, f"{where}: decision differs at top-2 gap {gap:.3e} >= {TIE_GAP} (max|logit| {scale:.2f})"
+    else:
+        assert rel < TIE_GAP, f"{where}: decision differs at relative gap {rel:.3e} >= {TIE_GAP} ({gap:.3e} abs)"
 
 
 def check_logits(gpu, ref, tol=REL_LOGIT_TOL):
@@ -16,25 +48,29 @@ def check_logits(gpu, ref, tol=REL_LOGIT_TOL):
     return err / scale
 
 
-def check_tokens_teacher_forced(w64, shape, prompt, gpu_tokens):
+def check_tokens_teacher_forced(w64, shape, prompt, gpu_tokens, where="stream"):
     """Every GPU-chosen token equals the oracle argmax on the GPU's own stream,
-    or the oracle prefers another token by less than TIE_GAP (reading R21)."""
+    or the oracle prefers another token by less than the R25 gap (reading R21).
+    Returns the number of exemptions taken."""
     z = L.forward_full(w64, shape, list(prompt) + list(gpu_tokens))[len(prompt) - 1:-1]
     exempt = 0
     for j, t in enumerate(gpu_tokens):
         best = int(np.argmax(z[j]))
         if best != t:
-            assert z[j][best] - z[j][t] < TIE_GAP * np.abs(z[j]).max(), (j, t, best, z[j][best] - z[j][t])
+            _exempt(f"{where}[{j}] gpu={t} oracle={best}", z[j][best] - z[j][t], z[j])
             exempt += 1
     return exempt
 
 
-def check_verify(res, ref, w):
-    """(a, next) bit-exact unless the deciding rows are near-ties."""
+def check_verify(res, ref, w, where="verify"):
+    """(a, next) bit-exact unless a deciding row is a near-tie (R25).  The
+    deciding rows are those both sides predicted before their paths part:
+    rows 0..min(a_gpu, a_oracle).  Returns True when exact."""
     a, nxt = res[0], res[1]
     if (a, nxt) == (ref["a"], ref["next"]):
         return True
     k = min(a, ref["a"])
-    rel = [g / np.abs(z).max() for g, z in zip(ref["gaps"][: k + 1], ref["logits"][: k + 1])]
-    assert min(rel) < TIE_GAP, (a, nxt, ref["a"], ref["next"], rel)
+    rel = [ref["gaps"][r] / np.abs(ref["logits"][r]).max() for r in range(k + 1)]
+    r = int(np.argmin(rel))                 # the nearest tie among the deciding rows
+    _exempt(f"{where} a={a}/{ref['a']} next={nxt}/{ref['next']} row {r}", ref["gaps"][r], ref["logits"][r])
     return False

@@ -25,3 +25,21 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Report every near-tie exemption the parity checks took (R25)."""
+    try:
+        from tests._parity import EXEMPTIONS
+    except Exception:  # pragma: no cover
+        return
+    tr = terminalreporter
+    tr.write_sep("-", f"R25 near-tie exemptions taken: {len(EXEMPTIONS)}")
+    for e in EXEMPTIONS:
+        tr.write_line(f"  {e['where']}: gap {e['abs_gap']:.3e} abs / {e['rel_gap']:.3e} rel "
+                      f"(max|logit| {e['scale']:.2f}, {e['criterion']} bound)")
+    out = os.environ.get("PS_EXEMPTIONS_JSON")
+    if out:
+        import json
+        with open(out, "w") as f:
+            json.dump(EXEMPTIONS, f, indent=1)

@@ -9,9 +9,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_functions():
+def declared_functions(header="pipespec.h"):
     names = set()
-    for h in os.listdir(os.path.join(ROOT, "include")):
+    for h in [header]:
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s+\**(ps_[a-z0-9_]+)\s*\(", src, re.M):
@@ -33,6 +33,24 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     # ctypes prototypes cover every declared function
     assert set(declared_functions()) <= set(abi._PROTOS)
+
+
+def test_product_library_carries_no_test_hooks():
+    """The protocol test double and kernel probes live in libpipespec_test.so
+    only; the trace accessor only in the PS_TRACE build."""
+    from paper_2505_01572_b200 import abi
+    lib = abi.lib()
+    for n in declared_functions("pipespec_test.h"):
+        assert not hasattr(lib, n), n
+
+
+def test_test_library_exports_its_header():
+    from paper_2505_01572_b200 import abi
+    tl = abi.test_lib()
+    names = [n for n in declared_functions("pipespec_test.h") if n != "ps_trace_read"]
+    missing = [n for n in names if not hasattr(tl, n)]
+    assert not missing, missing
+    assert set(names) <= set(abi._TEST_PROTOS)
 
 
 def test_pure_host_calls_without_gpu():

@@ -1,5 +1,6 @@
-"""GPU: the tcgen05 stream-K skinny GEMM (a4/a7-a10's contraction) against a
-plain PyTorch fp32 matmul of the same bf16 operands."""
+"""GPU: the tcgen05 stream-K skinny GEMM (a4/a7-a10's contraction, split-bf16
+activation operand, R28) against a plain PyTorch fp32 matmul of the
+bf16 weights and the fp32 activations."""
 import pytest
 import torch
 
@@ -12,11 +13,12 @@ def test_gemm_matches_torch(N, K, R):
     from paper_2505_01572_b200.stage import test_gemm
     g = torch.Generator(device="cuda").manual_seed(N * 7 + K + R)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    X = torch.randn(32, K, device="cuda", generator=g).to(torch.bfloat16)
+    X = torch.randn(32, K, device="cuda", generator=g)
     out = test_gemm(W, X, R)
-    ref = X[:R].float() @ W.float().T
+    ref = (X[:R].double() @ W.double().T).float()
     err = (out - ref).abs().max().item()
-    assert err <= 1e-4 * max(1.0, ref.abs().max().item()) + 1e-5, err
+    # split operand: ~2^-16 relative per element -> far below a bf16 operand's 2^-8
+    assert err <= 2e-5 * max(1.0, ref.abs().max().item()) + 1e-5, err
 
 
 def test_gemm_row_invariance():
@@ -24,7 +26,7 @@ def test_gemm_row_invariance():
     from paper_2505_01572_b200.stage import test_gemm
     g = torch.Generator(device="cuda").manual_seed(1)
     W = (torch.randn(4096, 4096, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    X = torch.randn(32, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    X = torch.randn(32, 4096, device="cuda", generator=g)
     a = test_gemm(W, X, 1)
     b = test_gemm(W, X, 17)
     c = test_gemm(W, X, 32)

@@ -24,11 +24,12 @@ def target_ar(prompt, n, V):
     return c[len(prompt):]
 
 
-def _opts(k, n, gamma, look=0, lead=0):
+def _opts(k, n, gamma, look=0, lead=0, event_cap=0):
     from paper_2505_01572_b200 import abi
-    g = (C.c_int32 * k)(*([0] + [gamma] * (k - 1)))
-    la = (C.c_int32 * k)(*([0] + [look] * (k - 1)))
-    return abi.RunOpts(abi.PS_MODE_PIPESPEC, n, -1, g, la, lead), (g, la)
+    from paper_2505_01572_b200.stage import RunOptions
+    ro = RunOptions(k, n, abi.PS_MODE_PIPESPEC, [0] + [gamma] * (k - 1), [0] + [look] * (k - 1), max_lead=lead,
+                    event_cap=event_cap)
+    return ro.opts, ro
 
 
 @pytest.mark.parametrize("k,alpha,gamma,look,sleep", [(2, 0.8, 4, 0, 0), (2, 0.5, 8, 0, 50), (2, 1.0, 4, 0, 0),
@@ -42,10 +43,14 @@ def test_threads_lossless(k, alpha, gamma, look, sleep):
     out = np.zeros(n, dtype=np.int32)
     ln = C.c_int32()
     st = abi.RunStats()
-    abi.check(abi.lib().ps_test_fake_pipeline(k, prompt.ctypes.data, len(prompt), C.byref(opts), V, alpha, 7,
+    abi.test_check(abi.test_lib().ps_test_fake_pipeline(k, prompt.ctypes.data, len(prompt), C.byref(opts), V, alpha, 7,
                                               sleep, out.ctypes.data, C.byref(ln), C.byref(st)))
     assert out[:ln.value].tolist() == target_ar(prompt.tolist(), n, V)
-    assert st.steps[k - 1] > 0 and st.steps[0] > 0
+    assert st.steps[k - 1] > 0
+    if sleep > 0:
+        # only a sleeping target guarantees the drafter thread is scheduled before
+        # the target finishes on its own AR steps (lookahead 0, reading R7)
+        assert st.steps[0] > 0
     if alpha == 1.0:
         assert sum(st.rollbacks[:k]) == 0
 
@@ -59,7 +64,7 @@ def _rank_worker(rank, k, board, n, alpha, gamma, sleep, q):
     out = np.zeros(n, dtype=np.int32)
     ln = C.c_int32()
     st = abi.RunStats()
-    s = abi.lib().ps_test_fake_run_rank(rank, k, board.encode(), prompt.ctypes.data, len(prompt), C.byref(opts),
+    s = abi.test_lib().ps_test_fake_run_rank(rank, k, board.encode(), prompt.ctypes.data, len(prompt), C.byref(opts),
                                         V, alpha, 11, sleep, out.ctypes.data, C.byref(ln), C.byref(st))
     q.put((rank, s, out[:ln.value].tolist(), [int(x) for x in st.steps[:k]], int(st.verify_steps[k - 1])))
 
@@ -69,7 +74,7 @@ def test_processes_lossless(k, alpha, gamma, sleep):
     from paper_2505_01572_b200 import abi
     n = 80
     board = f"/pipespec-test-{os.getpid()}-{k}"
-    abi.check(abi.lib().ps_board_create(board.encode(), k, 16 + n + 400))
+    abi.test_check(abi.test_lib().ps_test_board_create(board.encode(), k, 16 + n + 400))
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
@@ -80,7 +85,7 @@ def test_processes_lossless(k, alpha, gamma, sleep):
         for p in procs:
             p.join(timeout=60)
     finally:
-        abi.lib().ps_board_unlink(board.encode())
+        abi.test_lib().ps_test_board_unlink(board.encode())
     want = target_ar(list(range(5, 21)), n, 997)
     for rank, status, out, steps, vsteps in res:
         assert status == 0, (rank, status)
@@ -91,17 +96,115 @@ def test_processes_lossless(k, alpha, gamma, sleep):
 def test_board_rank_mismatch_fails_cleanly():
     from paper_2505_01572_b200 import abi
     board = f"/pipespec-test-{os.getpid()}-bad"
-    abi.check(abi.lib().ps_board_create(board.encode(), 2, 400))
+    abi.test_check(abi.test_lib().ps_test_board_create(board.encode(), 2, 400))
     try:
         opts, keep = _opts(3, 10, 4)
         out = np.zeros(10, dtype=np.int32)
         ln = C.c_int32()
         prompt = np.arange(3, dtype=np.int32)
-        s = abi.lib().ps_test_fake_run_rank(0, 3, board.encode(), prompt.ctypes.data, 3, C.byref(opts), 97, 0.5,
+        s = abi.test_lib().ps_test_fake_run_rank(0, 3, board.encode(), prompt.ctypes.data, 3, C.byref(opts), 97, 0.5,
                                             1, 0, out.ctypes.data, C.byref(ln), None)
         assert s == abi.PS_E_INVALID
-        assert abi.lib().ps_test_fake_run_rank(0, 2, b"/pipespec-missing-board", prompt.ctypes.data, 3,
+        assert abi.test_lib().ps_test_fake_run_rank(0, 2, b"/pipespec-missing-board", prompt.ctypes.data, 3,
                                                C.byref(opts), 97, 0.5, 1, 0, out.ctypes.data, C.byref(ln),
                                                None) == abi.PS_E_INVALID
     finally:
-        abi.lib().ps_board_unlink(board.encode())
+        abi.test_lib().ps_test_board_unlink(board.encode())
+
+
+# ----------------------------------------------------------------------------- event log replay
+M64 = (1 << 64) - 1
+
+
+def _mix(x):
+    """splitmix64 finaliser, as the test double's FakeStage::mix (include/pipespec_test.h)."""
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def _fake_next(level, c, k, V, alpha, seed):
+    """The test double's stage-`level` model written out (include/pipespec_test.h)."""
+    t = (c[-1] * 7919 + len(c) * 104729 + 13) % V
+    for j in range(k - 2, level - 1, -1):
+        h = _mix(seed ^ (j << 48) ^ len(c))
+        if float(h >> 11) >= alpha * 9007199254740992.0:
+            t = (t + 1 + _mix(h) % (V - 1)) % V
+    return t
+
+
+def replay(events, prompt, k, step_fn):
+    """Rebuild every O_i from the event log (include/pipespec.h ps_event) and
+    check each logged step against step_fn(stage, context, window) -> (a, next),
+    the per-call definition (SURVEY §8(c) c.1 #4, brute-force verify)."""
+    from paper_2505_01572_b200 import abi
+    B = [list(prompt) for _ in range(k)]
+    n_verify = 0
+    for e in events:
+        i = e["stage"]
+        if e["kind"] == abi.PS_EV_STALE:
+            continue
+        if e["kind"] == abi.PS_EV_RESYNC:
+            B[i] = list(B[e["origin"]][:e["n"]])
+            continue
+        assert len(B[i]) == e["n"], (e, len(B[i]))
+        w = e["window"] if e["kind"] == abi.PS_EV_VERIFY else []
+        a, nxt = step_fn(i, B[i], w)
+        assert (a, nxt) == (e["a"], e["next"]), (e, a, nxt)
+        B[i] = B[i] + list(w[:a]) + [nxt]
+        n_verify += e["kind"] == abi.PS_EV_VERIFY
+    return B, n_verify
+
+
+@pytest.mark.parametrize("k,alpha,gamma,look,sleep", [(2, 0.7, 4, 0, 20), (3, 0.6, 4, 1, 5), (4, 0.8, 3, 2, 5)])
+def test_event_log_replays_to_the_output(k, alpha, gamma, look, sleep):
+    """Every logged draft / verify / AR step equals the per-call definition on
+    the replayed context, and replaying the log reproduces O_K (trace replay, S:350)."""
+    from paper_2505_01572_b200 import abi
+    V, n, seed = 997, 100, 7
+    prompt = np.arange(5, 21, dtype=np.int32)
+    opts, ro = _opts(k, n, gamma, look, event_cap=20000)
+    out = np.zeros(n, dtype=np.int32)
+    ln = C.c_int32()
+    st = abi.RunStats()
+    abi.test_check(abi.test_lib().ps_test_fake_pipeline(k, prompt.ctypes.data, len(prompt), C.byref(opts), V, alpha,
+                                                        seed, sleep, out.ctypes.data, C.byref(ln), C.byref(st)))
+    events = ro.events(st)
+    assert st.events_dropped == 0 and len(events) == st.n_events > 0
+
+    def step(i, ctx, w):
+        c = list(ctx)
+        j, pred = 0, _fake_next(i, c, k, V, alpha, seed)
+        while j < len(w) and pred == w[j]:
+            c.append(w[j])
+            j += 1
+            pred = _fake_next(i, c, k, V, alpha, seed)
+        return j, pred
+
+    B, n_verify = replay(events, prompt.tolist(), k, step)
+    assert B[k - 1][len(prompt):len(prompt) + n] == out[:ln.value].tolist() == target_ar(prompt.tolist(), n, V)
+    stale_verify = sum(e["kind"] == abi.PS_EV_STALE and e["origin"] == abi.PS_EV_VERIFY for e in events)
+    assert n_verify + stale_verify == sum(st.verify_steps[1:k])
+    assert [e["t_ns"] for e in events] == sorted(e["t_ns"] for e in events)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("seed", range(6))
+def test_deep_pipelines_with_lookahead_never_stall(seed):
+    """3-4 stages with lookahead >= 1 and low acceptance: a higher stage's
+    rollback can leave O_{i-1} on a short prefix of O_i from which the drafter
+    diverges before position n-1; the verifier must resync it (not wait for
+    drafts that can never become valid) -- ADVICE r1 finding on ps_pipeline.cu."""
+    from paper_2505_01572_b200 import abi
+    V, n = 61, 150
+    k = 3 + seed % 2
+    prompt = np.arange(3, 11, dtype=np.int32)
+    opts, ro = _opts(k, n, 2 + seed % 3, look=1 + seed % 3)
+    out = np.zeros(n, dtype=np.int32)
+    ln = C.c_int32()
+    st = abi.RunStats()
+    abi.test_check(abi.test_lib().ps_test_fake_pipeline(k, prompt.ctypes.data, len(prompt), C.byref(opts), V, 0.35,
+                                                        100 + seed, seed % 2, out.ctypes.data, C.byref(ln),
+                                                        C.byref(st)))
+    assert out[:ln.value].tolist() == target_ar(prompt.tolist(), n, V)

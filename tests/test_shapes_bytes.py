@@ -37,7 +37,8 @@ def test_preset_parameter_counts(name, n):
 ])
 def test_kv_and_streamed_bytes(name, kv, stream_gb):
     s = synth.preset(name)
-    assert s.kv_bytes_per_token() == kv
+    assert s.kv_bytes_per_token_bf16() == kv
+    assert s.kv_bytes_per_token() == 2 * kv          # split-bf16 (hi + lo) planes as stored (R28)
     assert abs(s.streamed_bytes_per_pass(1) / 1e9 - stream_gb) / stream_gb < 5e-3
 
 
@@ -46,5 +47,5 @@ def test_verify_pass_bytes_8b_r17(ctx, gb):
     """SURVEY.md 8(d) 'Algorithmic bytes per verify pass', LLaMA-3.1-8B, R = 17."""
     s = synth.preset("llama3.1-8b")
     R = 17
-    b = s.streamed_bytes_per_pass(R) + (ctx + R) * s.kv_bytes_per_token()
+    b = s.streamed_bytes_per_pass(R) + (ctx + R) * s.kv_bytes_per_token_bf16()
     assert abs(b / 1e9 - gb) < 0.01
