@@ -17,7 +17,8 @@ const char* ps_test_last_error(void);
 
 /* out[r][n] = sum_k X[r][k] * W[n][k] for r < R, n < N (fp32), through the
  * production tcgen05 stream-K GEMM kernel with a plain-store epilogue.
- * W: device bf16 [N, K]; X: device bf16 [32, K] (rows >= R ignored);
+ * W: device bf16 [N, K]; X: device bf16 [64, K], the split-bf16 operand
+ * (rows 0..31 hi, rows 32..63 lo; X = hi + lo; rows >= R of each ignored);
  * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
 ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
 

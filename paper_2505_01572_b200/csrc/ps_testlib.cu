@@ -166,7 +166,7 @@ static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_
   const int RP = R <= 16 ? 16 : 32;
   CUtensorMap mW, mX;
   if ((st = make_map(&mW, W, N, K, 128)) != PS_OK) return st;
-  if ((st = make_map(&mX, X, kMaxRows, K, RP)) != PS_OK) return st;
+  if ((st = make_map(&mX, X, 2 * kMaxRows, K, RP)) != PS_OK) return st;   // split operand: hi + lo rows
   GemmShape gs = gemm_shape((N + 127) / 128, K, g_num_sms);
   StepIn hin{};
   hin.R = R;

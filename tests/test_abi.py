@@ -60,8 +60,8 @@ def test_pure_host_calls_without_gpu():
     assert lib.ps_version() >= 100
     s = synth.preset("llama3.1-8b")
     sh = stage.model_shape(s)
-    # 32 layers x 2 x 8 heads x 64 tokens x 128 x 2 bytes per page, 8 pages for 512 tokens
-    assert lib.ps_kv_pool_bytes(ctypes.byref(sh), 512, 64) == 8 * 32 * 2 * 8 * 64 * 128 * 2
+    # 32 layers x 4 planes (K hi/lo, V hi/lo) x 8 heads x 64 tokens x 128 x 2 bytes per page, 8 pages
+    assert lib.ps_kv_pool_bytes(ctypes.byref(sh), 512, 64) == 8 * 32 * 4 * 8 * 64 * 128 * 2
     # invalid arguments are rejected before any device work
     h = ctypes.c_void_p()
     st = lib.ps_stage_create(ctypes.byref(sh), None, None, None, ctypes.byref(h))
