@@ -138,10 +138,18 @@ struct GemmSmem {
   static constexpr int kBytes = kOffMisc + 16 + 1024;               // + alignment slack
 };
 
+// Accumulator of one unit segment: the MMA's N = 2 RP columns hold W·x_hi
+// (columns [0, RP)) and W·x_lo (columns [RP, 2 RP)) of the split operand; the
+// row result is their fp32 sum (fixed order: hi + lo).
 template <int RP>
 PS_DEV void load_acc(uint32_t taddr, float* v) {
+  float lo[RP];
   tmem_ld16(taddr, v);
   if constexpr (RP == 32) tmem_ld16(taddr + 16, v + 16);
+  tmem_ld16(taddr + RP, lo);
+  if constexpr (RP == 32) tmem_ld16(taddr + RP + 16, lo + 16);
+#pragma unroll
+  for (int r = 0; r < RP; ++r) v[r] += lo[r];
 }
 
 // Per-kernel (or per-phase) epilogue preparation: rstd_r from the producer's
@@ -609,8 +617,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
   uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffMisc);
   volatile int* flag = (volatile int*)(smem + L::kOffMisc + 4);
 
-  constexpr int kTmemCols = RP == 16 ? 32 : 64;
-  constexpr uint32_t kIdesc = idesc_bf16_f32<128, RP>();
+  constexpr int kTmemCols = RP == 16 ? 64 : 128;        // 2 accumulators x N = 2 RP columns
+  constexpr uint32_t kIdesc = idesc_bf16_f32<128, 2 * RP>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long U = (long long)p.n_tiles * p.kb_total;
   const int G = gridDim.x, c = blockIdx.x;
@@ -698,7 +706,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         const long long seg_end = min(u_end, (long long)(t + 1) * kbt);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t dcol = tmem + acc * RP;
+        const uint32_t dcol = tmem + acc * 2 * RP;
         for (; u < seg_end; ++u) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -708,11 +716,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
             mbar_arrive(&empty[stage]);
           } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {   // W·x_hi + W·x_lo (split-bf16 operand)
+            for (int k = 0; k < 4; ++k)   // N = 2 RP: the hi and lo rows of the split operand in one MMA
               mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
                        (u != seg_begin || k > 0) ? 1u : 0u);
-              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + RP * 128 + 32 * k), kIdesc, 1u);
-            }
             mma_commit(&empty[stage]);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -743,7 +749,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       float v[RP];
-      load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * RP, v);
+      load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 2 * RP, v);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;

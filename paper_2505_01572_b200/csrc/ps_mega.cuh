@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   MegaPhase* sph = (MegaPhase*)(smem + L::kOffPhase);
   StepIn* sstep = (StepIn*)(smem + L::kOffStep);
 
-  constexpr int kTmemCols = RP == 16 ? 32 : 64;
-  constexpr uint32_t kIdesc = idesc_bf16_f32<128, RP>();
+  constexpr int kTmemCols = RP == 16 ? 64 : 128;        // 2 accumulators x N = 2 RP columns
+  constexpr uint32_t kIdesc = idesc_bf16_f32<128, 2 * RP>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
 
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
 #endif
           first = false;
           tc_fence_after();
-          const uint32_t dcol = tmem + acc * RP;
+          const uint32_t dcol = tmem + acc * 2 * RP;
           for (; u < seg_end; ++u, ++it) {
             const int slot = it % kMegaStages;
             mbar_wait(&full[slot], (it / kMegaStages) & 1);
@@ -257,11 +257,9 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
             const uint32_t a0 = smem_u32(sA + slot * L::kABytes);
             const uint32_t x0 = smem_u32(sX + slot * L::kXBytes);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {   // W·x_hi + W·x_lo (split-bf16 operand)
+            for (int k = 0; k < 4; ++k)   // N = 2 RP: the hi and lo rows of the split operand in one MMA
               mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
                        (u != seg_begin || k > 0) ? 1u : 0u);
-              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + RP * 128 + 32 * k), kIdesc, 1u);
-            }
             mma_commit(&empty[slot]);
           }
           mma_commit(&tfull[acc]);
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
               PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 6);
             }
             float v[RP];
-            load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * RP, v);
+            load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 2 * RP, v);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             ++nacc;

@@ -254,3 +254,107 @@ extern "C" ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int3
   cudaEventDestroy(e1);
   return PS_OK;
 }
+
+// ============================================================================ tcgen05 throughput probe
+// One CTA per SM, one thread issues `iters` units of: mode 0 = 4x tcgen05.cp
+// 128x256b (a 16 KB weight tile smem -> TMEM) + commit; mode 1 = 8 MMAs
+// (M128 N16 K16, A from TMEM) + commit; mode 2 = 8 MMAs with A from smem +
+// commit; mode 3 = copy + MMAs.  Reports ns per unit (the commit of each unit
+// is waited on every `depth` units).
+__global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, int iters, int depth, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  constexpr uint32_t kI = idesc_bf16_f32<128, 16>();
+  if (threadIdx.x == 32) {
+    const unsigned long long t0 = globaltimer();
+    uint32_t ph = 0;
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t a0 = smem_u32(sm + (i & 7) * 16384);
+      const uint32_t x0 = smem_u32(sm + 8 * 16384);
+      const uint32_t ta = tmem + 64 + (i % 14) * 32;
+      if (mode == 0 || mode == 3)
+        for (int k = 0; k < 4; ++k) tmem_cp_128x256b(ta + 8 * k, smem_desc_sw128(a0 + 32 * k));
+      if (mode == 1 || mode == 3)
+        for (int k = 0; k < 4; ++k) {
+          mma_bf16_ts(tmem, ta + 8 * k, smem_desc_sw128(x0 + 32 * k), kI, 1u);
+          mma_bf16_ts(tmem, ta + 8 * k, smem_desc_sw128(x0 + 2048 + 32 * k), kI, 1u);
+        }
+      if (mode == 2)
+        for (int k = 0; k < 4; ++k) {
+          mma_bf16(tmem, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI, 1u);
+          mma_bf16(tmem, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 2048 + 32 * k), kI, 1u);
+        }
+      constexpr uint32_t kI32 = idesc_bf16_f32<128, 32>();
+      if (mode == 4)   // 4 MMAs, N = 32 (hi and lo rows in one B tile), one accumulator
+        for (int k = 0; k < 4; ++k) mma_bf16(tmem, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI32, 1u);
+      if (mode == 5)   // 8 MMAs N = 16, hi -> D0, lo -> D1
+        for (int k = 0; k < 4; ++k) {
+          mma_bf16(tmem, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI, 1u);
+          mma_bf16(tmem + 16, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 2048 + 32 * k), kI, 1u);
+        }
+      if (mode == 6)   // 4 MMAs N = 32, k parity -> D0 / D1
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tmem + (k & 1) * 32, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI32, 1u);
+      if (mode == 7)   // 4 MMAs N = 16 (plain bf16 operand), one accumulator
+        for (int k = 0; k < 4; ++k) mma_bf16(tmem, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI, 1u);
+      if (mode == 8)   // 8 MMAs N = 16, 4 accumulators
+        for (int k = 0; k < 4; ++k) {
+          mma_bf16(tmem + (k & 1) * 32, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI, 1u);
+          mma_bf16(tmem + (k & 1) * 32 + 16, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 2048 + 32 * k), kI, 1u);
+        }
+      // non-swapped orientation: activations as A (M = 128, mostly padding),
+      // weights as B (N = 256 or 128 rows): bytes of WEIGHTS per unit = N * 128
+      constexpr uint32_t kI256 = idesc_bf16_f32<128, 256>();
+      constexpr uint32_t kI128 = idesc_bf16_f32<128, 128>();
+      if (mode == 10)  // weights N = 256 (32 KB per unit), 4 MMAs
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tmem + 256 * (i & 1), smem_desc_sw128(x0 + 32 * k), smem_desc_sw128(smem_u32(sm + (i & 3) * 32768) + 32 * k),
+                   kI256, 1u);
+      if (mode == 11)  // weights N = 128 (16 KB per unit), 4 MMAs
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tmem + 128 * (i & 1), smem_desc_sw128(x0 + 32 * k), smem_desc_sw128(a0 + 32 * k), kI128, 1u);
+      if (mode == 9)   // 4 MMAs N = 32, 4 accumulators (one per k step)
+        for (int k = 0; k < 4; ++k)
+          mma_bf16(tmem + k * 32, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kI32, 1u);
+      if ((i + 1) % depth == 0) {
+        mma_commit(&bar[0]);
+        mbar_wait(&bar[0], ph);
+        ph ^= 1;
+      }
+    }
+    mma_commit(&bar[0]);
+    mbar_wait(&bar[0], ph);
+    out[blockIdx.x] = globaltimer() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+extern "C" ps_status ps_test_tc_probe(int32_t mode, int32_t iters, int32_t depth, double* ns_per_unit) {
+  const int smem = 9 * 16384 + 1024;
+  CU_TRY(cudaFuncSetAttribute(tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int dev = 0, sms = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  CU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  unsigned long long* d;
+  CU_TRY(cudaMalloc(&d, sms * 8));
+  tc_probe_kernel<<<sms, 128, smem>>>(mode, iters, depth, d);
+  CU_TRY(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(sms);
+  CU_TRY(cudaMemcpy(h.data(), d, sms * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  double m = 0;
+  for (auto v : h) m = std::max(m, (double)v);
+  *ns_per_unit = m / iters;
+  return PS_OK;
+}
