@@ -406,10 +406,6 @@ def main():
     pass_gbs = pass_bytes / (pass_ms * 1e-3) / 1e9
     draft_bytes = ds.streamed_bytes_per_pass(1) + (ctx + 1) * ds.kv_bytes_per_token()
     draft_gbs = draft_bytes / (draft_ms * 1e-3) / 1e9
-    # the standalone gate/up GEMM of one M_1 layer (same tcgen05 mainloop), for reference
-    n_it = ts.n_layers
-    gu_ms = sum(target.time_kernel(4, l % ts.n_layers, 1) for l in range(n_it)) / n_it
-    gu_bytes = 2 * ts.d_ffn * ts.d_model * 2 + R * ts.d_model * 2 + R * ts.d_ffn * 2
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -470,8 +466,6 @@ def main():
                      "bound": "hbm", "achieved": pass_gbs, "peak": peak, "unit": "GB/s", "frac": pass_gbs / peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": pass_bytes, "rows": R,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
-        "gate_up_gemm_standalone": {"ms": gu_ms, "GB/s": gu_bytes / (gu_ms * 1e-3) / 1e9,
-                                    "frac": gu_bytes / (gu_ms * 1e-3) / 1e9 / peak},
         "e2e": {"value": e2e, "unit": "tokens/s",
                 "h2d_bytes_per_step": fwd_per_step * STEP_IN_BYTES + g * 4,
                 "d2h_bytes_per_step": fwd_per_step * STEP_OUT_BYTES},

@@ -117,9 +117,10 @@ typedef struct ps_stage_opts {
   void* kv_pool;
   int64_t kv_pool_bytes;
   void* stream;
-  int32_t use_graphs;       /* 1: capture one CUDA graph per rows bucket      */
-  int32_t use_megakernel;   /* 1: whole forward as one persistent cooperative
-                               kernel (ps_mega.cuh); 0: one kernel per step   */
+  int32_t use_graphs;       /* ignored (kept for layout stability): a forward
+                               is ONE persistent kernel launch               */
+  int32_t use_megakernel;   /* must be 1: the whole forward as one persistent
+                               cooperative kernel (ps_mega.cuh)              */
   int32_t max_ctas;         /* megakernel CTAs (one per SM), 0 = every SM; a
                                smaller grid leaves SMs to concurrent stages  */
 } ps_stage_opts;
@@ -348,14 +349,7 @@ ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const c
  * launched (graph launches count their kernels) since process start. */
 int64_t ps_kernel_launch_count(void);
 
-/* Per-kernel timing (measurement only): re-launch one kernel of the stage's
- * most recent forward configuration (same rows bucket, same device StepIn)
- * through the one-kernel-per-step path, `iters` times back to back on the
- * stage stream; *avg_ms = CUDA-event time per launch.  kind: 0 embed, 1 QKV
- * GEMM, 2 attention, 3 O GEMM, 4 gate/up GEMM, 5 down GEMM, 6 lm_head GEMM,
- * 7 argmax/scan; layer selects the weights.  Overwrites the stage's scratch
- * activations (not its token buffer or KV below kv_len). */
-ps_status ps_time_kernel(ps_stage* stage, int32_t kind, int32_t layer, int32_t iters, double* avg_ms);
+
 
 #ifdef __cplusplus
 }

@@ -1,7 +1,7 @@
 /*
  * pipespec_test.h — TEST library of the pipespec project (libpipespec_test.so,
  * built from csrc/ps_testlib.cu; never loaded by the product path).  It holds
- * the test double of the async runtime's protocol and single-kernel probes;
+ * the test double of the async runtime's protocol and hardware probes;
  * the product library libpipespec.so exports none of these.  Errors of this
  * library are read with ps_test_last_error.
  */
@@ -15,22 +15,17 @@ extern "C" {
 
 const char* ps_test_last_error(void);
 
-/* out[r][n] = sum_k X[r][k] * W[n][k] for r < R, n < N (fp32), through the
- * production tcgen05 stream-K GEMM kernel with a plain-store epilogue.
- * W: device bf16 [N, K]; X: device bf16 [64, K], the split-bf16 operand
- * (rows 0..31 hi, rows 32..63 lo; X = hi + lo; rows >= R of each ignored);
- * out: device float [R, N]; K % 64 == 0; 1 <= R <= 32.  Synchronises stream. */
-ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R, void* stream);
-
-/* As ps_test_gemm, then `iters` timed launches: *avg_ms = CUDA-event time per
- * launch.  test_mode: bit0 skip the TMA loads, bit1 skip the MMAs (probes of
- * the pipeline's own overhead). */
-ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                             void* stream, int32_t iters, int32_t test_mode, float* avg_ms);
-
 /* Launch-overhead probe: an empty kernel with `smem` bytes of dynamic shared
  * memory, `iters` back-to-back launches; *avg_ms per launch. */
 ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, int32_t iters, float* avg_ms);
+
+/* tcgen05 throughput probe (scripts/tc_probe.py): one CTA per SM, one thread
+ * issues `iters` units of a mode (0: tcgen05.cp of a 16 KB tile to TMEM;
+ * 1/2: 8 MMAs M128 N16 K16 with A in TMEM / smem; 3: copy + MMAs; 4-9: N and
+ * accumulator-chain variants of the swap-AB orientation; 10/11: weights as
+ * the B operand, N = 256 / 128), committing every `depth` units; writes the
+ * slowest SM's ns per unit. */
+ps_status ps_test_tc_probe(int32_t mode, int32_t iters, int32_t depth, double* ns_per_unit);
 
 /* Protocol test double of the async runtime (no GPU): k stages over a
  * closed-form host "model" -- stage k-1 emits next(c) = (c[-1]*7919 +

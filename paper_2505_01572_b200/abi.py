@@ -121,7 +121,6 @@ _PROTOS = {
     "ps_board_unlink": (C.c_int32, [C.c_char_p]),
     "ps_pipeline_run_rank": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_void_p, C.c_int32,
                                          C.POINTER(RunOpts), C.c_void_p, _I32P, C.POINTER(RunStats)]),
-    "ps_time_kernel": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
 }
 
 # libpipespec_test.so (include/pipespec_test.h): test infrastructure, never
@@ -136,11 +135,8 @@ _TEST_PROTOS = {
                                           C.c_void_p, _I32P, C.POINTER(RunStats)]),
     "ps_test_board_create": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32]),
     "ps_test_board_unlink": (C.c_int32, [C.c_char_p]),
-    "ps_test_gemm_timed": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                                       C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "ps_test_launch_overhead": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
-    "ps_test_gemm": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                                 C.c_void_p]),
+    "ps_test_tc_probe": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
 }
 # trace build only (PS_LIB=.../libpipespec_trace.so)
 _TRACE_PROTOS = {"ps_trace_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64])}

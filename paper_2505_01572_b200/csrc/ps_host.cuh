@@ -1,6 +1,6 @@
 // ps_host.cuh — host helpers shared by the product library (ps_stage.cu) and
 // the test library (ps_testlib.cu): errors, TMA descriptors, stream-K
-// partitions and the per-step GEMM launch.  Internal; not part of the ABI.
+// partitions, device setup.  Internal; not part of the ABI.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -57,17 +57,7 @@ static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64
 }
 
 // ============================================================================ GEMM launch
-constexpr int kStages = 4;   // x (16 KB weights + RP*128 B activations): 2 CTAs/SM
 static int g_num_sms = 0;
-
-// Kernel attributes are per device (per context): set them on every device a
-// stage is created on (cheap; idempotent).
-template <int RP, bool GU>
-static ps_status gemm_setup_attr() {
-  CU_TRY(cudaFuncSetAttribute(gemm_kernel<RP, kStages, GU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              GemmSmem<RP, kStages, GU>::kBytes));
-  return PS_OK;
-}
 
 struct GemmShape {
   int n_tiles, kb_total, grid, maxseg;
@@ -100,54 +90,6 @@ static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) 
   return g;
 }
 
-static ps_status launch_gemm(int RP, bool GU, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& a2,
-                             const CUtensorMap& x, const GemmParams& p, int grid, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e;
-  if (RP == 16 && !GU) {
-    cfg.dynamicSmemBytes = GemmSmem<16, kStages, false>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, false>, a0, a1, a2, x, p);
-  } else if (RP == 16) {
-    cfg.dynamicSmemBytes = GemmSmem<16, kStages, true>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<16, kStages, true>, a0, a1, a2, x, p);
-  } else if (!GU) {
-    cfg.dynamicSmemBytes = GemmSmem<32, kStages, false>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, false>, a0, a1, a2, x, p);
-  } else {
-    cfg.dynamicSmemBytes = GemmSmem<32, kStages, true>::kBytes;
-    e = cudaLaunchKernelEx(&cfg, gemm_kernel<32, kStages, true>, a0, a1, a2, x, p);
-  }
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
-  g_launches++;
-  return PS_OK;
-}
-
-template <typename K, typename P>
-static ps_status launch_simple(K kernel, dim3 grid, dim3 block, size_t smem, const P& params, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, params);
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-  g_launches++;
-  return PS_OK;
-}
-
 static ps_status init_device_globals(int device) {
   CU_TRY(cudaSetDevice(device));
   int major = 0, minor = 0;
@@ -158,12 +100,6 @@ static ps_status init_device_globals(int device) {
   CU_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device));
   ps_status st;
   if ((st = get_encoder()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<16, false>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<16, true>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<32, false>()) != PS_OK) return st;
-  if ((st = gemm_setup_attr<32, true>()) != PS_OK) return st;
-  CU_TRY(cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-  CU_TRY(cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
   return PS_OK;
 }
 

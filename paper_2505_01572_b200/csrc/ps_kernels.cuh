@@ -1,21 +1,20 @@
-// ps_kernels.cuh — the verify-pass kernels (sm_100a).
+// ps_kernels.cuh — the device functions of the verify pass (sm_100a), run as
+// the phases of the persistent megakernel (ps_mega.cuh):
 //
-//   embed_kernel        a1+a2+a3: window rows -> x (fp32 residual), x∘g (bf16 GEMM
-//                        operand) and per-128-column sum-of-squares slots
-//   gemm_kernel         a4/a7/a8/a9/a10: persistent stream-K skinny GEMM on tcgen05
-//                        (swap-AB: weights are the M=128 side, the R<=32 rows the
-//                        N side), TMA-staged weights with a STAGES-deep mbarrier
-//                        ring, TMEM accumulators double-buffered, fused epilogues:
+//   embed_row           a1+a2+a3: window rows -> x (fp32 residual), x∘g (split-bf16
+//                        GEMM operand) and per-128-column sum-of-squares slots
+//   GEMM phases         a4/a7/a8/a9/a10: stream-K skinny GEMM on tcgen05 (the
+//                        mainloop lives in ps_mega.cuh), fused epilogues:
 //                          EPI_QKV    RMSNorm row scale + RoPE + paged KV append (a3,a5)
 //                          EPI_RESID  residual add + next RMSNorm operand + sumsq (a7,a9)
 //                          EPI_SWIGLU RMSNorm row scale + SiLU(gate)*up           (a8)
 //                          EPI_LMHEAD final-norm scale + fp32 logits (on request)
 //                                     + per-row greedy key by atomicMax       (a10)
 //                          EPI_STORE  plain fp32 store (unit tests)
-//   attn_kernel         a6: split-KV decode attention over the paged KV cache,
+//   attn_run            a6: split-KV decode attention over the paged KV cache,
 //                        fixed 64-key chunks at absolute positions, causal inside the
 //                        window, GQA; deterministic last-CTA combine
-//   argmax_scan_kernel  a11 (+a13 data): vocab argmax from the partials, synthetic
+//   argmax_run          a11 (+a13 data): vocab argmax from the partials, synthetic
 //                        override (benchmarks), draft compare, first-mismatch scan
 //
 // RMSNorm is applied as a deferred row scale: the producer of x writes the bf16
@@ -66,7 +65,7 @@ struct StepIn {                    // written by the host before every forward
 constexpr int kFlagLogits = 1;
 constexpr int kFlagSynth = 2;
 
-struct StepOut {                   // written by argmax_scan_kernel (== ps_verify_result)
+struct StepOut {                   // written by argmax_run (== ps_verify_result)
   int32_t a, next, R, kv_len;      // R = -1: a row token was out of range (nothing committed)
   int32_t pred[kMaxRows];
 };
@@ -122,21 +121,6 @@ struct GemmParams {
 // (tile, k-block) pairs in tile-major order.
 PS_DEV long long sk_begin(long long U, int G, int c) { return U * c / G; }
 PS_DEV int sk_owner(long long U, int G, long long u) { return (int)(((u + 1) * G - 1) / U); }
-
-template <int RP, int STAGES, bool GU>
-struct GemmSmem {
-  static constexpr int kABytes = 128 * 64 * 2;      // 16 KB weight tile (128 rows x 64 K)
-  static constexpr int kXBytes = 2 * RP * 64 * 2;   // activation tiles: hi then lo (RP rows x 64 K each)
-  static constexpr int kScratch = 128 * (RP + 1) * 4;
-  static constexpr int kOffX = STAGES * kABytes;
-  static constexpr int kOffScratch = kOffX + STAGES * kXBytes;
-  static constexpr int kOffRed = kOffScratch + kScratch;            // u64 [4][RP]
-  static constexpr int kOffRstd = kOffRed + 4 * RP * 8;             // float [RP]
-  static constexpr int kOffKvRow = kOffRstd + RP * 4;               // long long [RP]
-  static constexpr int kOffBar = kOffKvRow + RP * 8;                // full, empty, tfull[2], tempty[2]
-  static constexpr int kOffMisc = kOffBar + (2 * STAGES + 4) * 8;   // tmem base, flag
-  static constexpr int kBytes = kOffMisc + 16 + 1024;               // + alignment slack
-};
 
 // Accumulator of one unit segment: the MMA's N = 2 RP columns hold W·x_hi
 // (columns [0, RP)) and W·x_lo (columns [RP, 2 RP)) of the split operand; the
@@ -589,184 +573,6 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
   return finalized;   // this CTA completed tile t (its outputs are written)
 }
 
-// 192 threads: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-5
-// epilogue (TMEM lane quarter = warp % 4).  <= ~110 KB smem and <= 170 regs so
-// two CTAs fit per SM: under programmatic dependent launch the next kernel's
-// CTA becomes resident beside this one and streams its first weight tiles
-// while this kernel's tail (stream-K fixup, epilogue) is still running.
-constexpr int kGemmThreads = 192;
-
-template <int RP, int STAGES, bool GU>
-__global__ void __launch_bounds__(kGemmThreads, 2)
-gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
-            const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mX,
-            const __grid_constant__ GemmParams p) {
-  using L = GemmSmem<RP, STAGES, GU>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sX = smem + L::kOffX;
-  float* scratch = (float*)(smem + L::kOffScratch);
-  unsigned long long* red = (unsigned long long*)(smem + L::kOffRed);
-  float* rstd = (float*)(smem + L::kOffRstd);
-  long long* kvrow = (long long*)(smem + L::kOffKvRow);
-  uint64_t* full = (uint64_t*)(smem + L::kOffBar);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(smem + L::kOffMisc);
-  volatile int* flag = (volatile int*)(smem + L::kOffMisc + 4);
-
-  constexpr int kTmemCols = RP == 16 ? 64 : 128;        // 2 accumulators x N = 2 RP columns
-  constexpr uint32_t kIdesc = idesc_bf16_f32<128, 2 * RP>();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long U = (long long)p.n_tiles * p.kb_total;
-  const int G = gridDim.x, c = blockIdx.x;
-  const long long u_begin = sk_begin(U, G, c), u_end = sk_begin(U, G, c + 1);
-  const int kbt = p.kb_total;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&mA0);
-    if (GU || p.mode == EPI_QKV) tma_prefetch_desc(&mA1);
-    if (p.mode == EPI_QKV) tma_prefetch_desc(&mA2);
-    tma_prefetch_desc(&mX);
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_launch_dependents();
-  if (threadIdx.x == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
-
-  if (warp == 0) {
-    // ================= TMA producer =================
-    if (lane == 0) {
-      auto load_A = [&](long long u, int s) {
-        const int t = (int)(u / kbt), kb = (int)(u % kbt);
-        uint8_t* dst = sA + s * L::kABytes;
-        if constexpr (GU) {
-          tma_load_2d(dst, &mA0, &full[s], kb * 64, t * 64, kEvictFirst);
-          tma_load_2d(dst + 64 * 128, &mA1, &full[s], kb * 64, t * 64, kEvictFirst);
-        } else if (p.mode == EPI_QKV) {
-          if (t < p.t1) tma_load_2d(dst, &mA0, &full[s], kb * 64, t * 128, kEvictFirst);
-          else if (t < p.t2) tma_load_2d(dst, &mA1, &full[s], kb * 64, (t - p.t1) * 128, kEvictFirst);
-          else tma_load_2d(dst, &mA2, &full[s], kb * 64, (t - p.t2) * 128, kEvictFirst);
-        } else {
-          tma_load_2d(dst, &mA0, &full[s], kb * 64, t * 128, kEvictFirst);
-        }
-      };
-      auto load_X = [&](long long u, int s) {     // hi rows [0, RP), lo rows [kMaxRows, kMaxRows + RP)
-        const int kb = (int)(u % kbt);
-        tma_load_2d(sX + s * L::kXBytes, &mX, &full[s], kb * 64, 0, kEvictLast);
-        tma_load_2d(sX + s * L::kXBytes + RP * 128, &mX, &full[s], kb * 64, kMaxRows, kEvictLast);
-      };
-      const long long n_units = u_end - u_begin;
-      const int pre = (int)(n_units < STAGES ? n_units : STAGES);
-      // Weights do not depend on the previous kernel: stream them before the
-      // grid dependency resolves (PDL), then fetch the activation tiles.
-      const bool no_tma = p.test_mode & 1;
-      for (int i = 0; i < pre; ++i) {
-        if (no_tma) { mbar_arrive(&full[i]); continue; }
-        mbar_arrive_expect_tx(&full[i], L::kABytes + L::kXBytes);
-        load_A(u_begin + i, i);
-      }
-      pdl_wait();
-      if (!no_tma)
-        for (int i = 0; i < pre; ++i) load_X(u_begin + i, i);
-      int stage = 0;
-      uint32_t phase = 1;   // ring wrapped once by the prologue (if pre == STAGES)
-      for (long long u = u_begin + pre; u < u_end; ++u) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (no_tma) {
-          mbar_arrive(&full[stage]);
-        } else {
-          mbar_arrive_expect_tx(&full[stage], L::kABytes + L::kXBytes);
-          load_A(u, stage);
-          load_X(u, stage);
-        }
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      PS_TRACE_STAMP(p.dbg, c * 4 + 1);
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      long long u = u_begin;
-      while (u < u_end) {
-        const int t = (int)(u / kbt);
-        const long long seg_begin = u;
-        const long long seg_end = min(u_end, (long long)(t + 1) * kbt);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tmem + acc * 2 * RP;
-        for (; u < seg_end; ++u) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * L::kABytes);
-          const uint32_t x0 = smem_u32(sX + stage * L::kXBytes);
-          if (p.test_mode & 2) {
-            mbar_arrive(&empty[stage]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)   // N = 2 RP: the hi and lo rows of the split operand in one MMA
-              mma_bf16(dcol, smem_desc_sw128(a0 + 32 * k), smem_desc_sw128(x0 + 32 * k), kIdesc,
-                       (u != seg_begin || k > 0) ? 1u : 0u);
-            mma_commit(&empty[stage]);
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        if (p.test_mode & 2) mbar_arrive(&tfull[acc]);
-        else mma_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
-      PS_TRACE_STAMP(p.dbg, c * 4 + 2);
-    }
-  } else {
-    // ================= epilogue (128 threads, TMEM lane = e) =================
-    const int quarter = warp & 3;
-    const int e = quarter * 32 + lane;
-    pdl_wait();
-    const StepIn* st = p.step;
-    const int R = st->R;
-    const int pos0 = st->pos0;
-    epi_prepare<RP>(p, e, R, pos0, scratch, rstd, kvrow);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    long long u = u_begin;
-    while (u < u_end) {
-      const int t = (int)(u / kbt);
-      const long long seg_begin = u;
-      const long long seg_end = min(u_end, (long long)(t + 1) * kbt);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      float v[RP];
-      load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 2 * RP, v);
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-      u = seg_end;
-
-      epi_segment<RP>(p, t, seg_begin, seg_end, U, G, c, kbt, v, e, lane, quarter, R, pos0, scratch, red, rstd,
-                      kvrow, flag);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 3);
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
-}
-
 // ------------------------------------------------------------------ embed (a1-a3)
 struct EmbedParams {
   const StepIn* step;
@@ -828,14 +634,6 @@ PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
     sq += __shfl_xor_sync(0xffffffffu, sq, 2);
     if (ok && (tid & 3) == 0) p.ss[(size_t)r * p.ss_ld + col / 128] = sq;
   }
-}
-
-__global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ EmbedParams p) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int r = blockIdx.x;
-  if (r >= p.step->R) return;
-  embed_row(p, r, threadIdx.x);
 }
 
 // ------------------------------------------------------------------ tensor-parallel reduce (a14)
@@ -1255,14 +1053,6 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
   }
 }
 
-template <int HD>
-__global__ void __launch_bounds__(256) attn_kernel(const __grid_constant__ AttnParams p) {
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  pdl_wait();
-  pdl_launch_dependents();
-  attn_run<HD, 8>(p, attn_smem, threadIdx.x, blockIdx.x, gridDim.x, 0);
-}
-
 // ------------------------------------------------------------------ argmax + compare + scan (a11)
 struct ArgmaxParams {
   const StepIn* step;
@@ -1365,13 +1155,6 @@ PS_DEV void argmax_run(const ArgmaxParams& p, int tid, int* s_pred, int bar) {
       }
     }
   }
-}
-
-__global__ void __launch_bounds__(1024) argmax_scan_kernel(const __grid_constant__ ArgmaxParams p) {
-  __shared__ int s_pred[kMaxRows];
-  pdl_wait();
-  pdl_launch_dependents();
-  argmax_run<1024>(p, threadIdx.x, s_pred, 0);
 }
 
 }  // namespace ps

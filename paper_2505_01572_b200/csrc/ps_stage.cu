@@ -1,7 +1,7 @@
 // ps_stage.cu — host side of the verify hot path: stage state (token buffer O_i,
 // paged-KV page table and free list), TMA descriptors over the borrowed
-// weights, the per-forward kernel sequence (PDL-chained, captured into one CUDA
-// graph per rows bucket) and the C ABI of include/pipespec.h.
+// weights, the megakernel's phase tables (one persistent launch per forward)
+// and the C ABI of include/pipespec.h.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -44,7 +44,6 @@ struct ps_stage {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int max_seq = 0, max_window = 0, page_size = 0;
-  bool use_graphs = true;
   // weights (borrowed)
   const __nv_bfloat16* embed = nullptr;
   const __nv_bfloat16* lm_head = nullptr;
@@ -72,7 +71,6 @@ struct ps_stage {
   double last_fwd_ms = 0, sum_fwd_ms = 0;
   long long n_fwd = 0;
   // megakernel: phase tables per (bucket, with_head), device tensor maps, counters
-  bool use_mega = true;
   MegaPhase* mega_ph[4] = {nullptr, nullptr, nullptr, nullptr};
   CUtensorMap* mega_maps[4] = {nullptr, nullptr, nullptr, nullptr};
   int mega_n[4] = {0, 0, 0, 0};
@@ -114,9 +112,6 @@ struct ps_stage {
   int ss_ld = 0, xg_ld = 0, max_chunks = 0, max_rb = 0, attn_grid = 0;
   GemmShape gs_qkv, gs_o, gs_gu, gs_d, gs_lm;
   int lm_tiles = 0;
-  // graphs per (bucket, with_head)
-  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  int kernels_per_fwd[2] = {0, 0};
   // token buffer O_i
   std::vector<int32_t> tokens;
   long long kv_len = 0;
@@ -190,7 +185,7 @@ struct HostMaps {
 };
 
 // Parameters of one step of the forward (rows bucket b, layer l) -- shared by
-// the per-kernel path (launch_one) and the megakernel phase table.
+// the megakernel phase table.
 static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostMaps& hm) {
   const ps_model_shape& sh = S->sh;
   const int d = sh.d_model, hq = sh.n_heads * sh.head_dim, hkv = sh.n_kv_heads * sh.head_dim;
@@ -304,36 +299,6 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       }
       return;
     }
-  }
-}
-
-static int gemm_grid(const ps_stage* S, int kind) {
-  switch (kind) {
-    case K_QKV: return S->gs_qkv.grid;
-    case K_O: return S->gs_o.grid;
-    case K_GU: return S->gs_gu.grid;
-    case K_DOWN: return S->gs_d.grid;
-    default: return S->gs_lm.grid;
-  }
-}
-
-// Launch one kernel of the forward for rows bucket b (layer l where relevant).
-static ps_status launch_one(ps_stage* S, int b, int kind, int l) {
-  MegaPhase P;
-  HostMaps hm;
-  build_phase(S, b, kind, l, P, hm);
-  const int RP = bucket_rp(b);
-  switch (P.kind) {
-    case PH_EMBED:
-      return launch_simple(embed_kernel, dim3(RP), dim3(128), 0, P.em, S->stream);
-    case PH_ATTN:
-      if (S->sh.head_dim == 128)
-        return launch_simple(attn_kernel<128>, dim3(S->attn_grid), dim3(256), kAttnSmem, P.a, S->stream);
-      return launch_simple(attn_kernel<64>, dim3(S->attn_grid), dim3(256), kAttnSmem, P.a, S->stream);
-    case PH_ARGMAX:
-      return launch_simple(argmax_scan_kernel, dim3(1), dim3(1024), 0, P.am, S->stream);
-    default:
-      return launch_gemm(RP, P.gu != 0, *hm.a0, *hm.a1, *hm.a2, *hm.x, P.g, gemm_grid(S, kind), S->stream);
   }
 }
 
@@ -465,48 +430,6 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   return PS_OK;
 }
 
-// Enqueue one forward over StepIn rows (already uploaded): embed, L x {QKV,
-// attention, O, gate/up, down}, then (with_head) lm_head + argmax/scan.
-// Consecutive kernels are chained with programmatic dependent launch.
-static ps_status enqueue_forward(ps_stage* S, int b, bool with_head) {
-  ps_status st;
-  int nk = 0;
-  if ((st = launch_one(S, b, K_EMBED, 0)) != PS_OK) return st;
-  ++nk;
-  for (int l = 0; l < S->sh.n_layers; ++l)
-    for (int kind = K_QKV; kind <= K_DOWN; ++kind) {
-      if ((st = launch_one(S, b, kind, l)) != PS_OK) return st;
-      ++nk;
-    }
-  if (with_head) {
-    if ((st = launch_one(S, b, K_LMHEAD, 0)) != PS_OK) return st;
-    if ((st = launch_one(S, b, K_ARGMAX, 0)) != PS_OK) return st;
-    nk += 2;
-  }
-  S->kernels_per_fwd[with_head ? 1 : 0] = nk;
-  return PS_OK;
-}
-
-static ps_status run_forward_kernels(ps_stage* S, int b, bool with_head) {
-  if (!S->use_graphs) return enqueue_forward(S, b, with_head);
-  cudaGraphExec_t& ge = S->graph[b][with_head ? 1 : 0];
-  if (!ge) {
-    cudaGraph_t g;
-    CU_TRY(cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal));
-    long long before = g_launches.load();
-    ps_status st = enqueue_forward(S, b, with_head);
-    cudaError_t e = cudaStreamEndCapture(S->stream, &g);
-    g_launches.store(before);
-    if (st != PS_OK) return st;
-    if (e != cudaSuccess) return fail(PS_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
-    CU_TRY(cudaGraphInstantiate(&ge, g, 0));
-    cudaGraphDestroy(g);
-  }
-  CU_TRY(cudaGraphLaunch(ge, S->stream));
-  g_launches += S->kernels_per_fwd[with_head ? 1 : 0];
-  return PS_OK;
-}
-
 // ---------------------------------------------------------------- paging
 // Mapped logical pages always form a prefix [0, n_mapped) of the page table:
 // ensure_pages extends it, free_pages_from cuts it.
@@ -573,9 +496,6 @@ ps_status ps_stage_destroy(ps_stage* S) {
   if (!S) return PS_OK;
   cudaSetDevice(S->device);
   if (S->stream) cudaStreamSynchronize(S->stream);
-  for (auto& gb : S->graph)
-    for (auto& g : gb)
-      if (g) cudaGraphExecDestroy(g);
   for (int k = 0; k < 4; ++k) {
     if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
     if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
@@ -734,7 +654,6 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
         shape->d_model % 128)
       return fail(PS_E_INVALID, "tensor parallel needs heads, kv_heads, vocab divisible by tp, d_ffn by 64*tp, "
                                 "d_model by 128");
-    if (!o || !o->use_megakernel) return fail(PS_E_INVALID, "tensor parallel needs use_megakernel = 1");
   }
   if (o && o->max_ctas < 0) return fail(PS_E_INVALID, "max_ctas must be >= 0");
   if (o->max_seq < 2) return fail(PS_E_INVALID, "max_seq must be >= 2");
@@ -783,8 +702,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->max_seq = o->max_seq;
   S->max_window = o->max_window;
   S->page_size = o->page_size;
-  S->use_graphs = o->use_graphs != 0;
-  S->use_mega = o->use_megakernel != 0;
+  if (!o->use_megakernel) return bail(fail(PS_E_INVALID, "use_megakernel must be 1 (the only forward path)"));
   if (o->stream) {
     S->stream = (cudaStream_t)o->stream;
   } else {
@@ -921,7 +839,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemcpy(S->d_syn, &S->h_syn, sizeof(SynthParams), cudaMemcpyHostToDevice));
   S_TRY(cudaStreamSynchronize(S->stream));
   // phase tables now (tensor-parallel groups build theirs at connect time)
-  if (tp == 1 && S->use_mega) P_TRY(build_all_tables(S));
+  if (tp == 1) P_TRY(build_all_tables(S));
   *out = S;
 #undef S_TRY
 #undef P_TRY
@@ -973,7 +891,7 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   CU_TRY(cudaEventRecord(S->in_ev[S->in_slot], S->stream));
   S->in_slot = (S->in_slot + 1) % 8;
   if (with_head) CU_TRY(cudaEventRecord(S->fwd_ev[0], S->stream));
-  st = S->use_mega ? launch_mega(S, b, with_head) : run_forward_kernels(S, b, with_head);
+  st = launch_mega(S, b, with_head);
   if (st != PS_OK) return st;
   S->gen = gen;                        // the forward is enqueued: commit the counters
   S->gen_head = gen_head;
@@ -1211,7 +1129,7 @@ ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
   info->kv_len = S->kv_len;
   info->pages_in_use = pages_in_use(S);
   info->pages_total = S->pages_total;
-  info->launches_per_verify = S->use_mega ? 1 : 1 + 5LL * S->sh.n_layers + 2;
+  info->launches_per_verify = 1;   // one persistent megakernel per forward
   info->rows_buckets[0] = 16;
   info->rows_buckets[1] = 32;
   info->last_fwd_ms = S->last_fwd_ms;
@@ -1270,30 +1188,6 @@ ps_status ps_set_synthetic(ps_stage* S, const int32_t* Sv, int32_t len_S, int32_
 }
 
 }  // extern "C"
-
-// ============================================================================ measurement / trace hooks
-extern "C" ps_status ps_time_kernel(ps_stage* S, int32_t kind, int32_t layer, int32_t iters, double* avg_ms) {
-  if (!S || !avg_ms || iters < 1) return fail(PS_E_INVALID, "bad arguments");
-  PS_NOT_INFLIGHT(S);
-  if (kind < K_EMBED || kind > K_ARGMAX) return fail(PS_E_INVALID, "unknown kernel kind %d", kind);
-  if (layer < 0 || (S->sh.n_layers > 0 && layer >= S->sh.n_layers)) return fail(PS_E_INVALID, "bad layer");
-  CU_TRY(cudaSetDevice(S->device));
-  cudaEvent_t e0, e1;
-  CU_TRY(cudaEventCreate(&e0));
-  CU_TRY(cudaEventCreate(&e1));
-  ps_status st = PS_OK;
-  CU_TRY(cudaEventRecord(e0, S->stream));
-  for (int i = 0; i < iters && st == PS_OK; ++i) st = launch_one(S, S->last_bucket, kind, layer);
-  CU_TRY(cudaEventRecord(e1, S->stream));
-  CU_TRY(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (st != PS_OK) return st;
-  *avg_ms = ms / iters;
-  return PS_OK;
-}
 
 #if PS_TRACE
 extern "C" ps_status ps_trace_read(ps_stage* S, int32_t which, void* dst, int64_t bytes) {

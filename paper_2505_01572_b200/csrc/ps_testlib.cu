@@ -4,7 +4,8 @@
 //    code as the product runtime (ps_board.h), so the async protocol --
 //    threads and processes, rollbacks, epochs, the event log -- is testable
 //    without a GPU;
-//  * single-kernel probes of the production GEMM kernel (ps_kernels.cuh).
+//  * microbenchmarks of the hardware paths the kernels are built from
+//    (launch overhead, tcgen05 copy / MMA throughput).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -155,82 +156,6 @@ extern "C" ps_status ps_test_fake_pipeline(int32_t k, const int32_t* prompt, int
 }
 
 // ============================================================================ single-kernel probes
-static ps_status test_gemm_impl(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                void* stream, int iters, int test_mode, float* ms_out) {
-  ps_status st;
-  if (R < 1 || R > kMaxRows || K % 64 || N < 1) return fail(PS_E_INVALID, "bad test gemm shape");
-  int dev = 0;
-  CU_TRY(cudaGetDevice(&dev));
-  if ((st = init_device_globals(dev)) != PS_OK) return st;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int RP = R <= 16 ? 16 : 32;
-  CUtensorMap mW, mX;
-  if ((st = make_map(&mW, W, N, K, 128)) != PS_OK) return st;
-  if ((st = make_map(&mX, X, 2 * kMaxRows, K, RP)) != PS_OK) return st;   // split operand: hi + lo rows
-  GemmShape gs = gemm_shape((N + 127) / 128, K, g_num_sms);
-  StepIn hin{};
-  hin.R = R;
-  StepIn* din;
-  float* ws;
-  unsigned* cnt;
-  const size_t ws_bytes = (size_t)gs.n_tiles * gs.maxseg * kMaxRows * 128 * 8;
-  CU_TRY(cudaMalloc(&din, sizeof(StepIn)));
-  CU_TRY(cudaMalloc(&ws, ws_bytes));
-  CU_TRY(cudaMemset(ws, 0, ws_bytes));
-  CU_TRY(cudaMalloc(&cnt, (size_t)gs.n_tiles * 4));
-  CU_TRY(cudaMemset(cnt, 0, (size_t)gs.n_tiles * 4));
-  GemmParams p = {};
-  p.mode = EPI_STORE;
-  p.N = N;
-  p.n_tiles = gs.n_tiles;
-  p.kb_total = gs.kb_total;
-  p.maxseg = gs.maxseg;
-  p.grid = gs.grid;
-  p.step = din;
-  p.out = out;
-  p.ld_out = N;
-  p.ws = ws;
-  p.counters = cnt;
-  p.ll = 1;
-  p.test_mode = test_mode;
-  cudaEvent_t e0, e1;
-  CU_TRY(cudaEventCreate(&e0));
-  CU_TRY(cudaEventCreate(&e1));
-  // every launch is a new "forward" (distinct LL flag generation)
-  hin.gen = 1;
-  CU_TRY(cudaMemcpy(din, &hin, sizeof hin, cudaMemcpyHostToDevice));
-  p.ll_tag = 1;
-  st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
-  CU_TRY(cudaEventRecord(e0, s));
-  for (int i = 0; i < iters && st == PS_OK; ++i) {
-    p.ll_tag = 2 + i % 1000;          // distinct flags for back-to-back launches
-    st = launch_gemm(RP, false, mW, mW, mW, mX, p, gs.grid, s);
-  }
-  CU_TRY(cudaEventRecord(e1, s));
-  cudaError_t e = cudaStreamSynchronize(s);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  if (ms_out) *ms_out = ms / (iters > 0 ? iters : 1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaFree(din);
-  cudaFree(ws);
-  cudaFree(cnt);
-  if (st != PS_OK) return st;
-  if (e != cudaSuccess) return fail(PS_E_CUDA, "test gemm: %s", cudaGetErrorString(e));
-  return PS_OK;
-}
-
-extern "C" ps_status ps_test_gemm(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                  void* stream) {
-  return test_gemm_impl(W, X, out, N, K, R, stream, 0, 0, nullptr);
-}
-
-extern "C" ps_status ps_test_gemm_timed(const void* W, const void* X, float* out, int32_t N, int32_t K, int32_t R,
-                                        void* stream, int32_t iters, int32_t test_mode, float* avg_ms) {
-  return test_gemm_impl(W, X, out, N, K, R, stream, iters, test_mode, avg_ms);
-}
-
 __global__ void empty_smem_kernel(int* p) {
   extern __shared__ int sm_[];
   if (threadIdx.x == 0 && p) sm_[0] = p[0];

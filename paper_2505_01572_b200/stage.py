@@ -120,12 +120,6 @@ class Stage:
         t = _i32(tokens)
         abi.check(abi.lib().ps_resync(self._h, t.ctypes.data, len(t)))
 
-    def time_kernel(self, kind: int, layer: int = 0, iters: int = 20) -> float:
-        """Average ms per launch of one kernel of the last forward configuration."""
-        ms = C.c_double()
-        abi.check(abi.lib().ps_time_kernel(self._h, kind, layer, iters, C.byref(ms)))
-        return ms.value
-
     def draft(self, n_steps: int) -> list[int]:
         out = np.zeros(max(1, n_steps), dtype=np.int32)
         abi.check(abi.lib().ps_draft(self._h, n_steps, out.ctypes.data))
@@ -306,19 +300,3 @@ def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PI
     if return_events:
         return out[:n.value].tolist(), stats, ro.events(stats)
     return out[:n.value].tolist(), stats
-
-
-def test_gemm(W: torch.Tensor, X: torch.Tensor, R: int) -> torch.Tensor:
-    """Test hook (libpipespec_test.so): out[r, n] = X[r] . W[n] through the
-    production tcgen05 GEMM kernel.  X: fp32 [32, K] -- handed to the kernel
-    as the split-bf16 operand it consumes (hi rows 0..31 = bf16(X), lo rows
-    32..63 = bf16(X - hi); pure marshalling, the products run on the GPU)."""
-    N, K = W.shape
-    assert X.shape == (32, K) and X.dtype == torch.float32 and W.dtype == torch.bfloat16
-    hi = X.to(torch.bfloat16)
-    lo = (X - hi.float()).to(torch.bfloat16)
-    Xs = torch.cat([hi, lo]).contiguous()
-    out = torch.zeros(R, N, dtype=torch.float32, device=W.device)
-    s = torch.cuda.current_stream()
-    abi.test_check(abi.test_lib().ps_test_gemm(W.data_ptr(), Xs.data_ptr(), out.data_ptr(), N, K, R, s.cuda_stream))
-    return out

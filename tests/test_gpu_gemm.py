@@ -1,33 +1,35 @@
-"""GPU: the tcgen05 stream-K skinny GEMM (a4/a7-a10's contraction, split-bf16
-activation operand, R28) against a plain PyTorch fp32 matmul of the
-bf16 weights and the fp32 activations."""
+"""GPU: the megakernel's tcgen05 GEMM (a10's contraction: the lm_head over
+the split-bf16 operand) isolated by a ZERO-layer model, whose logits are
+rms(E[tok]) * g_f . W_lm^T -- no attention, no MLP -- against a float64 matmul
+of the same bf16 weights (vocabularies spanning ragged tiles, window sizes in
+both rows buckets)."""
+from dataclasses import replace
+
+import numpy as np
 import pytest
 import torch
+
+import synth
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("N,K,R", [(128, 64, 1), (256, 64, 16), (1000, 4096, 17), (6144, 4096, 32),
-                                   (4096, 14336, 5), (300, 192, 3), (2048, 8192, 9)])
-def test_gemm_matches_torch(N, K, R):
-    from paper_2505_01572_b200.stage import test_gemm
-    g = torch.Generator(device="cuda").manual_seed(N * 7 + K + R)
-    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    X = torch.randn(32, K, device="cuda", generator=g)
-    out = test_gemm(W, X, R)
-    ref = (X[:R].double() @ W.double().T).float()
-    err = (out - ref).abs().max().item()
-    # split operand: ~2^-16 relative per element -> far below a bf16 operand's 2^-8
-    assert err <= 2e-5 * max(1.0, ref.abs().max().item()) + 1e-5, err
-
-
-def test_gemm_row_invariance():
-    """Row r's result does not depend on R (16- vs 32-row buckets): bit-exact."""
-    from paper_2505_01572_b200.stage import test_gemm
-    g = torch.Generator(device="cuda").manual_seed(1)
-    W = (torch.randn(4096, 4096, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    X = torch.randn(32, 4096, device="cuda", generator=g)
-    a = test_gemm(W, X, 1)
-    b = test_gemm(W, X, 17)
-    c = test_gemm(W, X, 32)
-    assert torch.equal(a[0], b[0]) and torch.equal(b, c[:17])
+@pytest.mark.parametrize("vocab,d,rows", [(256, 128, 1), (1000, 4096, 5), (32000, 2048, 17), (128256, 4096, 9),
+                                          (300, 192, 32)])
+def test_zero_layer_logits_are_the_lm_head_gemm(vocab, d, rows):
+    from paper_2505_01572_b200 import Stage
+    s = replace(synth.preset("toy-verifier"), name="gemm", vocab=vocab, d_model=d, n_layers=0, n_heads=d // 64,
+                n_kv_heads=d // 64, d_ffn=d)
+    w = synth.make_weights(s, seed=vocab + d, device="cuda")
+    st = Stage(s, w, max_seq=64, max_window=31)
+    toks = [int(x) for x in synth.make_prompt(vocab, rows + 1, seed=3)]
+    st.prefill(toks[:1])
+    a, nxt, logits = st.verify(toks[1:rows], want_logits=True)
+    st.close()
+    E = w["embed"].double().cpu().numpy()[toks[:rows]]
+    xn = E / np.sqrt((E * E).mean(-1, keepdims=True) + s.rms_eps) * w["final_norm"].double().cpu().numpy()
+    ref = xn @ w["lm_head"].double().cpu().numpy().T
+    err = np.abs(logits - ref).max()
+    # split-bf16 operand: ~2^-16 relative per element, fp32 accumulation
+    assert err <= 2e-5 * np.abs(ref).max(), err
+    assert list(np.argmax(logits, 1)[:a + 1]) == list(np.argmax(ref, 1)[:a + 1])

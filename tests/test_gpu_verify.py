@@ -180,29 +180,6 @@ def test_lazy_resync_catch_up_equals_eager(toy):
     check_verify((a3, n3), ref, 0)
 
 
-@pytest.mark.parametrize("name,layers", [("toy-verifier", None), ("llama3.1-8b", 2)])
-def test_megakernel_equals_per_kernel_path(name, layers):
-    """The persistent megakernel and the one-kernel-per-step path run the same
-    arithmetic: logits bit-identical, same (a, next)."""
-    from paper_2505_01572_b200 import Stage
-    s = synth.preset(name)
-    if layers:
-        s = synth.reduced_depth(s, layers)
-    w = synth.make_weights(s, seed=5, device="cuda")
-    prompt = list(synth.make_prompt(s.vocab, 100, seed=6))
-    outs = []
-    for mega in (True, False):
-        st = Stage(s, w, max_seq=200, megakernel=mega)
-        st.prefill(prompt)
-        toks = st.draft(3)
-        st.prefill(prompt)
-        outs.append((toks, st.verify(toks[:2] + [(toks[2] + 1) % s.vocab], want_logits=True)))
-        st.close()
-    (t1, (a1, n1, l1)), (t2, (a2, n2, l2)) = outs
-    assert t1 == t2 and (a1, n1) == (a2, n2)
-    assert np.array_equal(l1, l2)
-
-
 @pytest.mark.slow
 def test_bench_config_self_consistency():
     """BASELINE configs[1] at full size (LLaMA-3.2-1B -> LLaMA-3.1-8B shapes,
