@@ -199,7 +199,30 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, int iters, i
   tc_fence_after();
   const uint32_t tmem = tslot;
   constexpr uint32_t kI = idesc_bf16_f32<128, 16>();
-  if (threadIdx.x == 32) {
+  if (mode >= 12) {   // TMEM -> registers -> shared memory: 256 columns x 32 lanes by warp 0 per unit
+    float* T = reinterpret_cast<float*>(sm);
+    if (warp == 0) {
+      const unsigned long long t0 = globaltimer();
+      float acc = 0.f;
+      for (int i = 0; i < iters; ++i) {
+        for (int c0 = 0; c0 < 256; c0 += 32) {
+          float a32[32];
+          tmem_ld32(tmem + c0, a32);
+          if (mode == 12) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(T + (threadIdx.x & 31) * 260 + c0 + 4 * q) =
+                  make_float4(a32[4 * q], a32[4 * q + 1], a32[4 * q + 2], a32[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) acc += a32[q];
+          }
+        }
+      }
+      if ((threadIdx.x & 31) == 0) out[blockIdx.x] = globaltimer() - t0;
+      if (acc == 1234.5f) T[0] = acc;
+    }
+  } else if (threadIdx.x == 32) {
     const unsigned long long t0 = globaltimer();
     uint32_t ph = 0;
     for (int i = 0; i < iters; ++i) {

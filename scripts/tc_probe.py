@@ -5,7 +5,8 @@ L = abi.test_lib()
 L.ps_test_tc_probe.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 MODES = [(0, "cp 16KB"), (1, "8 MMA A=tmem"), (2, "8 MMA A=smem"), (3, "cp + 8 MMA tmem"),
          (4, "4 MMA N32 1acc"), (5, "8 MMA N16 2acc"), (6, "4 MMA N32 2acc"), (7, "4 MMA N16 1acc"),
-         (8, "8 MMA N16 4acc"), (9, "4 MMA N32 4acc"), (10, "W as B N256 32KB"), (11, "W as B N128 16KB")]
+         (8, "8 MMA N16 4acc"), (9, "4 MMA N32 4acc"), (10, "W as B N256 32KB"), (11, "W as B N128 16KB"),
+         (12, "TMEM->smem 256 col"), (13, "TMEM->regs 256 col")]
 ns = C.c_double()
 abi.test_check(L.ps_test_tc_probe(2, 200000, 4, C.byref(ns)))     # warm up the clocks
 for mode, name in MODES[int(sys.argv[1]) if len(sys.argv) > 1 else 0:]:
