@@ -9,5 +9,5 @@ Both `oracle/` and `paper_2505_01572_b200/` may import it; neither imports
 the other.
 """
 from .shapes import ModelShape, PRESETS, preset, reduced_depth  # noqa: F401
-from .weights import make_weights, weights_to_numpy  # noqa: F401
+from .weights import make_weights, make_weights_sharded, weights_to_numpy  # noqa: F401
 from .prompts import make_prompt, make_window  # noqa: F401

@@ -80,3 +80,43 @@ def weights_to_numpy(w: dict) -> dict:
     out = {k: _np64(w[k]) for k in ("embed", "lm_head", "final_norm")}
     out["layers"] = [{k: _np64(v) for k, v in lw.items()} for lw in w["layers"]]
     return out
+
+
+def make_weights_sharded(shape: ModelShape, seed: int, rank: int, tp: int, device="cpu", std: float = 0.02,
+                         gain_std: float = 0.1) -> dict:
+    """Rank `rank`'s Megatron shard of make_weights(shape, seed) (the layout of
+    include/pipespec.h ps_placement: Q/K/V by heads, gate/up by FFN rows, O and
+    down by the matching input columns, lm_head by vocabulary rows; embed and
+    gains replicated), generated tensor by tensor so the full model is never
+    resident (a 70B stage: 141 GB).  Bit-identical to slicing make_weights."""
+    T, r = tp, rank
+    d, hq, hkv, f = shape.d_model, shape.q_dim, shape.kv_dim, shape.d_ffn
+    hd = shape.head_dim
+    qh, kh, fr, vr = shape.n_heads // T, shape.n_kv_heads // T, f // T, shape.vocab // T
+
+    def rows(t, a, b):
+        return t[a:b].contiguous()
+
+    def cols(t, a, b):
+        return t[:, a:b].contiguous()
+
+    embed = _randn((shape.vocab, d), seed, -1, "embed", device, std)
+    full_lm = embed if shape.tied else _randn((shape.vocab, d), seed, -1, "lm_head", device, std)
+    w = {"embed": embed, "lm_head": rows(full_lm, r * vr, (r + 1) * vr),
+         "final_norm": _gain(d, seed, -1, "final_norm", device, gain_std)}
+    del full_lm
+    layers = []
+    for l in range(shape.n_layers):
+        layers.append({
+            "wq": rows(_randn((hq, d), seed, l, "wq", device, std), r * qh * hd, (r + 1) * qh * hd),
+            "wk": rows(_randn((hkv, d), seed, l, "wk", device, std), r * kh * hd, (r + 1) * kh * hd),
+            "wv": rows(_randn((hkv, d), seed, l, "wv", device, std), r * kh * hd, (r + 1) * kh * hd),
+            "wo": cols(_randn((d, hq), seed, l, "wo", device, std), r * qh * hd, (r + 1) * qh * hd),
+            "wg": rows(_randn((f, d), seed, l, "wg", device, std), r * fr, (r + 1) * fr),
+            "wu": rows(_randn((f, d), seed, l, "wu", device, std), r * fr, (r + 1) * fr),
+            "wd": cols(_randn((d, f), seed, l, "wd", device, std), r * fr, (r + 1) * fr),
+            "n_attn": _gain(d, seed, l, "n_attn", device, gain_std),
+            "n_mlp": _gain(d, seed, l, "n_mlp", device, gain_std),
+        })
+    w["layers"] = layers
+    return w

@@ -95,3 +95,23 @@ def test_tp_connect_group_gloo():
         p.join(timeout=60)
     for _, got in res:
         assert got == [bytes([1]) * 64, bytes([2]) * 64]
+
+
+def test_sharded_generation_equals_slicing_the_full_model():
+    """synth.make_weights_sharded (used for the 70B stages) is bit-identical to
+    slicing the full model with stage.shard_weights."""
+    import torch
+
+    import synth
+    from paper_2505_01572_b200.stage import shard_weights
+    s = synth.preset("toy-tp")
+    full = synth.make_weights(s, seed=5)
+    for T in (2, 4):
+        for r in range(T):
+            a = synth.make_weights_sharded(s, seed=5, rank=r, tp=T)
+            b = shard_weights(s, full, r, T)
+            for k in ("embed", "lm_head", "final_norm"):
+                assert torch.equal(a[k], b[k]), k
+            for la, lb in zip(a["layers"], b["layers"]):
+                for k in la:
+                    assert torch.equal(la[k], lb[k]), k
