@@ -17,9 +17,12 @@ roofline the dominant kernel (gate/up GEMM of M_1) timed live with CUDA events
 cpu_baseline / --impl reference: the fp64 oracle on the host cores (bounded
          sample, extrapolated in depth)
 
-N>1 (torchrun): every rank runs an independent replica of the batch-1 job
-(weak scaling, no data-path collective); the stage-per-GPU pipeline is the
-NEXT-1 runtime.
+N>1 (torchrun, one process per GPU): the paper's layout (SURVEY
+§8(d)/(e)) -- each model on its own GPU, the largest tensor parallel: N=2 config
+2 (1B@0 -> 8B@1), N=3 config 3 (68M -> 7B -> 13B), N=4 config 4 with the 70B
+TP2 on GPUs 2-3, N=8 config 4 with the 70B TP4 on GPUs 4-7; async PipeSpec
+through ps_pipeline_run_rank(_group) over a shared-memory board, next to the
+target's AR and synchronous SD on the same GPUs (run_layout).
 """
 from __future__ import annotations
 
@@ -48,15 +51,21 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--draft", default="llama3.2-1b")
     ap.add_argument("--target", default="llama3.1-8b")
-    ap.add_argument("--prompt", type=int, default=512)
+    ap.add_argument("--prompt", type=int, default=None)
     ap.add_argument("--gen", type=int, default=256)
     ap.add_argument("--gamma", type=int, default=4)   # SD window tuned on B200 over {3,4,5,8} (paper SD: 8)
     ap.add_argument("--alpha", type=float, default=0.8)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--multi-gpu-extras", action="store_true",
-                    help="N>1: also time M_1 tensor-parallel over the N GPUs and the stage-per-GPU async pipeline")
-    return ap.parse_args()
+    ap.add_argument("--config", choices=sorted(LAYOUT_CONFIGS), default=None,
+                    help="N>1 layout workload (default: c2 at N=2, c3 at N=3, c4 otherwise)")
+    ap.add_argument("--layers", type=int, default=None, help="N>1 smoke runs: cap every model's depth")
+    ap.add_argument("--lookahead", type=int, default=0, help="N>1: verifier lookahead (P:285: 0)")
+    a = ap.parse_args()
+    a.prompt_set = a.prompt is not None
+    if a.prompt is None:
+        a.prompt = 512
+    return a
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -163,68 +172,221 @@ def aggregate(dev_s, wall_s, tokens, world, device="cpu"):
     return float(times[0]), float(times[1]), float(tok[0])
 
 
-def multi_gpu_extras(args, rank, world, ts, wt, drafter, target, prompt, S, g):
-    """N > 1 only (beside the replica line): (1) M_1's verify pass tensor-
-    parallel over all N GPUs -- Megatron shards, the all-reduces and the
-    vocab-parallel argmax inside the megakernel over NVLink peer memory
-    (SURVEY §8(e), a14); (2) the paper's stage-per-GPU layout, M_0 on rank 0's
-    GPU and M_1 on rank 1's, async PipeSpec through the shared-memory board.
-    Each part reports an error string instead of failing the bench."""
+# ----------------------------------------------------------------------------- N > 1: the paper's layouts
+# each model on its own GPU(s), the largest tensor parallel
+# (P:179-181).  config 2 (k=2, 1B -> 8B, 512-token prompt) at N = 2; config 3
+# (k=3, 68M -> 7B -> 13B, 1K prompt) at N = 3; config 4 (k=3, 1B -> 8B -> 70B,
+# 2K prompt) at N = 4 (70B TP2 on GPUs 2-3) and N = 8 (70B TP4 on GPUs 4-7).
+LAYOUT_CONFIGS = {
+    "c2": {"models": ["llama3.2-1b", "llama3.1-8b"], "prompt": 512, "name": "BASELINE configs[1]"},
+    "c3": {"models": ["llama-68m", "llama2-7b", "llama2-13b"], "prompt": 1024, "name": "BASELINE configs[2]"},
+    "c4": {"models": ["llama3.2-1b", "llama3.1-8b", "llama3.1-70b"], "prompt": 2048, "name": "BASELINE configs[3]"},
+}
+
+
+def layout_for(n_gpus, cfg_name, shapes):
+    """Devices of each stage: one GPU per drafter, the remaining GPUs (the
+    largest power of two that divides the target's KV heads) to the target,
+    placed at the end (8 GPUs: 1B@0, 8B@1, 70B TP4@4-7)."""
+    k = len(shapes)
+    rest = n_gpus - (k - 1)
+    if rest < 1:
+        raise ValueError(f"{cfg_name} needs >= {k} GPUs")
+    t = 1
+    while t * 2 <= rest and shapes[-1].n_kv_heads % (t * 2) == 0 and shapes[-1].vocab % (t * 2) == 0:
+        t *= 2
+    devs = [[i] for i in range(k - 1)] + [list(range(n_gpus - t, n_gpus))]
+    return devs
+
+
+def run_layout(args, rank, local, world):
+    """N > 1: async PipeSpec with one stage per GPU (group), through
+    ps_pipeline_run_rank(_group) over the shared-memory board.  A step is one
+    whole generation of --gen tokens; value = generated tokens / the max over
+    ranks of the device time of the timed steps."""
     import torch
     import torch.distributed as dist
-    from paper_2505_01572_b200 import (Stage, board_create, board_unlink, pipeline_run_rank, shard_weights,
-                                       tp_connect_group)
-    out = {}
-    obj = [prompt, S, f"/pipespec-bench-{os.getpid()}"]
-    dist.broadcast_object_list(obj, src=0)        # every rank works on rank 0's prompt and stream
-    p0, S0, board = obj
-    try:
-        tps = Stage(ts, shard_weights(ts, wt, rank, world), max_seq=args.prompt + 64, max_window=g,
-                    tp_rank=rank, tp_size=world)
-        tp_connect_group(tps)
-        tps.prefill(p0)
-        win = S0[:g]
-        res = None
-        for it in range(13):
-            if it == 3:
-                torch.cuda.synchronize()
-                dist.barrier()
-                tps.reset_timers()
-            res = tps.verify(win)
-            tps.kv_rollback(len(p0))
-        inf = tps.info()
-        ms = torch.tensor([inf["sum_fwd_ms"] / max(1, inf["n_fwd"])], device="cuda", dtype=torch.float64)
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        R = g + 1
-        byts = ts.streamed_bytes_per_pass(R) + (len(p0) + R) * ts.kv_bytes_per_token()
-        out["tp_verify_pass"] = {"tp": world, "ms": float(ms[0]), "rows": R, "ctx": len(p0),
-                                 "accepted": res[0], "agg_GB/s": byts / (float(ms[0]) * 1e-3) / 1e9}
-        tps.close()
-    except Exception as e:  # noqa: BLE001
-        out["tp_verify_pass"] = {"error": repr(e)[:300]}
-    try:
+
+    import synth
+    from paper_2505_01572_b200 import (Stage, abi, board_create, board_unlink, group_call, pipeline_run_rank,
+                                       tp_connect_local)
+    cfg_name = args.config or {2: "c2", 3: "c3"}.get(world, "c4")
+    cfg = LAYOUT_CONFIGS[cfg_name]
+    shapes = [synth.preset(m) for m in cfg["models"]]
+    if args.layers:
+        shapes = [synth.reduced_depth(s, min(s.n_layers, args.layers)) for s in shapes]
+    prompt_len = args.prompt if args.prompt_set else cfg["prompt"]
+    k = len(shapes)
+    K = k - 1
+    devs = layout_for(world, cfg_name, shapes)
+    ndev = torch.cuda.device_count()
+    phys = lambda r: r % ndev                      # (test boxes with fewer GPUs than ranks share devices)
+    owner = {d[0]: i for i, d in enumerate(devs)}
+    my_stage = owner.get(rank)
+    g = args.gamma
+    max_seq = prompt_len + args.gen + 4 * g + 96
+    prompt = [int(x) for x in synth.make_prompt(shapes[-1].vocab, prompt_len, seed=args.seed + 17)]
+    group = []
+    n_sm = torch.cuda.get_device_properties(phys(local)).multi_processor_count
+    if my_stage is not None:
+        s = shapes[my_stage]
+        members = devs[my_stage]
+        T = len(members)
+        share = {}
+        for m in members:
+            share[phys(m)] = share.get(phys(m), 0) + 1
+        for r_, m in enumerate(members):
+            dev = phys(m)
+            with torch.cuda.device(dev):
+                w = (synth.make_weights(s, seed=args.seed + my_stage, device=f"cuda:{dev}") if T == 1 else
+                     synth.make_weights_sharded(s, seed=args.seed + my_stage, rank=r_, tp=T, device=f"cuda:{dev}"))
+                group.append(Stage(s, w, max_seq=max_seq, max_window=max(g, 1), device=dev, tp_rank=r_, tp_size=T,
+                                   max_ctas=n_sm // share[dev] if share[dev] > 1 else 0))
+        if T > 1:
+            tp_connect_local(group)
+        group_call(group, lambda st: st.prefill(prompt))
+    # --- the target's autoregressive stream S (the lossless reference and the AR baseline)
+    tgt_owner = devs[K][0]
+    ar_tok_s = None
+    S = None
+    if my_stage == K:
+        lead = group[0]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lead.stream)
+        S = group_call(group, lambda st: st.draft(args.gen + 2 * g + 2))
+        e1.record(lead.stream)
+        e1.synchronize()
+        ar_tok_s = len(S) / (e0.elapsed_time(e1) / 1e3)
+        group_call(group, lambda st: st.kv_rollback(prompt_len))
+    obj = [S, ar_tok_s]
+    dist.broadcast_object_list(obj, src=tgt_owner)
+    S, ar_tok_s = obj
+    if my_stage is not None and my_stage < K:
+        alphas = [args.alpha] * (K - my_stage)
+        group_call(group, lambda st: st.set_synthetic(S, prompt_len, level=my_stage, top=K, alphas=alphas,
+                                                      seed=args.seed + 1234))
+
+    def one_generation(tag, lookahead, max_lead=0, timed=False):
+        board = f"/pipespec-bench-{os.getpid() if rank == 0 else 0}-{tag}"
+        obj = [board]
+        dist.broadcast_object_list(obj, src=0)
+        board = obj[0]
         if rank == 0:
-            board_create(board, 2, len(p0) + args.gen + 512)
-            drafter.set_synthetic(S0, len(p0), level=0, top=1, alphas=[args.alpha], seed=args.seed + 1234)
+            board_create(board, k, prompt_len + args.gen + 1024)
         dist.barrier()
-        if rank < 2:
-            stage = drafter if rank == 0 else target
+        out, st, dt = None, None, 0.0
+        if my_stage is not None:
             torch.cuda.synchronize()
-            w0 = time.perf_counter()
-            got, st = pipeline_run_rank(stage, rank, 2, board, p0, args.gen, gammas=[0, g])
-            dt = time.perf_counter() - w0
-            ok = got == S0[:args.gen]
+            gammas = [0] + [g] * K
+            out, st = pipeline_run_rank(group if len(group) > 1 else group[0], my_stage, k, board, prompt, args.gen,
+                                        gammas=gammas, lookaheads=[0] + [lookahead] * K, max_lead=max_lead)
+            torch.cuda.synchronize()
+            dt = st.wall_ns / 1e9
         dist.barrier()
         if rank == 0:
             board_unlink(board)
-            out["stage_per_gpu_pipespec"] = {"layout": "M_0 on GPU 0, M_1 on GPU 1, one process each",
-                                             "tokens_per_s": len(got) / dt,
-                                             "tokens_per_s_decode": len(got) / (st.wall_ns / 1e9),
-                                             "lossless": ok, "verify_steps": int(st.verify_steps[1]),
-                                             "rollbacks": int(st.rollbacks[0])}
-    except Exception as e:  # noqa: BLE001
-        out["stage_per_gpu_pipespec"] = {"error": repr(e)[:300]}
-    return out
+        if my_stage == K:
+            assert out == S[:args.gen], f"{tag}: output differs from M_K autoregressive decoding"
+        return out, st, dt
+
+    for i in range(args.warmup):
+        one_generation(f"w{i}", args.lookahead)
+    for st_ in group:
+        st_.reset_timers()
+    L = abi.lib()
+    launches0 = L.ps_kernel_launch_count()
+    dev_s, wall_s, tokens = 0.0, 0.0, 0
+    accept = {}
+    stats_last = None
+    with ClockSampler(phys(local)) as clk:
+        for i in range(args.steps):
+            w0 = time.perf_counter()
+            e0 = e1 = None
+            if group:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(group[0].stream)
+            out, st, dt = one_generation(f"s{i}", args.lookahead)
+            if group:
+                e1.record(group[0].stream)
+                e1.synchronize()
+                dev_s += e0.elapsed_time(e1) / 1e3
+            wall_s += time.perf_counter() - w0
+            tokens += args.gen
+            if st is not None:
+                stats_last = st
+                for kk, c in enumerate(st.accept_hist):
+                    if c:
+                        accept[kk] = accept.get(kk, 0) + int(c)
+    launches = L.ps_kernel_launch_count() - launches0
+    # synchronous SD on the same GPUs: the verifier waits for gamma drafts and the
+    # drafter stops gamma ahead (lookahead = max_lead = gamma), one generation
+    w0 = time.perf_counter()
+    one_generation("sync", g, max_lead=g)
+    sync_s = time.perf_counter() - w0
+    w0 = time.perf_counter()
+    one_generation("la0", 0)
+    la0_s = time.perf_counter() - w0
+    t = torch.tensor([dev_s, wall_s, sync_s, la0_s, float(launches)], dtype=torch.float64)
+    dist.all_reduce(t[:4], op=dist.ReduceOp.MAX)
+    lt = t[4:].clone()
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    dev_s, wall_s, sync_s, la0_s = [float(x) for x in t[:4]]
+    # the target's verify pass (device events around each of its passes)
+    info = group[0].info() if my_stage == K else None
+    obj = [info, accept if my_stage == K else None,
+           ({"steps": [int(x) for x in stats_last.steps[:k]], "verify_steps": [int(x) for x in stats_last.verify_steps[:k]],
+             "rollbacks": [int(x) for x in stats_last.rollbacks[:k]]} if my_stage == K and stats_last else None)]
+    dist.broadcast_object_list(obj, src=tgt_owner)
+    info, accept, run_stats = obj
+    if rank == 0:
+        ts = shapes[-1]
+        T = len(devs[-1])
+        pass_ms = info["sum_fwd_ms"] / max(1, info["n_fwd"])
+        ctx = prompt_len + args.gen / 2
+        R = g + 1
+        pass_bytes = ts.streamed_bytes_per_pass(R) / T + (ctx + R) * ts.kv_bytes_per_token() / T
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = peaks.get("hbm_gbs", 6650.0)
+        value = tokens / dev_s
+        gbs = pass_bytes / (pass_ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"k={k} {' -> '.join(m for m in cfg['models'])} ({cfg['name']}), async PipeSpec "
+                                   f"(Alg.1), lookahead {args.lookahead}, gamma {g}, synthetic alpha {args.alpha} per link",
+                       "layout": {m: ([f"GPU {d}" for d in dl] if len(dl) == 1 else
+                                      [f"TP{len(dl)} on GPUs {dl[0]}-{dl[-1]}"])
+                                  for m, dl in zip(cfg["models"], devs)},
+                       "prompt": prompt_len, "gen": args.gen, "global_batch": 1,
+                       "parallelism": "stage-per-GPU" + (f" + TP{len(devs[-1])}" if len(devs[-1]) > 1 else ""),
+                       "step": f"one generation of {args.gen} tokens",
+                       "l2": "inputs > L2 (the target's weights streamed per verify pass)"},
+            "ar_tokens_per_s": ar_tok_s, "speedup_vs_ar": value / ar_tok_s,
+            "sync_sd_same_gpus": {"tokens_per_s": args.gen / sync_s, "mode": "lookahead = max_lead = gamma"},
+            "pipespec_lookahead0_tokens_per_s": args.gen / la0_s,
+            "speedup_vs_sync_sd": value / (args.gen / sync_s),
+            "accept_hist": accept, "run_stats": run_stats,
+            "verify_pass": {"stage": cfg["models"][-1], "tp": T, "ms": pass_ms, "rows": R,
+                            "bytes_per_gpu": pass_bytes, "GB/s_per_gpu": gbs, "frac": gbs / peak},
+            "roofline": {"kernel": f"{cfg['models'][-1]} verify forward (megakernel, per GPU of the stage)",
+                         "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "traffic": None, "algorithmic_bytes_per_launch": pass_bytes, "rows": R,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "e2e": {"value": tokens / wall_s, "unit": "tokens/s", "h2d_bytes_per_step": 4 * prompt_len,
+                    "d2h_bytes_per_step": 4 * args.gen},
+            "gpu_launches": int(lt[0]),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    for st_ in group:
+        st_.close()
+    dist.destroy_process_group()
 
 
 def oracle_sample(draft_shape, target_shape, wd, wt, gamma, alpha, seed, n_rounds, ctx=64, layers=2):
@@ -327,9 +489,16 @@ def main():
     from paper_2505_01572_b200 import Stage, abi
 
     rank, local, world = dist_env()
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU over NCCL; a box with fewer GPUs than ranks (smoke
+        # runs of the layout code) shares devices, which NCCL refuses: gloo then
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        return run_layout(args, rank, local, world)
     ds, ts = synth.preset(args.draft), synth.preset(args.target)
     g = args.gamma
     max_seq = args.prompt + args.gen + 4 * g + 64
@@ -452,7 +621,7 @@ def main():
         "config": {"workload": f"k=2 {args.draft}->{args.target} (BASELINE configs[1]), sync-SD round "
                                f"gamma={args.gamma}, synthetic alpha={args.alpha}, co-resident on 1 GPU",
                    "prompt": args.prompt, "gen": args.gen, "global_batch": world,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": "single GPU, stages co-resident",
                    "l2": "inputs > L2 (16 GB of 8B weights streamed per verify pass)"},
         "speedup_vs_ar": value / ar_tok_s, "ar_tokens_per_s": ar_tok_s,
         "pipeline_run": modes,
@@ -476,8 +645,6 @@ def main():
         # board energy counter across the timed region (this GPU's tokens; paper 4.5)
         line["energy"] = {"joules": clk.energy_j, "j_per_token": clk.energy_j / tokens,
                           "avg_w": clk.energy_j / max(wall_s, 1e-9), "source": "nvmlDeviceGetTotalEnergyConsumption"}
-    if world > 1 and args.multi_gpu_extras:
-        line["multi_gpu"] = multi_gpu_extras(args, rank, world, ts, wt, drafter, target, prompt, S, g)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, times, toks = oracle_sample(ds, ts, wd, wt, g, args.alpha, args.seed + 1234, 2)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",

@@ -345,6 +345,18 @@ ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const c
                                const int32_t* prompt, int32_t n_prompt, const ps_run_opts* opts,
                                int32_t* out, int32_t* out_len, ps_run_stats* stats);
 
+/* ps_pipeline_run_rank for a stage M_rank that is TENSOR PARALLEL over the n
+ * members group[0..n-1] (ranks of one group connected with
+ * ps_tp_connect_local, e.g. on n GPUs driven by this process): every step of
+ * the stage's loop (prefill, draft, verify, resync) runs on all members
+ * concurrently, one host thread each; the members must agree bit for bit
+ * (else PS_E_CUDA) and the leader's result drives the board.  n = 1 is
+ * ps_pipeline_run_rank. */
+ps_status ps_pipeline_run_rank_group(ps_stage* const* group, int32_t n, int32_t rank, int32_t k,
+                                     const char* board, const int32_t* prompt, int32_t n_prompt,
+                                     const ps_run_opts* opts, int32_t* out, int32_t* out_len,
+                                     ps_run_stats* stats);
+
 /* Device-side timing hook for benchmarks: number of kernels this library has
  * launched (graph launches count their kernels) since process start. */
 int64_t ps_kernel_launch_count(void);

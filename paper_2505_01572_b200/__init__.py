@@ -7,4 +7,5 @@ PipeSpecError(PS_E_CUDA).
 """
 from .abi import PipeSpecError  # noqa: F401
 from .stage import (Stage, pipeline_run, kv_pool_bytes, model_shape, shard_weights,  # noqa: F401
-                    tp_connect_local, tp_connect_group, board_create, board_unlink, pipeline_run_rank)
+                    tp_connect_local, tp_connect_group, board_create, board_unlink, pipeline_run_rank,
+                    group_call, RunOptions)

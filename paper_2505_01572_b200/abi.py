@@ -121,6 +121,9 @@ _PROTOS = {
     "ps_board_unlink": (C.c_int32, [C.c_char_p]),
     "ps_pipeline_run_rank": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_void_p, C.c_int32,
                                          C.POINTER(RunOpts), C.c_void_p, _I32P, C.POINTER(RunStats)]),
+    "ps_pipeline_run_rank_group": (C.c_int32, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_char_p,
+                                               C.c_void_p, C.c_int32, C.POINTER(RunOpts), C.c_void_p, _I32P,
+                                               C.POINTER(RunStats)]),
 }
 
 # libpipespec_test.so (include/pipespec_test.h): test infrastructure, never

@@ -250,31 +250,103 @@ extern "C" ps_status ps_board_unlink(const char* name) {
   return shm_unlink(name) == 0 ? PS_OK : fail(PS_E_INVALID, "cannot unlink board %s", name);
 }
 
-extern "C" ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const char* board,
-                                          const int32_t* prompt, int32_t n_prompt, const ps_run_opts* o,
-                                          int32_t* out, int32_t* out_len, ps_run_stats* stats) {
-  if (!stage || !board || !prompt || n_prompt < 1 || !o || !out || !out_len || o->max_new_tokens < 1)
-    return fail(PS_E_INVALID, "ps_pipeline_run_rank: NULL argument");
-  if (o->mode != PS_MODE_PIPESPEC) return fail(PS_E_INVALID, "ps_pipeline_run_rank runs PS_MODE_PIPESPEC only");
+// ---------------------------------------------------------------- tensor-parallel stage groups
+// A stage M_rank that is tensor parallel over n ranks driven by THIS process
+// (one host thread per member, ps_tp_connect_local): every board step runs on
+// all members concurrently; the members agree bit for bit, the leader's
+// result is the stage's.
+namespace {
+struct Group {
+  std::vector<ps_stage*> st;
+};
+template <class F>
+ps_status all_members(Group* g, F f) {
+  const int n = (int)g->st.size();
+  if (n == 1) return f(0);
+  std::vector<ps_status> r(n, PS_OK);
+  std::vector<std::string> err(n);
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; ++i)
+    th.emplace_back([&, i] {
+      r[i] = f(i);
+      if (r[i] != PS_OK) err[i] = ps_last_error();
+    });
+  r[0] = f(0);
+  if (r[0] != PS_OK) err[0] = ps_last_error();
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n; ++i)
+    if (r[i] != PS_OK) return fail(r[i], "tensor-parallel member %d: %s", i, err[i].c_str());
+  return PS_OK;
+}
+ps_status grp_draft1(void* c, int32_t* t) {
+  Group* g = (Group*)c;
+  std::vector<int32_t> tt(g->st.size());
+  ps_status st = all_members(g, [&](int i) { return ps_draft(g->st[i], 1, &tt[i]); });
+  if (st != PS_OK) return st;
+  for (size_t i = 1; i < tt.size(); ++i)
+    if (tt[i] != tt[0]) return fail(PS_E_CUDA, "tensor-parallel members disagree (%d vs %d)", tt[i], tt[0]);
+  *t = tt[0];
+  return PS_OK;
+}
+ps_status grp_verify(void* c, const int32_t* w, int32_t n, int32_t* a, int32_t* nx) {
+  Group* g = (Group*)c;
+  std::vector<int32_t> aa(g->st.size()), nn(g->st.size());
+  ps_status st = all_members(g, [&](int i) {
+    ps_verify_ticket tk;
+    ps_status s2 = ps_verify_async(g->st[i], w, n, &tk);
+    return s2 != PS_OK ? s2 : ps_verify_wait(g->st[i], &aa[i], &nn[i]);
+  });
+  if (st != PS_OK) return st;
+  for (size_t i = 1; i < aa.size(); ++i)
+    if (aa[i] != aa[0] || nn[i] != nn[0]) return fail(PS_E_CUDA, "tensor-parallel members disagree on (a, next)");
+  *a = aa[0];
+  *nx = nn[0];
+  return PS_OK;
+}
+ps_status grp_resync(void* c, const int32_t* t, int32_t n) {
+  Group* g = (Group*)c;
+  return all_members(g, [&](int i) { return ps_resync(g->st[i], t, n); });
+}
+ps_status grp_tokens(void* c, std::vector<int32_t>& v) { return tokens_of(((Group*)c)->st[0], v); }
+}  // namespace
+
+extern "C" ps_status ps_pipeline_run_rank_group(ps_stage* const* group, int32_t n, int32_t rank, int32_t k,
+                                                const char* board, const int32_t* prompt, int32_t n_prompt,
+                                                const ps_run_opts* o, int32_t* out, int32_t* out_len,
+                                                ps_run_stats* stats) {
+  if (!group || n < 1 || n > 8 || !board || !prompt || n_prompt < 1 || !o || !out || !out_len ||
+      o->max_new_tokens < 1)
+    return fail(PS_E_INVALID, "ps_pipeline_run_rank_group: bad argument");
+  for (int i = 0; i < n; ++i)
+    if (!group[i]) return fail(PS_E_INVALID, "NULL group member %d", i);
+  if (o->mode != PS_MODE_PIPESPEC) return fail(PS_E_INVALID, "per-rank runs are PS_MODE_PIPESPEC only");
   if (o->alpha) return fail(PS_E_INVALID, "per-rank runs take their synthetic override from ps_set_synthetic");
   ps_status st;
-  if (rank > 0 && (st = check_gammas(&stage, k, o, rank)) != PS_OK) return st;
-  if ((st = ps_prefill(stage, prompt, n_prompt)) != PS_OK) return st;
+  if (rank > 0 && (st = check_gammas(group, k, o, rank)) != PS_OK) return st;
+  Group g{std::vector<ps_stage*>(group, group + n)};
+  if ((st = all_members(&g, [&](int i) { return ps_prefill(g.st[i], prompt, n_prompt); })) != PS_OK) return st;
   ps_run_stats local;
   ps_run_stats* stt = stats ? stats : &local;
   memset(stt, 0, sizeof *stt);
   double ms0 = 0;
   int64_t n0 = 0;
-  fwd_totals(stage, &ms0, &n0);
+  fwd_totals(group[0], &ms0, &n0);
   std::string err;
-  st = run_rank(real_ops(stage), rank, k, board, n_prompt, o, out, out_len, stt, last_error_str, &err);
+  const StageOps ops = n == 1 ? real_ops(group[0]) : StageOps{&g, grp_draft1, grp_verify, grp_resync, grp_tokens};
+  st = run_rank(ops, rank, k, board, n_prompt, o, out, out_len, stt, last_error_str, &err);
   if (st != PS_OK) return fail(st, "%s", err.c_str());
   if (rank >= 0 && rank < 8) {
     double ms = 0;
-    int64_t n = 0;
-    fwd_totals(stage, &ms, &n);
+    int64_t nf = 0;
+    fwd_totals(group[0], &ms, &nf);
     stt->fwd_ns[rank] = (int64_t)((ms - ms0) * 1e6);
-    stt->n_fwd[rank] = n - n0;
+    stt->n_fwd[rank] = nf - n0;
   }
   return PS_OK;
+}
+
+extern "C" ps_status ps_pipeline_run_rank(ps_stage* stage, int32_t rank, int32_t k, const char* board,
+                                          const int32_t* prompt, int32_t n_prompt, const ps_run_opts* o,
+                                          int32_t* out, int32_t* out_len, ps_run_stats* stats) {
+  return ps_pipeline_run_rank_group(&stage, 1, rank, k, board, prompt, n_prompt, o, out, out_len, stats);
 }

@@ -268,15 +268,19 @@ def board_unlink(name: str):
 def pipeline_run_rank(stage, rank: int, k: int, board: str, prompt, max_new_tokens: int, gammas=None,
                       lookaheads=None, eos_id: int = -1, max_lead: int = 0, virtual_ns=None, event_cap: int = 0,
                       return_events: bool = False):
-    """This process's stage M_rank of a k-stage async PipeSpec run (ps_pipeline_run_rank)."""
+    """This process's stage M_rank of a k-stage async PipeSpec run
+    (ps_pipeline_run_rank); `stage` may be a list of the members of a
+    tensor-parallel group driven by this process (ps_pipeline_run_rank_group)."""
+    group = list(stage) if isinstance(stage, (list, tuple)) else [stage]
     ro = RunOptions(k, max_new_tokens, abi.PS_MODE_PIPESPEC, gammas, lookaheads, eos_id, max_lead,
                     virtual_ns=virtual_ns, event_cap=event_cap)
     p = _i32(prompt)
     out = np.zeros(max_new_tokens, dtype=np.int32)
     n = C.c_int32()
     stats = abi.RunStats()
-    abi.check(abi.lib().ps_pipeline_run_rank(stage.handle, rank, k, board.encode(), p.ctypes.data, len(p),
-                                             C.byref(ro.opts), out.ctypes.data, C.byref(n), C.byref(stats)))
+    hs = (C.c_void_p * len(group))(*[s.handle for s in group])
+    abi.check(abi.lib().ps_pipeline_run_rank_group(hs, len(group), rank, k, board.encode(), p.ctypes.data, len(p),
+                                                   C.byref(ro.opts), out.ctypes.data, C.byref(n), C.byref(stats)))
     if return_events:
         return out[:n.value].tolist(), stats, ro.events(stats)
     return out[:n.value].tolist(), stats
@@ -300,3 +304,31 @@ def pipeline_run(stages, prompt, max_new_tokens: int, mode: int = abi.PS_MODE_PI
     if return_events:
         return out[:n.value].tolist(), stats, ro.events(stats)
     return out[:n.value].tolist(), stats
+
+
+def group_call(group, fn):
+    """fn(member) on every member of a tensor-parallel group concurrently (one
+    thread each, as the ABI requires); returns the leader's result after
+    checking the members agree."""
+    import threading
+    res, err = [None] * len(group), [None] * len(group)
+
+    def go(i):
+        try:
+            res[i] = fn(group[i])
+        except BaseException as e:  # noqa: BLE001
+            err[i] = e
+
+    th = [threading.Thread(target=go, args=(i,)) for i in range(1, len(group))]
+    for t in th:
+        t.start()
+    go(0)
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    for r in res[1:]:
+        if r != res[0]:
+            raise RuntimeError(f"tensor-parallel members disagree: {r} vs {res[0]}")
+    return res[0]

@@ -53,3 +53,19 @@ def test_reference_arm_nonzero_rank_exits_silently():
                         "toy-drafter", "--target", "toy-verifier", "--steps", "1", "--warmup", "0"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+@pytest.mark.parametrize("n,cfg,want", [
+    (2, "c2", [[0], [1]]),
+    (3, "c3", [[0], [1], [2]]),
+    (4, "c4", [[0], [1], [2, 3]]),
+    (8, "c4", [[0], [1], [4, 5, 6, 7]]),
+])
+def test_layouts_follow_the_paper(n, cfg, want):
+    """N > 1: each model on its own GPU(s), the target tensor parallel over the
+    rest (8 GPUs 1B@0, 8B@1, 70B TP4@4-7; 4 GPUs 70B TP2@2-3)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+    shapes = [synth.preset(m) for m in bench.LAYOUT_CONFIGS[cfg]["models"]]
+    assert bench.layout_for(n, cfg, shapes) == want
