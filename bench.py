@@ -39,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tokens/s batch-1 greedy & speedup vs M_k autoregressive; verify HBM GB/s"
-STEP_IN_BYTES = 176     # sizeof(StepIn): uploaded per forward (host -> device)
+STEP_IN_BYTES = 304     # sizeof(StepIn): uploaded per forward (host -> device)
 STEP_OUT_BYTES = 144    # sizeof(StepOut): read back per forward (device -> host, mapped pinned)
 
 

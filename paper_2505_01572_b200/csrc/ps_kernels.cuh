@@ -26,14 +26,15 @@
 
 namespace ps {
 
-constexpr int kMaxRows = 32;       // max rows per forward (w <= 31)
+constexpr int kMaxRows = 32;       // max rows of a forward with the lm_head (verify / draft: w <= 31)
+constexpr int kRowsCap = 64;       // max rows of any forward (prefill chunks: the 64-row bucket)
 constexpr int kAttnChunk = 64;     // keys per split-KV chunk (absolute positions)
 
 // Split-bf16 activations (reading R28).  Every bf16 operand the
 // path derives from an fp32 activation is stored as a PAIR hi = bf16(v),
 // lo = bf16(v - hi) (~16 significant bits): the GEMM operands x∘g, attention
-// output and SwiGLU output (buffers of 2*kMaxRows rows: hi rows [0, 32), lo
-// rows [32, 64); the tensor cores take both, W·hi + W·lo accumulated in fp32),
+// output and SwiGLU output (buffers of 2*kRowsCap rows: hi rows [0, 64), lo
+// rows [64, 128); the tensor cores take both, W·hi + W·lo accumulated in fp32),
 // the query and softmax probabilities inside attention, and the KV cache.
 // With plain bf16 activations a 32-layer LLaMA-3.1-8B forward drifts ~4% of
 // max|logit| from exact arithmetic (scripts/precision_probe.py), twice the
@@ -50,7 +51,7 @@ PS_DEV uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
 constexpr int kKvPlanes = 4;
 
 struct StepIn {                    // written by the host before every forward
-  int32_t R;                       // rows in this forward, 1..kMaxRows
+  int32_t R;                       // rows in this forward, 1..kRowsCap (<= kMaxRows with the lm_head)
   int32_t pos0;                    // absolute position of row 0
   int32_t w;                       // drafts in the window (rows 1..w), verify only
   int32_t flags;                   // kFlagLogits | kFlagSynth
@@ -60,7 +61,7 @@ struct StepIn {                    // written by the host before every forward
   int32_t gen;                     // forwards so far on this stage (megakernel counter target)
   int32_t gen_head;                // forwards with lm_head so far (targets of the head phases)
   int32_t pad2[3];
-  int32_t tokens[kMaxRows];        // row tokens: [pending, d_0, ..., d_{w-1}]
+  int32_t tokens[kRowsCap];        // row tokens: [pending, d_0, ..., d_{w-1}] (or a prefill chunk)
 };
 constexpr int kFlagLogits = 1;
 constexpr int kFlagSynth = 2;
@@ -108,8 +109,10 @@ struct GemmParams {
   int amax_par;                    // 1: amax has two [kMaxRows] slots selected by gen_head parity
   // EPI_STORE
   float* out; int ld_out;
-  // stream-K fixup
+  // stream-K fixup (per 16-row chunk of the 64-row bucket: ws + chunk * ws_chunk floats,
+  // counters + chunk * cnt_chunk)
   float* ws; unsigned* counters;
+  long long ws_chunk; int cnt_chunk;
   int ll;                          // 1: flag-in-data partials (below); 0: release counter + reducer spin
   int ll_tag;                      // distinct per GEMM of a forward (< 1024); flag = gen << 10 ^ ll_tag
   unsigned long long* dbg;         // optional per-CTA %globaltimer trace [grid][4]
@@ -141,29 +144,35 @@ PS_DEV void load_acc(uint32_t taddr, float* v) {
 // partials combined in fixed order) and, for QKV, each row's KV slot offset.
 template <int RP>
 PS_DEV void epi_prepare(const GemmParams& p, int e, int R, int pos0, float* scratch, float* rstd, long long* kvrow) {
-  // rstd_r from the producer's sum-of-squares slots: 128/RP threads per row
-  // each load their slots in one batch; partials are combined in fixed order.
+  // rstd_r from the producer's sum-of-squares slots in a FIXED order whatever
+  // the rows bucket (row-bucket invariance): part q = 0..7 of row r sums the
+  // slots j = q, q + 8, ... in increasing j; the 8 parts are then added in
+  // order.  128 threads cover 16 rows x 8 parts per pass.
   {
-    constexpr int TPR = 128 / RP;            // threads per row
-    constexpr int MAXS = 64 / TPR;           // slots per thread (ss_n <= 64, d <= 8192)
-    const int row = e % RP, part = e / RP;
-    float sv[MAXS];
+    constexpr int MAXS = 8;                  // slots per part (ss_n <= 64, d <= 8192)
+    const int part = e & 7;
 #pragma unroll
-    for (int k = 0; k < MAXS; ++k) {
-      const int j = part + k * TPR;
-      sv[k] = (p.ss_in != nullptr && j < p.ss_n) ? p.ss_in[row * p.ss_ld + j] : 0.f;
+    for (int r0 = 0; r0 < RP; r0 += 16) {
+      const int row = r0 + (e >> 3);
+      float sv[MAXS];
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) {
+        const int j = part + 8 * k;
+        sv[k] = (p.ss_in != nullptr && j < p.ss_n) ? p.ss_in[row * p.ss_ld + j] : 0.f;
+      }
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < MAXS; ++k) s += sv[k];
+      scratch[row * 8 + part] = s;
     }
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < MAXS; ++k) s += sv[k];
-    scratch[part * RP + row] = s;
   }
   named_bar(1, 128);
   if (e < RP) {
     float r_ = 1.0f;
     if (p.ss_in != nullptr) {
       float s = 0.f;
-      for (int k = 0; k < 128 / RP; ++k) s += scratch[k * RP + e];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += scratch[e * 8 + k];
       r_ = rsqrtf(s * p.inv_d + p.eps);
     }
     rstd[e] = r_;
@@ -355,7 +364,12 @@ template <int RP, bool kLL = false>
 PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long long seg_end, long long U, int G, int c,
                         int kbt, float* v, int e, int lane, int quarter, int R, int pos0, float* scratch,
                         unsigned long long* red, const float* rstd, const long long* kvrow, volatile int* flag,
-                        float4* stage = nullptr, int stage_f4 = 0) {
+                        float4* stage = nullptr, int stage_f4 = 0, int r0 = 0) {
+  // r0: first row of this 16-row chunk (64-row bucket; 0 otherwise): rows r of
+  // the chunk are rows r0 + r of the forward (rstd / kvrow / pos0 are passed
+  // already offset); each chunk has its own partials and counters
+  float* const wsb = p.ws + (size_t)(r0 / 16) * p.ws_chunk;
+  unsigned* const cnt = p.counters + (r0 / 16) * p.cnt_chunk;
   bool finalized = false;
   // Epilogue operands that do not depend on this tile's result (residual x and
   // its gain; RoPE cos/sin) are loaded BEFORE the stream-K wait, so their
@@ -372,7 +386,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
     const bool ok = f < p.N;
     pre_g = ok ? __bfloat162float(p.gain[f]) : 0.f;
 #pragma unroll
-    for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+    for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)(r0 + r) * p.ld_x + f] : 0.f;
   }
   if (will_fin && p.mode == EPI_QKV && t < p.t2) {
     const int f = t < p.t1 ? t * 128 + e : (t - p.t1) * 128 + e;
@@ -396,7 +410,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
       const int seg = c - first;
       const uint32_t flag = ((uint32_t)p.step->gen << 10) ^ (uint32_t)p.ll_tag;
-      unsigned long long* wsp = reinterpret_cast<unsigned long long*>(p.ws) + (size_t)(t * p.maxseg) * RP * 128;
+      unsigned long long* wsp = reinterpret_cast<unsigned long long*>(wsb) + (size_t)(t * p.maxseg) * RP * 128;
       const int R2 = (R + 1) >> 1;               // live row pairs
       if (seg != 0) {                            // publish: data + flag, nothing else
 #pragma unroll
@@ -412,7 +426,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       const int first = sk_owner(U, G, tile_u0);
       const int nseg = sk_owner(U, G, tile_u0 + kbt - 1) - first + 1;
       const int seg = c - first;
-      float4* wsp = reinterpret_cast<float4*>(p.ws + (size_t)(t * p.maxseg) * RP * 128);
+      float4* wsp = reinterpret_cast<float4*>(wsb + (size_t)(t * p.maxseg) * RP * 128);
       constexpr int V4 = RP / 4;
       const int R4 = (R + 3) >> 2;               // float4s per thread that hold live rows
       if (seg != 0) {
@@ -428,13 +442,13 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       if (seg != 0) {
         named_bar(1, 128);
         if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
-        if (e == 0) red_release_add_gpu(&p.counters[t], 1u);
+        if (e == 0) red_release_add_gpu(&cnt[t], 1u);
         break;
       }
       if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 0);
       if (e == 0) {
-        spin_until_gpu(&p.counters[t], (unsigned)(nseg - 1));
-        p.counters[t] = 0u;                    // ready for the next forward
+        spin_until_gpu(&cnt[t], (unsigned)(nseg - 1));
+        cnt[t] = 0u;                           // ready for the next forward
       }
       named_bar(1, 128);
       if (e == 0) PS_TRACE_STAMP(p.dbg, c * 4 + 1);
@@ -455,7 +469,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       if (f < p.N) {
 #pragma unroll
         for (int r = 0; r < RP; ++r)
-          if (r < R) p.out[(size_t)r * p.ld_out + f] = v[r];
+          if (r < R) p.out[(size_t)(r0 + r) * p.ld_out + f] = v[r];
       }
     } else if (p.mode == EPI_RESID) {
       const int f = t * 128 + e;
@@ -463,7 +477,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       if constexpr (!kPre) {
         pre_g = ok ? __bfloat162float(p.gain[f]) : 0.f;
 #pragma unroll
-        for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)r * p.ld_x + f] : 0.f;
+        for (int r = 0; r < RP; ++r) pre_x[r] = (r < R && ok) ? p.x[(size_t)(r0 + r) * p.ld_x + f] : 0.f;
       }
       const float g = pre_g;
       const float* xo = pre_x;
@@ -473,8 +487,8 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
         float sq = 0.f;
         if (ok) {
           const float xn = xo[r] + v[r];
-          p.x[(size_t)r * p.ld_x + f] = xn;
-          split_bf16(xn * g, p.xg[(size_t)r * p.ld_xg + f], p.xg[(size_t)(r + kMaxRows) * p.ld_xg + f]);
+          p.x[(size_t)(r0 + r) * p.ld_x + f] = xn;
+          split_bf16(xn * g, p.xg[(size_t)(r0 + r) * p.ld_xg + f], p.xg[(size_t)(r0 + r + kRowsCap) * p.ld_xg + f]);
           sq = xn * xn;
         }
         sq = warp_sum(sq);
@@ -482,7 +496,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
       }
       named_bar(1, 128);
       if (e < R)
-        p.ss_out[(size_t)e * p.ss_out_ld + t] =
+        p.ss_out[(size_t)(r0 + e) * p.ss_out_ld + t] =
             ((scratch[0 * RP + e] + scratch[1 * RP + e]) + scratch[2 * RP + e]) + scratch[3 * RP + e];
       named_bar(1, 128);
     } else if (p.mode == EPI_SWIGLU) {
@@ -497,8 +511,8 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
             if (r < R) {
               const float gt = scratch[e * (RP + 1) + r];
               const float up = scratch[(e + 64) * (RP + 1) + r];
-              split_bf16(gt / (1.0f + __expf(-gt)) * up, p.h[(size_t)r * p.ld_h + f],
-                         p.h[(size_t)(r + kMaxRows) * p.ld_h + f]);
+              split_bf16(gt / (1.0f + __expf(-gt)) * up, p.h[(size_t)(r0 + r) * p.ld_h + f],
+                         p.h[(size_t)(r0 + r + kRowsCap) * p.ld_h + f]);
             }
           }
         }
@@ -535,7 +549,7 @@ PS_DEV bool epi_segment(const GemmParams& p, int t, long long seg_begin, long lo
         if (kind == 0) {
 #pragma unroll
           for (int r = 0; r < RP; ++r)
-            if (r < R) p.q[(size_t)r * p.ld_q + f] = v[r];
+            if (r < R) p.q[(size_t)(r0 + r) * p.ld_q + f] = v[r];
         } else {
           const int kh = f / hd;
           const size_t plane = (size_t)p.hkv * p.page_size * hd;   // elements per (layer, plane)
@@ -626,7 +640,7 @@ PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
         xd[0] = make_float4(xf[0], xf[1], xf[2], xf[3]);
         xd[1] = make_float4(xf[4], xf[5], xf[6], xf[7]);
         *reinterpret_cast<uint4*>(p.xg + (size_t)r * p.ld_xg + col + 8 * k) = make_uint4(oh[0], oh[1], oh[2], oh[3]);
-        *reinterpret_cast<uint4*>(p.xg + (size_t)(r + kMaxRows) * p.ld_xg + col + 8 * k) =
+        *reinterpret_cast<uint4*>(p.xg + (size_t)(r + kRowsCap) * p.ld_xg + col + 8 * k) =
             make_uint4(ol[0], ol[1], ol[2], ol[3]);
       }
     }
@@ -643,7 +657,7 @@ PS_DEV void embed_row(const EmbedParams& p, int r, int tid /* 0..127 */) {
 // operand x∘g and the per-128-column sums of squares -- the EPI_RESID epilogue
 // of the single-GPU path with the all-reduce folded in.
 struct TpParams {
-  const float* part[8];            // rank q's partial [kMaxRows][d] (peer memory for q != rank)
+  const float* part[8];            // rank q's partial [kRowsCap][d] (peer memory for q != rank)
   int n;                           // tp_size
   float* x; int ld_x;
   __nv_bfloat16* xg; int ld_xg; const __nv_bfloat16* gain;
@@ -671,7 +685,7 @@ PS_DEV void tp_reduce_unit(const TpParams& p, int r, int t, int lane) {
   split_bf16(xn.z * gb.x, h[2], l[2]);
   split_bf16(xn.w * gb.y, h[3], l[3]);
   *reinterpret_cast<uint2*>(p.xg + (size_t)r * p.ld_xg + f) = make_uint2(pack2(h[0], h[1]), pack2(h[2], h[3]));
-  *reinterpret_cast<uint2*>(p.xg + (size_t)(r + kMaxRows) * p.ld_xg + f) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
+  *reinterpret_cast<uint2*>(p.xg + (size_t)(r + kRowsCap) * p.ld_xg + f) = make_uint2(pack2(l[0], l[1]), pack2(l[2], l[3]));
   float sq = xn.x * xn.x + xn.y * xn.y + xn.z * xn.z + xn.w * xn.w;
   sq = warp_sum(sq);
   if (lane == 0) p.ss_out[(size_t)r * p.ss_out_ld + t] = sq;
@@ -990,7 +1004,7 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
         const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
         __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
 #pragma unroll
-        for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kMaxRows * p.ld_out]);
+        for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kRowsCap * p.ld_out]);
       }
       if (tid == 0) p.counters[kh * p.max_rb + rb] = 0u;
     }
@@ -1049,7 +1063,7 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
     const int r = mg / g, h = kh * g + mg % g;
     __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
 #pragma unroll
-    for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kMaxRows * p.ld_out]);
+    for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kRowsCap * p.ld_out]);
   }
 }
 

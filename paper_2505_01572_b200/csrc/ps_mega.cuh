@@ -58,7 +58,9 @@ constexpr unsigned kSpinCapNs = 64;
 
 constexpr int kMegaThreads = 224;   // 7 warps: W producer, MMA, 4 epilogue, X loader
 // ring depth per rows bucket (fills the SM's shared memory next to the 53 KB attention area)
-template <int RP> constexpr int mega_stages() { return RP == 16 ? 7 : 5; }
+// (RP = 64: the prefill bucket, 64 rows per forward, epilogues in 16-row chunks)
+template <int RP> constexpr int mega_stages() { return RP == 16 ? 7 : RP == 32 ? 5 : 4; }
+template <int RP> constexpr int epi_rows() { return RP < 32 ? RP : 32; }   // rows per epilogue pass (scratch)
 
 template <int RP, int STAGES = mega_stages<RP>()>
 struct MegaSmem {
@@ -67,7 +69,7 @@ struct MegaSmem {
   static constexpr int kXBytes = 2 * RP * 64 * 2;   // split-bf16 activation tiles: hi, then lo
   static constexpr int kOffX = kMegaStages * kABytes;
   static constexpr int kOffScratch = kOffX + kMegaStages * kXBytes;
-  static constexpr int kOffRed = kOffScratch + 128 * (RP + 1) * 4;
+  static constexpr int kOffRed = kOffScratch + 128 * (epi_rows<RP>() + 1) * 4;
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
   static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 127) / 128 * 128;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   MegaPhase* sph = (MegaPhase*)(smem + L::kOffPhase);
   StepIn* sstep = (StepIn*)(smem + L::kOffStep);
 
-  constexpr int kTmemCols = RP == 16 ? 64 : 128;        // 2 accumulators x N = 2 RP columns
+  constexpr int kTmemCols = 4 * RP;                     // 2 accumulators x N = 2 RP columns
   constexpr uint32_t kIdesc = idesc_bf16_f32<128, 2 * RP>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
@@ -215,9 +217,9 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         }
         const int slot = it % kMegaStages;
         mbar_wait(&empty[slot], ((it / kMegaStages) & 1) ^ 1);
-        // hi rows [0, RP) and lo rows [kMaxRows, kMaxRows + RP) of the operand
+        // hi rows [0, RP) and lo rows [kRowsCap, kRowsCap + RP) of the operand
         tma_load_2d(sX + slot * L::kXBytes, Q.mX, &full[slot], kb * 64, 0, kEvictLast);
-        tma_load_2d(sX + slot * L::kXBytes + RP * 128, Q.mX, &full[slot], kb * 64, kMaxRows, kEvictLast);
+        tma_load_2d(sX + slot * L::kXBytes + RP * 128, Q.mX, &full[slot], kb * 64, kRowsCap, kEvictLast);
         ++it;
       });
     }
@@ -357,18 +359,40 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
               if (u == ub) PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 5);
               PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 6);
             }
-            float v[RP];
-            load_acc<RP>(tmem + ((uint32_t)(quarter * 32) << 16) + acc * 2 * RP, v);
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
-            ++nacc;
-            u = seg_end;
-            // (the attention area stages stream-K partials, except in QKV phases:
-            // the next attention phase's K/V chunk is prefetched into it then)
-            epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch,
-                                  red, rstd, kvrow, flag,
-                                  gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
-                                  L::kAttnBytes / 16);
+            const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + acc * 2 * RP;
+            if constexpr (RP <= 32) {
+              float v[RP];
+              load_acc<RP>(tacc, v);
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+              ++nacc;
+              u = seg_end;
+              // (the attention area stages stream-K partials, except in QKV phases:
+              // the next attention phase's K/V chunk is prefetched into it then)
+              epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch,
+                                    red, rstd, kvrow, flag,
+                                    gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
+                                    L::kAttnBytes / 16);
+            } else {
+              // 64-row bucket: the epilogue in 16-row chunks (hi columns [16q, 16q + 16),
+              // lo columns RP + 16q ..); the accumulator is released after the last chunk
+              u = seg_end;
+              for (int r0 = 0; r0 < R; r0 += 16) {
+                float v[16], lo[16];
+                tmem_ld16(tacc + r0, v);
+                tmem_ld16(tacc + RP + r0, lo);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] += lo[r];
+                if (r0 + 16 >= R) {
+                  tc_fence_before();
+                  mbar_arrive(&tempty[acc]);
+                }
+                epi_segment<16, false>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter,
+                                       min(16, R - r0), pos0 + r0, scratch, red, rstd + r0, kvrow + r0, flag,
+                                       nullptr, 0, r0);
+              }
+              ++nacc;
+            }
             if (et == 0) PS_TRACE_STAMP(P.dbg, ((size_t)c * P.n_ph + ph) * 8 + 7);
           }
         }

@@ -51,7 +51,7 @@ struct ps_stage {
   std::vector<const __nv_bfloat16*> lw;   // [L][9]
   std::vector<LayerMaps> maps;
   CUtensorMap map_lm;
-  CUtensorMap map_xg[2], map_att[2], map_h[2];   // per rows bucket (16, 32)
+  CUtensorMap map_xg[3], map_att[3], map_h[3];   // per rows bucket (16, 32, 64)
   // KV pool (borrowed) + paging
   __nv_bfloat16* kv = nullptr;
   long long page_elems = 0;
@@ -71,9 +71,9 @@ struct ps_stage {
   double last_fwd_ms = 0, sum_fwd_ms = 0;
   long long n_fwd = 0;
   // megakernel: phase tables per (bucket, with_head), device tensor maps, counters
-  MegaPhase* mega_ph[4] = {nullptr, nullptr, nullptr, nullptr};
-  CUtensorMap* mega_maps[4] = {nullptr, nullptr, nullptr, nullptr};
-  int mega_n[4] = {0, 0, 0, 0};
+  MegaPhase* mega_ph[6] = {};          // per (rows bucket, with lm_head)
+  CUtensorMap* mega_maps[6] = {};
+  int mega_n[6] = {};
   unsigned* mega_done = nullptr;
   unsigned long long* mega_dbg = nullptr;   // PS_TRACE builds only: timeline stamps
   unsigned long long* epi_dbg = nullptr;
@@ -81,7 +81,7 @@ struct ps_stage {
   unsigned gen = 0, gen_head = 0;
   int n_ctas = 0;                    // megakernel grid (persistent CTAs, <= #SMs)
   // tensor parallelism (a14): this rank's exchange buffer = [phase counters |
-  // partial [2][kMaxRows][d] fp32 | argmax keys [2][kMaxRows] u64]; peers[q] is
+  // partial [2][kRowsCap][d] fp32 | argmax keys [2][kMaxRows] u64]; peers[q] is
   // rank q's buffer as mapped in this process (peer memory for q != tp_rank)
   int tp_rank = 0, tp_size = 1;
   int vocab_full = 0, vocab_off = 0;
@@ -91,6 +91,8 @@ struct ps_stage {
   bool peer_ipc[8] = {};
   bool tp_connected = false;
   size_t ws_bytes = 0;
+  long long ws_chunk = 0;            // floats per 16-row chunk region of the stream-K workspace
+  int cnt_chunk = 0;
   // asynchronous verify (ps_verify_async / ps_verify_wait)
   bool inflight = false;
   long long if_n = 0;                // len(O_i) when the pass was enqueued
@@ -119,7 +121,8 @@ struct ps_stage {
   std::vector<int32_t> S_host;
 };
 
-static int bucket_rp(int b) { return b == 0 ? 16 : 32; }
+// rows buckets: 16 and 32 (forwards with the lm_head: verify / draft), 64 (prefill chunks)
+static int bucket_rp(int b) { return b == 0 ? 16 : b == 1 ? 32 : 64; }
 
 // Device-wide setup of a stage's device: the shared GEMM/attention attributes
 // plus the megakernel instantiations (per device, so every GPU of a process).
@@ -128,10 +131,11 @@ static ps_status init_stage_device(int device) {
   if ((st = init_device_globals(device)) != PS_OK) return st;
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(mega_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<64>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
   return PS_OK;
 }
-static int bucket_of(int R) { return R <= 16 ? 0 : 1; }
+static int bucket_of(int R) { return R <= 16 ? 0 : R <= 32 ? 1 : 2; }
 
 // Calls that change or use the stage are refused while an asynchronous pass
 // is in flight (ps_verify_async ... ps_verify_wait).
@@ -197,6 +201,8 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
   p.step = S->d_in;
   p.ws = S->ws;
   p.counters = S->counters;
+  p.ws_chunk = S->ws_chunk;
+  p.cnt_chunk = S->cnt_chunk;
   p.ll = 1;
   p.ll_tag = 1 + kind + 8 * l;     // per-kernel path; the megakernel re-tags by phase index
   switch (kind) {
@@ -268,7 +274,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       p.ss_out = S->ss; p.ss_out_ld = S->ss_ld;
       if (S->tp_size > 1) {   // row-parallel: partial -> exchange slot 1
         p.mode = EPI_STORE;
-        p.out = (float*)(S->xch + S->off_part) + (size_t)kMaxRows * d; p.ld_out = d;
+        p.out = (float*)(S->xch + S->off_part) + (size_t)kRowsCap * d; p.ld_out = d;
       }
       hm = HostMaps{&M.d, &M.d, &M.d, &S->map_h[b]};
       return;
@@ -334,7 +340,7 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     TpParams& t = P.tp;
     t.n = S->tp_size;
     for (int q = 0; q < S->tp_size; ++q)
-      t.part[q] = (const float*)(S->peers[q] + S->off_part) + (after_down ? (size_t)kMaxRows * sh.d_model : 0);
+      t.part[q] = (const float*)(S->peers[q] + S->off_part) + (after_down ? (size_t)kRowsCap * sh.d_model : 0);
     t.x = S->x; t.ld_x = sh.d_model; t.xg = S->xg; t.ld_xg = S->xg_ld;
     t.gain = !after_down ? S->lw[(size_t)l * 9 + PS_N_MLP]
                          : (l + 1 < sh.n_layers ? S->lw[(size_t)(l + 1) * 9 + PS_N_ATTN] : S->final_norm);
@@ -421,9 +427,12 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   } else if (b == 0) {
     cfg.dynamicSmemBytes = MegaSmem<16>::kBytes;
     e = cudaLaunchKernelEx(&cfg, mega_kernel<16>, mp);
-  } else {
+  } else if (b == 1) {
     cfg.dynamicSmemBytes = MegaSmem<32>::kBytes;
     e = cudaLaunchKernelEx(&cfg, mega_kernel<32>, mp);
+  } else {
+    cfg.dynamicSmemBytes = MegaSmem<64>::kBytes;
+    e = cudaLaunchKernelEx(&cfg, mega_kernel<64>, mp);
   }
   if (e != cudaSuccess) return fail(PS_E_CUDA, "megakernel launch: %s", cudaGetErrorString(e));
   g_launches++;
@@ -496,7 +505,7 @@ ps_status ps_stage_destroy(ps_stage* S) {
   if (!S) return PS_OK;
   cudaSetDevice(S->device);
   if (S->stream) cudaStreamSynchronize(S->stream);
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 6; ++k) {
     if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
     if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
   }
@@ -524,7 +533,7 @@ ps_status ps_stage_destroy(ps_stage* S) {
 
 // ---------------------------------------------------------------- tensor-parallel wiring
 static void drop_tables(ps_stage* S) {   // phase tables embed peer pointers: rebuild after (re)connect
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 6; ++k) {
     if (S->mega_ph[k]) cudaFree(S->mega_ph[k]);
     if (S->mega_maps[k]) cudaFree(S->mega_maps[k]);
     S->mega_ph[k] = nullptr;
@@ -536,8 +545,8 @@ static void drop_tables(ps_stage* S) {   // phase tables embed peer pointers: re
 // and copies synchronously, which would wait for a peer rank's running
 // megakernel that is itself waiting for this rank's forward.
 static ps_status build_all_tables(ps_stage* S) {
-  for (int b = 0; b < 2; ++b)
-    for (int h = 0; h < 2; ++h) {
+  for (int b = 0; b < 3; ++b)
+    for (int h = 0; h < (b < 2 ? 2 : 1); ++h) {   // the 64-row bucket never runs the lm_head
       ps_status st = build_mega(S, b, h != 0);
       if (st != PS_OK) return st;
     }
@@ -744,24 +753,24 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaHostAlloc(&S->h_out, sizeof(StepOut), cudaHostAllocMapped));
   S_TRY(cudaHostGetDevicePointer((void**)&S->h_out_dev, S->h_out, 0));
   memset(S->h_in, 0, 8 * sizeof(StepIn));
-  S_TRY(cudaMalloc(&S->x, (size_t)kMaxRows * d * 4));
-  // split-bf16 GEMM operands: hi rows [0, kMaxRows), lo rows [kMaxRows, 2 kMaxRows)
-  S_TRY(cudaMalloc(&S->xg, (size_t)2 * kMaxRows * d * 2));
-  S_TRY(cudaMalloc(&S->att, (size_t)2 * kMaxRows * hq * 2));
-  S_TRY(cudaMalloc(&S->h, (size_t)2 * kMaxRows * f * 2));
-  S_TRY(cudaMalloc(&S->q, (size_t)kMaxRows * hq * 4));
-  S_TRY(cudaMalloc(&S->ss, (size_t)kMaxRows * S->ss_ld * 4));
+  S_TRY(cudaMalloc(&S->x, (size_t)kRowsCap * d * 4));
+  // split-bf16 GEMM operands: hi rows [0, kRowsCap), lo rows [kRowsCap, 2 kRowsCap)
+  S_TRY(cudaMalloc(&S->xg, (size_t)2 * kRowsCap * d * 2));
+  S_TRY(cudaMalloc(&S->att, (size_t)2 * kRowsCap * hq * 2));
+  S_TRY(cudaMalloc(&S->h, (size_t)2 * kRowsCap * f * 2));
+  S_TRY(cudaMalloc(&S->q, (size_t)kRowsCap * hq * 4));
+  S_TRY(cudaMalloc(&S->ss, (size_t)kRowsCap * S->ss_ld * 4));
   S_TRY(cudaMalloc(&S->logits, (size_t)kMaxRows * sh.vocab * 4));
-  S_TRY(cudaMemset(S->x, 0, (size_t)kMaxRows * d * 4));
-  S_TRY(cudaMemset(S->xg, 0, (size_t)2 * kMaxRows * d * 2));
-  S_TRY(cudaMemset(S->att, 0, (size_t)2 * kMaxRows * hq * 2));
-  S_TRY(cudaMemset(S->h, 0, (size_t)2 * kMaxRows * f * 2));
-  S_TRY(cudaMemset(S->q, 0, (size_t)kMaxRows * hq * 4));
-  S_TRY(cudaMemset(S->ss, 0, (size_t)kMaxRows * S->ss_ld * 4));
-  for (int b = 0; b < 2; ++b) {
-    P_TRY(make_map(&S->map_xg[b], S->xg, 2 * kMaxRows, d, bucket_rp(b)));
-    P_TRY(make_map(&S->map_att[b], S->att, 2 * kMaxRows, hq, bucket_rp(b)));
-    P_TRY(make_map(&S->map_h[b], S->h, 2 * kMaxRows, f, bucket_rp(b)));
+  S_TRY(cudaMemset(S->x, 0, (size_t)kRowsCap * d * 4));
+  S_TRY(cudaMemset(S->xg, 0, (size_t)2 * kRowsCap * d * 2));
+  S_TRY(cudaMemset(S->att, 0, (size_t)2 * kRowsCap * hq * 2));
+  S_TRY(cudaMemset(S->h, 0, (size_t)2 * kRowsCap * f * 2));
+  S_TRY(cudaMemset(S->q, 0, (size_t)kRowsCap * hq * 4));
+  S_TRY(cudaMemset(S->ss, 0, (size_t)kRowsCap * S->ss_ld * 4));
+  for (int b = 0; b < 3; ++b) {
+    P_TRY(make_map(&S->map_xg[b], S->xg, 2 * kRowsCap, d, bucket_rp(b)));
+    P_TRY(make_map(&S->map_att[b], S->att, 2 * kRowsCap, hq, bucket_rp(b)));
+    P_TRY(make_map(&S->map_h[b], S->h, 2 * kRowsCap, f, bucket_rp(b)));
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
   const int n = S->n_ctas;
@@ -772,26 +781,32 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->gs_d = gemm_shape((d + 127) / 128, f, n, align);
   S->gs_lm = gemm_shape((sh.vocab + 127) / 128, d, n, align);
   S->lm_tiles = S->gs_lm.n_tiles;
-  size_t ws_elems = 0;
+  size_t ws_tiles = 0;
   int max_tiles = 0;
   for (const GemmShape* g : {&S->gs_qkv, &S->gs_o, &S->gs_gu, &S->gs_d, &S->gs_lm}) {
-    ws_elems = std::max(ws_elems, (size_t)g->n_tiles * g->maxseg * kMaxRows * 128);
+    ws_tiles = std::max(ws_tiles, (size_t)g->n_tiles * g->maxseg);
     max_tiles = std::max(max_tiles, g->n_tiles);
   }
+  // stream-K partials [tile][segment][128][rows] of one forward (rows <= 32; 8-byte
+  // LL words), or of each 16-row chunk of the 64-row bucket (regions of ws_chunk floats)
+  const size_t ws_chunk = ws_tiles * 16 * 128 * 2;
+  const size_t ws_elems = ws_tiles * kRowsCap * 128;
+  S->ws_chunk = (long long)ws_chunk;
+  S->cnt_chunk = max_tiles;
   // fp32 partials (release path) or (fp32, flag) words (LL path): 8 bytes each;
   // zeroed so no stale flag of a freed buffer can match
   S->ws_bytes = ws_elems * 8;
   S_TRY(cudaMalloc(&S->ws, S->ws_bytes));
   S_TRY(cudaMemset(S->ws, 0, S->ws_bytes));
-  S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * 4));
-  S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * 4));
+  S_TRY(cudaMalloc(&S->counters, (size_t)max_tiles * (kRowsCap / 16) * 4));
+  S_TRY(cudaMemset(S->counters, 0, (size_t)max_tiles * (kRowsCap / 16) * 4));
   S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * 8));
   S_TRY(cudaMemset(S->amax, 0, (size_t)kMaxRows * 8));
   // --- attention workspace
-  S->max_chunks = (S->max_seq + kMaxRows + kAttnChunk - 1) / kAttnChunk;
+  S->max_chunks = (S->max_seq + kRowsCap + kAttnChunk - 1) / kAttnChunk;
   {
     const int g = sh.n_heads / sh.n_kv_heads;
-    S->max_rb = (kMaxRows * g + 63) / 64;   // row blocks of >= 64 rows (megakernel: 64, standalone: 128)
+    S->max_rb = (kRowsCap * g + 63) / 64;   // attention row blocks of 64 query rows
   }
   S->attn_grid = std::min(sh.n_kv_heads * S->max_rb * S->max_chunks, 2 * n);
   const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * 128;
@@ -802,14 +817,14 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   // --- RoPE table
   {
     std::vector<float2> cs;
-    rope_table(sh, S->max_seq + kMaxRows, cs);
+    rope_table(sh, S->max_seq + kRowsCap, cs);
     S_TRY(cudaMalloc(&S->rope_cs, cs.size() * sizeof(float2)));
     S_TRY(cudaMemcpy(S->rope_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
   // --- paged KV
   S->kv = (__nv_bfloat16*)o->kv_pool;
   S->page_elems = (long long)sh.n_layers * kKvPlanes * sh.n_kv_heads * S->page_size * sh.head_dim;
-  const int lpages = (S->max_seq + kMaxRows + S->page_size - 1) / S->page_size;
+  const int lpages = (S->max_seq + kRowsCap + S->page_size - 1) / S->page_size;
   S->pages_total = S->page_elems ? (int)(o->kv_pool_bytes / (S->page_elems * 2)) : lpages;   // 0 layers: no KV
   S->page_of.assign(lpages, -1);
   for (int p = S->pages_total - 1; p >= 0; --p) S->free_pages.push_back(p);
@@ -827,7 +842,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   // --- exchange buffer: megakernel phase-completion counters (cumulative; see
   // ps_mega.cuh), tensor-parallel partials and argmax keys (read by peers)
   S->off_part = ((size_t)kMaxPhases(sh.n_layers) * 4 + 255) / 256 * 256;
-  S->off_keys = S->off_part + (size_t)2 * kMaxRows * d * 4;
+  S->off_keys = S->off_part + (size_t)2 * kRowsCap * d * 4;
   S->xch_bytes = S->off_keys + (size_t)2 * kMaxRows * 8;
   S_TRY(cudaMalloc(&S->xch, S->xch_bytes));
   S_TRY(cudaMemset(S->xch, 0, S->xch_bytes));
@@ -879,7 +894,7 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
     in->syn_p0 = (int32_t)g;
     in->syn_onpath = (g >= 0 && S->onpath == g) ? 1 : 0;
   }
-  for (int j = 0; j < kMaxRows; ++j) in->tokens[j] = j < R ? toks[j] : 0;
+  for (int j = 0; j < kRowsCap; ++j) in->tokens[j] = j < R ? toks[j] : 0;
   const int b = bucket_of(R);
   S->last_bucket = b;
   // Forwards are enqueued back to back (prefill chunks): each uses its own
@@ -915,9 +930,10 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   S->kv_len = keep_kv;
   free_pages_from(S, S->kv_len);
   update_onpath(S);
-  // forward positions [kv_len, n-1) in chunks of kMaxRows rows (no lm_head)
+  // forward positions [kv_len, n-1) in chunks of up to kRowsCap rows (no lm_head;
+  // the 64-row bucket: half the weight passes of 32-row chunks)
   while (S->kv_len < n - 1) {
-    const int R = (int)std::min<long long>(kMaxRows, n - 1 - S->kv_len);
+    const int R = (int)std::min<long long>(kRowsCap, n - 1 - S->kv_len);
     ps_status st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
     if (st != PS_OK) {
       S->kv_len = 0;   // KV state unknown: force a full recompute next time
@@ -936,7 +952,7 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
 static ps_status catch_up(ps_stage* S, int reserve_rows) {
   const long long n = (long long)S->tokens.size();
   while ((n - 1 - S->kv_len) + reserve_rows > kMaxRows) {
-    const int R = (int)std::min<long long>(kMaxRows, n - 1 - S->kv_len);
+    const int R = (int)std::min<long long>(kRowsCap, n - 1 - S->kv_len);
     ps_status st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
     if (st != PS_OK) return st;
     S->kv_len += R;

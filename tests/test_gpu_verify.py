@@ -284,3 +284,25 @@ def test_long_context_head_dim_128():
     check_logits(logits, ref["logits"])
     check_verify((a, nxt), ref, len(window))
     st.close()
+
+
+@pytest.mark.parametrize("name,layers,n", [("toy-verifier", None, 150), ("llama3.1-8b", 2, 200)])
+def test_prefill_64_row_chunks(name, layers, n):
+    """NEXT-3 prefill: the prompt runs through the 64-row bucket (64-token
+    chunks + a ragged tail, split-bf16 N = 128 MMAs, 16-row epilogue chunks).
+    Its KV is bit-identical to a one-token-at-a-time prefill (row-bucket
+    invariance), and the next verify matches the oracle."""
+    s, w, st = make(name, 31, layers=layers, max_seq=n + 40)
+    w64 = synth.weights_to_numpy(w)
+    prompt = list(synth.make_prompt(s.vocab, n, seed=32))
+    st.prefill(prompt)                       # 64 + 64 + 21 (+ ragged) rows
+    a1, n1, l1 = st.verify([], want_logits=True)
+    st.prefill(prompt[:1])
+    for i in range(2, n + 1):                # one row per forward (the 16-row bucket)
+        st.prefill(prompt[:i])
+    a2, n2, l2 = st.verify([], want_logits=True)
+    assert (a1, n1) == (a2, n2) and np.array_equal(l1, l2)
+    ref = L.verify(w64, s, prompt, [])
+    check_logits(l1, ref["logits"])
+    check_verify((a1, n1), ref, 0)
+    st.close()
