@@ -509,6 +509,22 @@ def main():
     prompt = [int(x) for x in synth.make_prompt(ts.vocab, args.prompt, seed=args.seed + 17 + rank)]
     L = abi.lib()
 
+    # --- prefill (NEXT-3): the prompt through the 64-row bucket, timed on
+    # the stage stream (device time); reported beside, not in, decode tokens/s
+    def timed_prefill(st, shape):
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(st.stream)
+        st.prefill(prompt)
+        p1.record(st.stream)
+        p1.synchronize()
+        ms = p0.elapsed_time(p1)
+        n = len(prompt) - 1                       # positions forwarded (the last token is pending)
+        flops = 2.0 * shape.n_params() * n + 4.0 * shape.n_layers * shape.q_dim * n * n / 2
+        return {"ms": ms, "tokens": n, "forwards": -(-n // 64), "TFLOP/s": flops / (ms * 1e-3) / 1e12,
+                "tokens_per_s": n / (ms * 1e-3)}
+    prefill = {"target": timed_prefill(target, ts), "drafter": timed_prefill(drafter, ds)}
+
     # --- M_K autoregressive: the lossless reference stream S and the AR baseline
     target.prefill(prompt)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -624,6 +640,7 @@ def main():
                    "parallelism": "single GPU, stages co-resident",
                    "l2": "inputs > L2 (16 GB of 8B weights streamed per verify pass)"},
         "speedup_vs_ar": value / ar_tok_s, "ar_tokens_per_s": ar_tok_s,
+        "prefill": dict(prefill, bf16_tflops_sustained=peaks.get("bf16_tflops_sustained")),
         "pipeline_run": modes,
         "tokens_per_step": tot_tokens / world / args.steps,
         "verify_pass": {"ms": pass_ms, "rows": R, "ctx": ctx, "bytes": pass_bytes, "GB/s": pass_gbs,
