@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--alpha", type=float, default=0.8)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-k3", action="store_true", help="N=1: skip the k=3 configs (BASELINE configs[2], [3])")
+    ap.add_argument("--k3-gen", type=int, default=128, help="N=1: tokens generated per k=3 config run")
     ap.add_argument("--config", choices=sorted(LAYOUT_CONFIGS), default=None,
                     help="N>1 layout workload (default: c2 at N=2, c3 at N=3, c4 otherwise)")
     ap.add_argument("--layers", type=int, default=None, help="N>1 smoke runs: cap every model's depth")
@@ -80,6 +82,7 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.samples = []            # (sm_mhz, max_mhz, [reason names], power_w)
+        self.util = []               # NVML GPU utilization % (kernel-active time share)
         self.energy_j = None
         self._stop = threading.Event()
         self._nv = None
@@ -101,6 +104,10 @@ class ClockSampler:
                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
         reasons = [n for n, b in zip(self.NAMES, bits) if r & b]
         pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+        try:
+            self.util.append(float(nv.nvmlDeviceGetUtilizationRates(h).gpu))
+        except Exception:
+            pass
         self.samples.append((float(sm), float(mx), reasons, pw))
 
     def _sample_smi(self):
@@ -150,6 +157,8 @@ class ClockSampler:
                "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self._nv else "nvidia-smi"}
         if pw:
             out["power_w_median"] = statistics.median(pw)
+        if self.util:
+            out["gpu_util_mean_pct"] = statistics.mean(self.util)
         return out
 
 
@@ -476,6 +485,62 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def k3_configs(args, peaks, reuse):
+    """N = 1, all stages co-resident: BASELINE configs[2] (68M -> 7B -> 13B,
+    1K prompt) and configs[3] (1B -> 8B -> 70B, 2K prompt; 159.6 GB of bf16
+    weights on the one GPU) through ps_pipeline_run in AR, tiered sync SD and
+    async PipeSpec modes (synthetic alpha per link, ps_run_opts.alpha).  Each
+    mode's output must equal M_K's autoregressive output.  Reports tokens/s
+    (decode wall clock), the speedup over AR and the target's verify pass."""
+    import torch
+
+    import synth
+    from paper_2505_01572_b200 import Stage, pipeline_run
+    from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
+    out = {}
+    for cname in ("c3", "c4"):
+        cfg = LAYOUT_CONFIGS[cname]
+        t0 = time.perf_counter()
+        try:
+            shapes = [synth.preset(m) for m in cfg["models"]]
+            gen, plen = args.k3_gen, cfg["prompt"]
+            max_seq = plen + gen + 128
+            ws = [reuse.get((m, args.seed + i)) or synth.make_weights(s, seed=args.seed + i, device="cuda")
+                  for i, (m, s) in enumerate(zip(cfg["models"], shapes))]
+            stages = [Stage(s, w, max_seq=max_seq, max_window=8) for s, w in zip(shapes, ws)]
+            prompt = [int(x) for x in synth.make_prompt(shapes[-1].vocab, plen, seed=args.seed + 17)]
+            gam = [0, 3, args.gamma]
+            res = {"models": cfg["models"], "prompt": plen, "gen": gen, "gammas": gam,
+                   "alpha_per_link": args.alpha, "workload": cfg["name"]}
+            ar_out, ar_st = pipeline_run([stages[-1]], prompt, gen, mode=PS_MODE_AR)
+            res["ar_tokens_per_s"] = gen / (ar_st.wall_ns / 1e9)
+            for mname, mode in (("sync_sd_tiered", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
+                for st_ in stages:
+                    st_.reset_timers()
+                o, st = pipeline_run(stages, prompt, gen, mode=mode, gammas=gam, alphas=[args.alpha] * 2,
+                                     seed=args.seed + 4321)
+                assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
+                inf = stages[-1].info()
+                pass_ms = inf["sum_fwd_ms"] / max(1, inf["n_fwd"])
+                R = gam[-1] + 1
+                ts = shapes[-1]
+                byts = ts.streamed_bytes_per_pass(R) + (plen + gen / 2 + R) * ts.kv_bytes_per_token()
+                res[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns,
+                              "verify_steps": [int(x) for x in st.verify_steps[:3]],
+                              "target_verify_pass_ms": pass_ms,
+                              "target_verify_frac": byts / (pass_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
+            for st_ in stages:
+                st_.close()
+            del stages, ws
+            torch.cuda.empty_cache()
+            res["seconds"] = time.perf_counter() - t0
+            out[cname] = res
+        except Exception as e:  # noqa: BLE001
+            out[cname] = {"error": repr(e)[:300]}
+            torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- ours
 def main():
     args = parse()
@@ -617,16 +682,19 @@ def main():
     runs += [(f"pipespec_async_lookahead{la}", PS_MODE_PIPESPEC, la) for la in (1, 2, 4)]
     for mname, mode, la in runs:
         torch.cuda.synchronize()
-        w0m = time.perf_counter()
-        out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g], lookaheads=[0, la])
-        torch.cuda.synchronize()
-        dtm = time.perf_counter() - w0m
+        with ClockSampler(local) as mclk:   # per-mode NVML utilization and board energy (NEXT-4)
+            w0m = time.perf_counter()
+            out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g], lookaheads=[0, la])
+            torch.cuda.synchronize()
+            dtm = time.perf_counter() - w0m
         assert out == S[:args.gen], f"{mname}: output differs from M_K autoregressive decoding"
         modes[mname] = {"tokens_per_s": len(out) / dtm, "decode_s": st_.wall_ns / 1e9,
                         "tokens_per_s_decode": len(out) / (st_.wall_ns / 1e9) if st_.wall_ns else None,
                         "verify_steps": int(st_.verify_steps[1]), "rollbacks": int(st_.rollbacks[0]),
                         # tokens appended per verify step of M_K (Fig.4's histogram)
-                        "accept_hist": {int(k): int(c) for k, c in enumerate(st_.accept_hist) if c}}
+                        "accept_hist": {int(k): int(c) for k, c in enumerate(st_.accept_hist) if c},
+                        "gpu_util_mean_pct": mclk.summary().get("gpu_util_mean_pct"),
+                        "j_per_token": (mclk.energy_j / len(out)) if mclk.energy_j is not None else None}
     value = tot_tokens / dev_s
     e2e = tot_tokens / wall_s
     fwd_per_step = g + 1
@@ -662,6 +730,10 @@ def main():
         # board energy counter across the timed region (this GPU's tokens; paper 4.5)
         line["energy"] = {"joules": clk.energy_j, "j_per_token": clk.energy_j / tokens,
                           "avg_w": clk.energy_j / max(wall_s, 1e-9), "source": "nvmlDeviceGetTotalEnergyConsumption"}
+    if world == 1 and not args.no_k3:
+        drafter.close()
+        target.close()
+        line["k3_configs"] = k3_configs(args, peaks, {(args.draft, args.seed): wd, (args.target, args.seed + 1): wt})
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, times, toks = oracle_sample(ds, ts, wd, wt, g, args.alpha, args.seed + 1234, 2)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",

@@ -132,10 +132,11 @@ def test_tp_matches_single_rank_decisions(toy_group):
 
 
 @pytest.mark.parametrize("name,layers,T", [("llama3.1-8b", 2, 2), ("llama3.1-8b", 1, 4),
-                                           ("llama3.1-70b", 1, 2)])
+                                           ("llama3.1-70b", 1, 2), ("llama3.1-70b", 2, 4)])
 def test_tp_paper_widths(name, layers, T):
-    """8B (TP2 / TP4) and 70B (TP2, the paper's "split across 2 GPUs")
-    widths at reduced depth: logits and decisions vs the fp64 oracle."""
+    """8B (TP2 / TP4) and 70B (TP2, the paper's "split across 2 GPUs", P:181;
+    TP4, the 8-GPU layout of config 4) widths with the FULL 128256 vocabulary
+    at reduced depth: logits and decisions vs the fp64 oracle."""
     s = synth.reduced_depth(synth.preset(name), layers)
     w = synth.make_weights(s, seed=41, device="cuda")
     w64 = synth.weights_to_numpy(w)

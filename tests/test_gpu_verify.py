@@ -137,6 +137,7 @@ def test_synthetic_override_matches_counter_generator(toy):
     ("llama3.2-1b", None, 96, 16),
     ("llama3.1-8b", 2, 160, 16),
     ("llama2-7b", 2, 96, 7),
+    ("llama2-13b", 2, 96, 8),        # config 3's target: MHA (40 / 40 heads), d = 5120
 ])
 def test_paper_shapes_parity(name, layers, plen, w):
     """Full-width shapes: logits within 2e-2*max|logit| of the fp64 oracle,
