@@ -22,6 +22,8 @@
 // row r by rstd_r = 1/sqrt(mean(x_r^2)+eps)  ((x∘g)·W^T scaled by rstd is the
 // RMSNorm'd product, PAPER-independent algebra).
 #pragma once
+#include <type_traits>
+
 #include "ps_device.cuh"
 
 namespace ps {
@@ -1013,7 +1015,10 @@ PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, 
 }
 
 // Combine of the chunk partials written by attn_run<.., false>: one warp per
-// output row (kh, m); lanes hold HD/32 dims.  Deterministic chunk order.
+// output row (kh, m); lanes hold HD/32 dims.  Per row M = max_c m_c, L = sum_c
+// 2^(m_c - M) l_c, O = sum_c 2^(m_c - M) O_c / L in chunk order.  Lane c loads
+// chunk c's (m, l) once (its scale reaches the other lanes by shuffles) and
+// the O loads of 4 chunks are issued before any is used.
 template <int HD, int kRB>
 PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
   const StepIn* st = p.step;
@@ -1023,6 +1028,7 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
   const int nchunks = (pos0 + R + kAttnChunk - 1) / kAttnChunk;
   const int lane = threadIdx.x & 31;
   constexpr int DPL = HD / 32;
+  using VecT = typename std::conditional<DPL == 4, float4, float2>::type;
   for (int item = gwarp; item < p.hkv * rows; item += nwarps_total) {
     const int kh = item / rows, mg = item % rows;
     const int rb = mg / kRB, m = mg % kRB;
@@ -1030,36 +1036,43 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
     float acc[DPL];
 #pragma unroll
     for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
-    // chunk `lane`'s (m, l) is loaded once and kept for both M and L (one
-    // round trip less when the context has <= 32 chunks); same arithmetic
-    float2 ml0 = make_float2(-INFINITY, 0.f);
-    if (lane < nchunks) ml0 = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + lane) * kRB + m) * 2));
-    float M = ml0.x;
-    for (int cc = lane + 32; cc < nchunks; cc += 32)
-      M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
+    float M = -INFINITY;
+    for (int c0 = 0; c0 < nchunks; c0 += 32)
+      if (c0 + lane < nchunks) M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + c0 + lane) * kRB + m) * 2));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float Lp = (ml0.x == -INFINITY) ? 0.f : exp2f(ml0.x - M) * ml0.y;
-    for (int cc = lane + 32; cc < nchunks; cc += 32) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
-      Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
+    float Lp = 0.f;
+    for (int c0 = 0; c0 < nchunks; c0 += 32) {
+      float sc = 0.f;                    // 2^(m_c - M) of chunk c0 + lane
+      if (c0 + lane < nchunks) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + c0 + lane) * kRB + m) * 2));
+        sc = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
+        Lp += sc * ml.y;
+      }
+      const int nh = min(32, nchunks - c0);
+      for (int q0 = 0; q0 < nh; q0 += 4) {
+        VecT ov[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < nh)
+            ov[q] = __ldcg(reinterpret_cast<const VecT*>(p.ws_o + ((rbase + c0 + q0 + q) * kRB + m) * HD + lane * DPL));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float sq = __shfl_sync(0xffffffffu, sc, (q0 + q) & 31);
+          if (q0 + q < nh) {
+            if constexpr (DPL == 4) {
+              acc[0] += sq * ov[q].x; acc[1] += sq * ov[q].y; acc[2] += sq * ov[q].z; acc[3] += sq * ov[q].w;
+            } else {
+              acc[0] += sq * ov[q].x; acc[1] += sq * ov[q].y;
+            }
+          }
+        }
+      }
     }
+    // fixed-order sum over chunks: lanes hold chunk-strided partials, reduce by tree
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
     const float invL = 1.0f / Lp;
-#pragma unroll 8
-    for (int cc = 0; cc < nchunks; ++cc) {
-      const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2);
-      const float sc = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
-      const float* op = p.ws_o + ((rbase + cc) * kRB + m) * HD + lane * DPL;
-      if constexpr (DPL == 4) {
-        const float4 o4 = __ldcg(reinterpret_cast<const float4*>(op));
-        acc[0] += sc * o4.x; acc[1] += sc * o4.y; acc[2] += sc * o4.z; acc[3] += sc * o4.w;
-      } else {
-        const float2 o2 = __ldcg(reinterpret_cast<const float2*>(op));
-        acc[0] += sc * o2.x; acc[1] += sc * o2.y;
-      }
-    }
     const int r = mg / g, h = kh * g + mg % g;
     __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
 #pragma unroll
