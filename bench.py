@@ -533,6 +533,16 @@ def k3_configs(args, peaks, reuse):
                    "alpha_per_link": args.alpha, "workload": cfg["name"]}
             ar_out, ar_st = pipeline_run([stages[-1]], prompt, gen, mode=PS_MODE_AR)
             res["ar_tokens_per_s"] = gen / (ar_st.wall_ns / 1e9)
+            # Table 1's grid: {sync, async} x {2-model (M_1 -> M_2), 3-model}
+            grid = {}
+            for mname, mode, sel in (("sync_sd_2model", PS_MODE_SYNC_SD, [1, 2]), ("pipespec_async_2model",
+                                                                                  PS_MODE_PIPESPEC, [1, 2])):
+                sub = [stages[i] for i in sel]
+                o, st = pipeline_run(sub, prompt, gen, mode=mode, gammas=[0, args.gamma], alphas=[args.alpha],
+                                     seed=args.seed + 4321)
+                assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
+                grid[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns}
+            res["table1_grid"] = grid
             for mname, mode in (("sync_sd_tiered", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
                 for st_ in stages:
                     st_.reset_timers()
@@ -548,6 +558,8 @@ def k3_configs(args, peaks, reuse):
                               "verify_steps": [int(x) for x in st.verify_steps[:3]],
                               "target_verify_pass_ms": pass_ms,
                               "target_verify_frac": byts / (pass_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
+                grid[mname.replace("sync_sd_tiered", "sync_sd_3model").replace("pipespec_async", "pipespec_async_3model")] = \
+                    {"tokens_per_s": res[mname]["tokens_per_s"], "speedup_vs_ar": res[mname]["speedup_vs_ar"]}
             for st_ in stages:
                 st_.close()
             del stages, ws

@@ -10,8 +10,9 @@ gamma, lookahead 0, AR steps when no valid draft.
 
 Acceptance is synthetic (reading R24): the verifier's emitted token follows a
 fixed random stream S (chained override with alpha = 1 above it) and the
-drafter agrees with it with probability alpha; both still run their real
-forwards.  Generations of --gen tokens restart from a 64-token prompt until
+drafter agrees with it with probability alpha (a new counter seed per
+generation: with one seed every generation would replay the same acceptance
+pattern); both still run their real forwards.  Generations of --gen tokens restart from a 64-token prompt until
 --steps verifier steps per (alpha, gamma) cell.
 
 Usage: python scripts/rate_check.py [--steps 10000] [--out profiles/r02_rate_check.json]
@@ -34,6 +35,9 @@ ap.add_argument("--steps", type=int, default=10000)
 ap.add_argument("--gen", type=int, default=512)
 ap.add_argument("--verifier", default="llama3.1-8b")
 ap.add_argument("--out", default=None)
+ap.add_argument("--pad", type=float, default=1.5, help="drafter steps of slack per verifier step (x (gamma + 3))")
+ap.add_argument("--alphas", default="0.5,0.8,0.95")
+ap.add_argument("--gammas", default="2,4,8")
 a = ap.parse_args()
 
 
@@ -63,26 +67,33 @@ dra.prefill(prompt)
 dra.draft(8)
 draft_ms = dra.info()["last_fwd_ms"]
 cells = []
-for alpha in (0.5, 0.8, 0.95):
-    for gamma in (2, 4, 8):
-        # the verifier emits S (alpha 1 above it); the drafter agrees with it w.p. alpha
-        ver.set_synthetic(S, len(prompt), level=1, top=2, alphas=[1.0], seed=77)
-        dra.set_synthetic(S, len(prompt), level=0, top=2, alphas=[alpha, 1.0], seed=77)
-        pad_ns = int((pass_ms + (gamma + 3) * draft_ms * 1.5 + 0.5) * 1e6)
+for alpha in [float(x) for x in a.alphas.split(",")]:
+    for gamma in [int(x) for x in a.gammas.split(",")]:
+        pad_ns = int((pass_ms + (gamma + 3) * draft_ms * a.pad + 0.5) * 1e6)
         steps = verify = tokens = 0
         runs = 0
+        wins = []
         while steps < a.steps:
-            out, st = pipeline_run([dra, ver], prompt, a.gen, mode=PS_MODE_PIPESPEC, gammas=[0, gamma],
-                                   lookaheads=[0, 0], virtual_ns=[0, pad_ns])
+            # the verifier emits S (alpha 1 above it); the drafter agrees with it
+            # w.p. alpha -- a fresh counter seed per generation, so the acceptance
+            # pattern over positions is a new draw every time
+            seed = 1000 * runs + 77
+            ver.set_synthetic(S, len(prompt), level=1, top=2, alphas=[1.0], seed=seed)
+            dra.set_synthetic(S, len(prompt), level=0, top=2, alphas=[alpha, 1.0], seed=seed)
+            out, st, ev = pipeline_run([dra, ver], prompt, a.gen, mode=PS_MODE_PIPESPEC, gammas=[0, gamma],
+                                       lookaheads=[0, 0], virtual_ns=[0, pad_ns], event_cap=20000, return_events=True)
             assert out == S[:a.gen], "output differs from the verifier's stream"
             steps += int(st.steps[1])
             verify += int(st.verify_steps[1])
             tokens += len(out)
             runs += 1
+            wins += [e["w"] for e in ev if e["stage"] == 1 and e["kind"] == 1]
         rho, en = verify / steps, tokens / steps
         cell = {"alpha": alpha, "gamma": gamma, "verifier_steps": steps, "generations": runs,
                 "rho_measured": rho, "rho_eq3": eq3(alpha, gamma), "EN_measured": en,
-                "EN_eq1": eq1(alpha, gamma, eq3(alpha, gamma)), "virtual_step_ms": pad_ns / 1e6}
+                "EN_eq1": eq1(alpha, gamma, eq3(alpha, gamma)), "virtual_step_ms": pad_ns / 1e6,
+                "mean_window": float(np.mean(wins)) if wins else 0.0,
+                "full_windows": float(np.mean([w == gamma for w in wins])) if wins else 0.0}
         cell["rho_abs_err"] = abs(rho - cell["rho_eq3"])
         cell["EN_rel_err"] = abs(en - cell["EN_eq1"]) / cell["EN_eq1"]
         cells.append(cell)
