@@ -26,6 +26,9 @@ ps_status ps_test_launch_overhead(int32_t smem, int32_t threads, int32_t grid, i
  * the B operand, N = 256 / 128), committing every `depth` units; writes the
  * slowest SM's ns per unit. */
 ps_status ps_test_tc_probe(int32_t mode, int32_t iters, int32_t depth, double* ns_per_unit);
+/* The same unit issued by the leader CTA of 2-CTA clusters as
+ * tcgen05.mma.cta_group::2 with M = 256 (16 KB of weights per SM per unit). */
+ps_status ps_test_tc_probe2(int32_t iters, int32_t depth, double* ns_per_unit);
 
 /* Protocol test double of the async runtime (no GPU): k stages over a
  * closed-form host "model" -- stage k-1 emits next(c) = (c[-1]*7919 +

@@ -140,6 +140,7 @@ _TEST_PROTOS = {
     "ps_test_board_unlink": (C.c_int32, [C.c_char_p]),
     "ps_test_launch_overhead": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "ps_test_tc_probe": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
+    "ps_test_tc_probe2": (C.c_int32, [C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
 }
 # trace build only (PS_LIB=.../libpipespec_trace.so)
 _TRACE_PROTOS = {"ps_trace_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64])}

@@ -306,3 +306,80 @@ extern "C" ps_status ps_test_tc_probe(int32_t mode, int32_t iters, int32_t depth
   *ns_per_unit = m / iters;
   return PS_OK;
 }
+
+// ---------------------------------------------------------------------------- CTA-pair probe
+// The same unit as mode 7 of tc_probe_kernel (4 MMAs of K = 16 over a 16 KB
+// weight tile per SM, N = 32), issued as tcgen05.mma.cta_group::2 with M = 256
+// by the leader CTA of each 2-CTA cluster: does the per-instruction cost stay,
+// doubling the weights consumed per SM per unit time?
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    tc_probe2_kernel(int iters, int depth, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  cluster_sync_all();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  constexpr uint32_t kI = idesc_bf16_f32<256, 32>();
+  if (rank == 0 && threadIdx.x == 32) {
+    const unsigned long long t0 = globaltimer();
+    uint32_t ph = 0;
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t a0 = smem_u32(sm + (i & 7) * 16384);
+      const uint32_t x0 = smem_u32(sm + 8 * 16384);
+      for (int k = 0; k < 4; ++k)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(smem_desc_sw128(a0 + 32 * k)), "l"(smem_desc_sw128(x0 + 32 * k)), "r"(kI), "r"(1u)
+                     : "memory");
+      if ((i + 1) % depth == 0) {
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+    mbar_wait(&bar, ph);
+    out[blockIdx.x] = globaltimer() - t0;
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+extern "C" ps_status ps_test_tc_probe2(int32_t iters, int32_t depth, double* ns_per_unit) {
+  const int smem = 9 * 16384 + 1024;
+  CU_TRY(cudaFuncSetAttribute(tc_probe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int dev = 0, sms = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  CU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  sms &= ~1;
+  unsigned long long* d;
+  CU_TRY(cudaMalloc(&d, sms * 8));
+  CU_TRY(cudaMemset(d, 0, sms * 8));
+  tc_probe2_kernel<<<sms, 128, smem>>>(iters, depth, d);
+  CU_TRY(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(sms);
+  CU_TRY(cudaMemcpy(h.data(), d, sms * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  double m = 0;
+  for (auto v : h) m = std::max(m, (double)v);
+  *ns_per_unit = m / iters;   // per pair-unit: 4 MMAs of M = 256 (16 KB of weights per SM)
+  return PS_OK;
+}

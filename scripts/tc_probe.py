@@ -14,3 +14,7 @@ for mode, name in MODES[int(sys.argv[1]) if len(sys.argv) > 1 else 0:]:
         ns = C.c_double()
         abi.test_check(L.ps_test_tc_probe(mode, 50000, depth, C.byref(ns)))
         print(f"{name:18s} depth {depth:2d}: {ns.value:8.1f} ns/unit", flush=True)
+
+ns = C.c_double()
+abi.test_check(L.ps_test_tc_probe2(50000, 4, C.byref(ns)))
+print(f"{'2-CTA M256 N32 4 MMA':18s} depth  4: {ns.value:8.1f} ns/unit (16 KB per SM)", flush=True)
