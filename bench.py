@@ -600,8 +600,8 @@ def main():
     max_seq = args.prompt + args.gen + 4 * g + 64
     wd = synth.make_weights(ds, seed=args.seed, device="cuda")
     wt = synth.make_weights(ts, seed=args.seed + 1, device="cuda")
-    drafter = Stage(ds, wd, max_seq=max_seq, max_window=g)
-    target = Stage(ts, wt, max_seq=max_seq, max_window=g)
+    drafter = Stage(ds, wd, max_seq=max_seq + 64, max_window=max(g, 8))
+    target = Stage(ts, wt, max_seq=max_seq + 64, max_window=max(g, 8))
     prompt = [int(x) for x in synth.make_prompt(ts.vocab, args.prompt, seed=args.seed + 17 + rank)]
     L = abi.lib()
 
@@ -711,11 +711,15 @@ def main():
     # lookahead sweep, with the verifier waiting for L >= 1 drafts (reading R7)
     runs = [("ar", PS_MODE_AR, 0), ("sync_sd", PS_MODE_SYNC_SD, 0), ("pipespec_async", PS_MODE_PIPESPEC, 0)]
     runs += [(f"pipespec_async_lookahead{la}", PS_MODE_PIPESPEC, la) for la in (1, 2, 4)]
+    # the best 2-model synchronous SD on these kernels: gamma swept (P:285 uses 8)
+    runs += [(f"sync_sd_gamma{gg}", PS_MODE_SYNC_SD, -gg) for gg in (2, 3, 5, 6, 8) if gg != g]
     for mname, mode, la in runs:
+        gmode = -la if la < 0 else g
+        la = max(la, 0)
         torch.cuda.synchronize()
         with ClockSampler(local) as mclk:   # per-mode NVML utilization and board energy (NEXT-4)
             w0m = time.perf_counter()
-            out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, g], lookaheads=[0, la])
+            out, st_ = pipeline_run([drafter, target], prompt, args.gen, mode=mode, gammas=[0, gmode], lookaheads=[0, la])
             torch.cuda.synchronize()
             dtm = time.perf_counter() - w0m
         assert out == S[:args.gen], f"{mname}: output differs from M_K autoregressive decoding"
@@ -726,6 +730,10 @@ def main():
                         "accept_hist": {int(k): int(c) for k, c in enumerate(st_.accept_hist) if c},
                         "gpu_util_mean_pct": mclk.summary().get("gpu_util_mean_pct"),
                         "j_per_token": (mclk.energy_j / len(out)) if mclk.energy_j is not None else None}
+    sd_modes = {k: v for k, v in modes.items() if k == "sync_sd" or k.startswith("sync_sd_gamma")}
+    best_sd = max(sd_modes, key=lambda k: sd_modes[k]["tokens_per_s"])
+    modes["best_sync_sd"] = {"mode": best_sd, "gamma": g if best_sd == "sync_sd" else int(best_sd[13:]),
+                             "tokens_per_s": sd_modes[best_sd]["tokens_per_s"]}
     value = tot_tokens / dev_s
     e2e = tot_tokens / wall_s
     fwd_per_step = g + 1
