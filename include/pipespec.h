@@ -246,6 +246,7 @@ typedef struct ps_stage_info {
   double last_fwd_ms, sum_fwd_ms;
   int64_t n_fwd;
   int32_t max_window, max_seq;  /* the stage's creation options                */
+  int32_t attn_sc;              /* 64-key chunks per attention work item (from max_seq) */
 } ps_stage_info;
 ps_status ps_stage_reset_timers(ps_stage* stage);
 ps_status ps_stage_get_info(const ps_stage* stage, ps_stage_info* info);

@@ -29,6 +29,11 @@ ps_status ps_test_tc_probe(int32_t mode, int32_t iters, int32_t depth, double* n
 /* The same unit issued by the leader CTA of 2-CTA clusters as
  * tcgen05.mma.cta_group::2 with M = 256 (16 KB of weights per SM per unit). */
 ps_status ps_test_tc_probe2(int32_t iters, int32_t depth, double* ns_per_unit);
+/* mma.sync m16n8k16 bf16 issue interval: one CTA per SM of `warps` warps, each
+ * issuing iters x 8 HMMAs in `chains` (1/2/4/8) independent accumulator chains;
+ * ns (events) and cycles (clock64, CTA 0 warp 0) per HMMA per warp. */
+ps_status ps_test_hmma_probe(int32_t warps, int32_t chains, int32_t iters, double* ns_per_hmma,
+                             double* cycles_per_hmma);
 
 /* Protocol test double of the async runtime (no GPU): k stages over a
  * closed-form host "model" -- stage k-1 emits next(c) = (c[-1]*7919 +

@@ -57,7 +57,7 @@ class StageInfo(C.Structure):
     _fields_ = [("n_tokens", C.c_int64), ("kv_len", C.c_int64), ("pages_in_use", C.c_int64),
                 ("pages_total", C.c_int64), ("launches_per_verify", C.c_int64), ("rows_buckets", C.c_int32 * 4),
                 ("last_fwd_ms", C.c_double), ("sum_fwd_ms", C.c_double), ("n_fwd", C.c_int64),
-                ("max_window", C.c_int32), ("max_seq", C.c_int32)]
+                ("max_window", C.c_int32), ("max_seq", C.c_int32), ("attn_sc", C.c_int32)]
 
 
 class VerifyResult(C.Structure):
@@ -141,6 +141,7 @@ _TEST_PROTOS = {
     "ps_test_launch_overhead": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "ps_test_tc_probe": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "ps_test_tc_probe2": (C.c_int32, [C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
+    "ps_test_hmma_probe": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 # trace build only (PS_LIB=.../libpipespec_trace.so)
 _TRACE_PROTOS = {"ps_trace_read": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64])}

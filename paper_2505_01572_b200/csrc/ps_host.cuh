@@ -56,6 +56,23 @@ static ps_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64
   return PS_OK;
 }
 
+// The paged KV pool for the attention ring: [plane 4][rows][hd] bf16 viewed as
+// a 3D tensor {hd, rows, plane} (the plane stride = one plane of one page's
+// layer block: hkv * page_size rows), box {64, 16, 4}: one TMA moves 16 keys
+// x 64 dims of all four planes (K_hi, K_lo, V_hi, V_lo), SWIZZLE_128B.
+static ps_status make_map_kv(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t hd, uint64_t plane_rows) {
+  if (((uintptr_t)ptr & 15) || (hd * 2) % 16) return fail(PS_E_INVALID, "KV pool not 16-byte aligned");
+  cuuint64_t dims[3] = {hd, rows, 4};
+  cuuint64_t strides[2] = {hd * 2, plane_rows * hd * 2};
+  cuuint32_t box[3] = {64, 16, 4};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled (KV) failed (%d)", (int)r);
+  return PS_OK;
+}
+
 // ============================================================================ GEMM launch
 static int g_num_sms = 0;
 

@@ -707,22 +707,47 @@ PS_DEV void tp_reduce_unit(const TpParams& p, int r, int t, int lane) {
 struct AttnParams {
   const StepIn* step;
   const float* q; int ld_q;
-  const __nv_bfloat16* kv; const int32_t* page_table; int page_size; long long page_stride;
+  const int32_t* page_table; int page_size, page_shift;   // page_size = 1 << page_shift
+  const CUtensorMap* kvmap;        // the KV pool as {hd, rows, plane}, box {64, 16, 4}, 128B swizzle
+  long long rows_per_page;         // page_stride / hd
   int layer, hkv, H, hd;
   float scale_log2;                // log2(e) / sqrt(hd)
-  int max_chunks, max_rb;
-  float* ws_o;                     // [hkv][max_rb][max_chunks][rows per block][hd]
-  float* ws_ml;                    // [hkv][max_rb][max_chunks][rows per block][2]
-  unsigned* counters;              // [hkv][max_rb]
+  int max_chunks, max_rb;          // max_chunks: item partials per (head, row block)
+  int sc;                          // 64-key chunks per work item (a per-stage constant)
+  float* ws_o;                     // [hkv][max_rb][max_chunks][kAttnRB][hd]
+  float* ws_ml;                    // [hkv][max_rb][max_chunks][kAttnRB][2]
   __nv_bfloat16* out; int ld_out;
-  unsigned long long* dbg;         // optional per-CTA stage stamps [cta][8] (first item)
+  unsigned long long* dbg;         // optional per-CTA stamps [cta][8] (PS_TRACE builds)
 };
 
-constexpr int kAttnPad = 8;        // smem row padding (bf16 elements): conflict-free ldmatrix
-// smem: K_hi, K_lo, V_hi, V_lo chunks [64][HD+8] bf16 + combine scratch (the
-// query fragments live in registers, built from the fp32 q directly)
-constexpr int attn_smem_bytes(int /*nw*/) { return kKvPlanes * kAttnChunk * (128 + kAttnPad) * 2 + 64 * 4 * 3 + 64; }
-constexpr int kAttnSmem = attn_smem_bytes(8);
+// ---------------------------------------------------------------- decode attention (a6)
+// Work items: (KV head kh, block rb of kAttnRB = 32 query rows, item j = sc
+// consecutive 64-key chunks at absolute positions [64 sc j, 64 sc (j + 1))).
+// sc is a per-stage constant (ps_stage: from max_seq), so a row's arithmetic
+// does not depend on R or on the context length (row-bucket invariance: a
+// verify row equals the AR step at that position bit for bit).  CTA c of G
+// owns the contiguous item range [c n / G, (c + 1) n / G) and streams the
+// items' 16-key stages back to back through a 4-deep TMA ring (3 stages in
+// flight while one is used), so the schedule never changes an item's math.
+//
+// Inside a stage the 4 warps split the head dimension: warp w owns dims
+// [w hd/4, (w+1) hd/4).  S = Q K^T is summed from the 4 warps' partial dot
+// products (smem exchange, fixed order w = 0..3, identical in every warp);
+// every warp runs the same online softmax (running max m, sum l) and
+// accumulates O for its own dims.  All 128 threads work at any R (a decode
+// row block of 4 rows is one 16-row MMA group), instead of one warp per 16
+// rows.  Split-bf16 operands on mma.sync m16n8k16: (q_hi + q_lo)(k_hi +
+// k_lo)^T ~ q_hi k_hi + q_lo k_hi + q_hi k_lo (the lo*lo term ~2^-16
+// relative), likewise P V.
+constexpr int kAttnNG = 1;                  // 16-row MMA groups per item
+constexpr int kAttnRB = 16 * kAttnNG;       // query rows per item
+constexpr int kAttnStep = 16;               // keys per ring stage
+constexpr int kAttnStages = 4;              // ring depth
+template <int HD> __host__ __device__ constexpr int attn_stage_bytes() { return kKvPlanes * kAttnStep * HD * 2; }
+// smem: the ring (kAttnStages x [hd/64][plane][16 keys][128 B], 128B-swizzled
+// by TMA) + its full barriers; the S exchange uses the epilogue scratch area
+constexpr int attn_smem_bytes(int /*nw*/) { return kAttnStages * attn_stage_bytes<128>() + 64; }
+constexpr int kAttnXBytes = 4 * kAttnNG * 2 * 32 * 16;   // S exchange: [warp][group][n-tile][lane] float4 (x2 buffers)
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -739,10 +764,6 @@ PS_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-PS_DEV uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 // Split a pair of fp32 values into hi / lo packed bf16x2 registers.
 PS_DEV void split_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   __nv_bfloat16 h0, l0, h1, l1;
@@ -751,313 +772,406 @@ PS_DEV void split_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   hi = pack2(h0, h1);
   lo = pack2(l0, l1);
 }
-
-// Issue (cp.async, one commit group) the K/V chunk (all four planes) of this
-// CTA's first work item if it lies wholly in the context (positions < pos0:
-// not rewritten by the coming QKV phase).  Returns the prefetched item id, or -1.
-template <int HD, int NW>
-PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* attn_smem, int tid, int cta) {
-  constexpr int kRB = NW * 16, NT = NW * 32, LD = HD + kAttnPad, VPR = HD / 8;
-  const StepIn* st = p.step;
-  const int R = st->R, pos0 = st->pos0;
-  const int rows = R * (p.H / p.hkv);
-  const int n_rb = (rows + kRB - 1) / kRB;
-  const int nchunks = (pos0 + R + kAttnChunk - 1) / kAttnChunk;
-  if (cta >= p.hkv * n_rb * nchunks) return -1;
-  const int c = cta % nchunks, kh = cta / (nchunks * n_rb);
-  const int k0 = c * kAttnChunk;
-  if (k0 + kAttnChunk > pos0) return -1;
-  __nv_bfloat16* sKV = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  const long long page = p.page_table[k0 / p.page_size];
-  const int slot0 = k0 % p.page_size;
-  for (int i = tid; i < kKvPlanes * kAttnChunk * VPR; i += NT) {
-    const int pl = i / (kAttnChunk * VPR), row = (i / VPR) % kAttnChunk, cv = i % VPR;
-    const __nv_bfloat16* src = p.kv + (size_t)page * p.page_stride +
-                               ((size_t)((p.layer * kKvPlanes + pl) * p.hkv + kh) * p.page_size + slot0 + row) * HD + cv * 8;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sKV + (pl * kAttnChunk + row) * LD + cv * 8)),
-                 "l"(src) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  return cta;
+// Byte offset of (plane pl, key r, dim d; d % 8 == 0) in a ring stage laid out
+// [hd/64][plane][16 keys][128 B] with the TMA 128B swizzle (16-byte chunk c of
+// row r at c ^ (r & 7)): ldmatrix rows of 8 keys hit 8 distinct bank groups.
+PS_DEV uint32_t attn_sw(int pl, int r, int d) {
+  return (uint32_t)((d >> 6) * (kKvPlanes * kAttnStep * 128) + pl * (kAttnStep * 128) + r * 128 +
+                    ((((d & 63) >> 3) ^ (r & 7)) << 4));
 }
 
-// S = Q K^T and O = P V with split-bf16 operands on mma.sync m16n8k16:
-// (q_hi + q_lo)(k_hi + k_lo)^T ~ q_hi k_hi + q_lo k_hi + q_hi k_lo (the
-// dropped lo*lo term is ~2^-16 relative), likewise P V.
-template <int HD, int NW, bool kInlineCombine = true>
-PS_DEV void attn_run(const AttnParams& p, uint8_t* attn_smem, int tid, int cta, int ncta, int bar,
-                     int pref_item = -1) {
-  constexpr int kRB = NW * 16;                          // query rows per block
-  constexpr int NT = NW * 32;
-  constexpr int LD = HD + kAttnPad;                     // smem row stride (elements)
-  __nv_bfloat16* sKh = reinterpret_cast<__nv_bfloat16*>(attn_smem);
-  __nv_bfloat16* sKl = sKh + kAttnChunk * LD;
-  __nv_bfloat16* sVh = sKl + kAttnChunk * LD;
-  __nv_bfloat16* sVl = sVh + kAttnChunk * LD;
-  float* sM = reinterpret_cast<float*>(sVl + kAttnChunk * LD);   // combine scratch [64]
-  int& s_last = *reinterpret_cast<int*>(sM + 3 * 64);
-  const StepIn* st = p.step;
-  const int R = st->R, pos0 = st->pos0;
-  const int g = p.H / p.hkv;
-  const int rows = R * g;
-  const int n_rb = (rows + kRB - 1) / kRB;
-  const int n_keys = pos0 + R;
-  const int nchunks = (n_keys + kAttnChunk - 1) / kAttnChunk;
+struct AttnGeom {
+  int rows, n_rb, n_keys, nsc, n_items;
+  PS_DEV AttnGeom(const AttnParams& p) {
+    const int R = p.step->R;
+    rows = R * (p.H / p.hkv);
+    n_rb = (rows + kAttnRB - 1) / kAttnRB;
+    n_keys = p.step->pos0 + R;
+    const int nchunks = (n_keys + kAttnChunk - 1) / kAttnChunk;
+    nsc = (nchunks + p.sc - 1) / p.sc;
+    n_items = p.hkv * n_rb * nsc;
+  }
+  PS_DEV int first(int c, int G) const { return (int)((long long)c * n_items / G); }
+  // item -> KV head, row block, item index j, key range [kbeg, kend), stages
+  PS_DEV void item(const AttnParams& p, int it, int& kh, int& rb, int& j, int& kbeg, int& kend, int& ns) const {
+    j = it % nsc;
+    rb = (it / nsc) % n_rb;
+    kh = it / (nsc * n_rb);
+    kbeg = j * p.sc * kAttnChunk;
+    kend = min(n_keys, (j + 1) * p.sc * kAttnChunk);
+    ns = (kend - kbeg + kAttnStep - 1) / kAttnStep;
+  }
+};
+
+// Ring producer state (one thread): the stream position of the next stage to
+// issue and the KV row of its first key (plane 0); the page is looked up one
+// stage ahead, so an issue never waits on the page table.
+struct AttnProducer {
+  int item, s, ns, kbeg, kh;
+  long long row;                       // pool row of key kbeg + 16 s, plane 0 (valid if more)
+  bool more;
+};
+PS_DEV long long attn_row(const AttnParams& p, int kh, int k0) {
+  const long long page = p.page_table[k0 >> p.page_shift];
+  return page * p.rows_per_page + ((long long)(p.layer * kKvPlanes * p.hkv + kh) << p.page_shift) +
+         (k0 & (p.page_size - 1));
+}
+PS_DEV void attn_producer_init(const AttnParams& p, const AttnGeom& gm, int it0, int it_end, AttnProducer& u) {
+  u.more = it0 < it_end;
+  if (!u.more) return;
+  int rb, j, kend;
+  u.item = it0;
+  u.s = 0;
+  gm.item(p, it0, u.kh, rb, j, u.kbeg, kend, u.ns);
+  u.row = attn_row(p, u.kh, u.kbeg);
+}
+// advance to the next stage of the stream, then look up its row
+PS_DEV void attn_producer_seek(const AttnParams& p, const AttnGeom& gm, int it_end, AttnProducer& u) {
+  if (++u.s >= u.ns) {
+    if (++u.item >= it_end) {
+      u.more = false;
+      return;
+    }
+    int rb, j, kend;
+    gm.item(p, u.item, u.kh, rb, j, u.kbeg, kend, u.ns);
+    u.s = 0;
+  }
+  u.row = attn_row(p, u.kh, u.kbeg + u.s * kAttnStep);
+}
+// TMA of ring stage `seq` (buffer seq % 4): 16 keys x all four planes, one box
+// per 64 dims.  Keys past the context are loaded too (finite: the pool is
+// zeroed at stage creation) and masked.
+template <int HD>
+PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t bars_u32, uint32_t seq, long long row) {
+  const int buf = seq % kAttnStages;
+  const uint32_t bar = bars_u32 + buf * 8;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(attn_stage_bytes<HD>())
+               : "memory");
+#pragma unroll
+  for (int h = 0; h < HD / 64; ++h)
+    tma_load_3d(ring_u32 + buf * attn_stage_bytes<HD>() + h * (kKvPlanes * kAttnStep * 128), p.kvmap, bar, h * 64,
+                (int)row, 0, kEvictFirst);
+}
+
+// During the QKV phase: issue the first ring stages (up to kAttnStages) of this
+// CTA's stream whose keys all lie below pos0 (not rewritten by QKV).  Returns
+// how many were issued (they are the stream's stages seq .. seq + n - 1).
+template <int HD>
+PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* ring, uint64_t* bars, uint32_t seq, int cta, int ncta) {
+  const AttnGeom gm(p);
+  const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
+  AttnProducer u;
+  attn_producer_init(p, gm, it0, it_end, u);
+  int n = 0;
+  const int pos0 = p.step->pos0;
+  while (u.more && n < kAttnStages && u.kbeg + (u.s + 1) * kAttnStep <= pos0) {
+    attn_issue<HD>(p, smem_u32(ring), smem_u32(bars), seq + n, u.row);
+    ++n;
+    attn_producer_seek(p, gm, it_end, u);
+  }
+  return n;
+}
+
+// (noinline: ptxas allocates a called function's registers beside the
+// caller's live ones, so the megakernel keeps little live across the call)
+template <int HD>
+__device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* bars, float4* xbuf, int tid, int cta, int ncta,
+                     uint32_t& seq, int npref) {
+  constexpr int DW = HD / 4;          // dims per warp
+  constexpr int KS = DW / 16;         // k steps of QK per warp
+  constexpr int NTO = DW / 8;         // output n-tiles per warp
+  const AttnGeom gm(p);
+  const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
+  if (it0 >= it_end) return;
+  const int g = p.H / p.hkv, pos0 = p.step->pos0;
+  const float* const qp = p.q;
+  const int ld_q = p.ld_q;
+  const float qscale = p.scale_log2;
   const int warp = tid >> 5, lane = tid & 31;
-  const int n_items = p.hkv * n_rb * nchunks;
-  for (int item = cta; item < n_items; item += ncta) {
-    const int c = item % nchunks;
-    const int rb = (item / nchunks) % n_rb;
-    const int kh = item / (nchunks * n_rb);
-    const int m0 = rb * kRB;
-    const int mrows = min(kRB, rows - m0);
-    const int k0 = c * kAttnChunk;
-    const int nk = min(kAttnChunk, n_keys - k0);
-    const bool stamp = tid == 0 && item == cta;
-    if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
-    const int nwarps_used = (mrows + 15) / 16;
-    // ---- K/V chunk, four planes: cp.async (16 B, zero-fill past nk) -- every
-    // copy in flight at once (skipped when prefetched during the QKV phase)
-    const long long page = p.page_table[k0 / p.page_size];
-    const int slot0 = k0 % p.page_size;
-    constexpr int VPR = HD / 8;                          // 16-byte vectors per row
-    for (int i = (item == pref_item) ? kKvPlanes * kAttnChunk * VPR : tid; i < kKvPlanes * kAttnChunk * VPR; i += NT) {
-      const int pl = i / (kAttnChunk * VPR), row = (i / VPR) % kAttnChunk, cv = i % VPR;
-      const int ok = row < nk ? 16 : 0;
-      const __nv_bfloat16* src = p.kv + (size_t)page * p.page_stride +
-                                 ((size_t)((p.layer * kKvPlanes + pl) * p.hkv + kh) * p.page_size + slot0 +
-                                  (row < nk ? row : 0)) * HD + cv * 8;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sKh + (pl * kAttnChunk + row) * LD + cv * 8)),
-                   "l"(src), "r"(ok) : "memory");
+  const int d_own = warp * DW;
+  const uint32_t ring_u32 = smem_u32(ring), bars_u32 = smem_u32(bars), xbuf_u32 = smem_u32(xbuf);
+  // producer (thread 0): the next stage to issue, up to kAttnStages ahead
+  AttnProducer pu;
+  pu.more = false;
+  uint32_t pseq = seq;
+  if (tid == 0) {
+    attn_producer_init(p, gm, it0, it_end, pu);
+    for (int n = 0; n < npref && pu.more; ++n) {
+      attn_producer_seek(p, gm, it_end, pu);
+      ++pseq;
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    // ---- this warp's query fragments (A operand of m16n8k16, rows lane/4 and
-    // lane/4 + 8, dims 2(lane%4) + {0,1} and + 8 of each 16-wide k step),
-    // loaded straight from the fp32 q, pre-scaled, split into hi / lo
-    uint32_t qh[HD / 16][4], ql[HD / 16][4];
-    {
-      int qoff[2];
+    fence_proxy_async_global();          // this forward's new K/V rows (QKV epilogue stores) -> TMA
+    while (pu.more && pseq < seq + kAttnStages) {
+      attn_issue<HD>(p, ring_u32, bars_u32, pseq++, pu.row);
+      attn_producer_seek(p, gm, it_end, pu);
+    }
+  }
+  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
+#if PS_TRACE
+  unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
+#define PS_ATTN_LAP(acc)                         \
+  do {                                           \
+    const unsigned long long t_ = globaltimer(); \
+    acc += t_ - tr_t;                            \
+    tr_t = t_;                                   \
+  } while (0)
+#else
+#define PS_ATTN_LAP(acc) \
+  do {                   \
+  } while (0)
+#endif
+  // consumer cursor
+  int item = it0, s = 0, ns = 0, kbeg = 0, kend = 0, kh = 0, rb = 0, j = 0, ngr = 0;
+  int qpos[kAttnNG][2];
+  uint32_t qh[kAttnNG][KS][4], ql[kAttnNG][KS][4];
+  float mrow[kAttnNG][2], lrow[kAttnNG][2];
+  float oacc[kAttnNG][NTO][4];
+  while (true) {
+    if (s == 0) {
+      // ---- new item: geometry, this warp's query fragments (own dims), state
+      gm.item(p, item, kh, rb, j, kbeg, kend, ns);
+      const int m0 = rb * kAttnRB;
+      const int mrows = min(kAttnRB, gm.rows - m0);
+      ngr = (mrows + 15) >> 4;
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        const int m = warp * 16 + (lane >> 2) + hr * 8;
-        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-        qoff[hr] = m < mrows ? r * p.ld_q + h * HD : -1;
-      }
-      float2 qv[HD / 16][4];
+      for (int gi = 0; gi < kAttnNG; ++gi) {
+        int qoff[2];
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int o = qoff[j & 1];
-          const int d = kk * 16 + (lane & 3) * 2 + (j >> 1) * 8;
-          qv[kk][j] = (o >= 0 && warp < nwarps_used) ? *reinterpret_cast<const float2*>(p.q + o + d)
-                                                     : make_float2(0.f, 0.f);
+        for (int hr = 0; hr < 2; ++hr) {
+          const int m = gi * 16 + (lane >> 2) + hr * 8;
+          const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+          qoff[hr] = m < mrows ? r * ld_q + h * HD : -1;
+          qpos[gi][hr] = min(kend - 1, pos0 + r);    // last key this row sees in this item
         }
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
+        for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          split_pack(qv[kk][j].x * p.scale_log2, qv[kk][j].y * p.scale_log2, qh[kk][j], ql[kk][j]);
+          for (int jq = 0; jq < 4; ++jq) {
+            const int o = qoff[jq & 1];
+            const int d = d_own + kk * 16 + (lane & 3) * 2 + (jq >> 1) * 8;
+            const float2 qv = o >= 0 ? *reinterpret_cast<const float2*>(qp + o + d) : make_float2(0.f, 0.f);
+            split_pack(qv.x * qscale, qv.y * qscale, qh[gi][kk][jq], ql[gi][kk][jq]);
+          }
+        mrow[gi][0] = mrow[gi][1] = -INFINITY;
+        lrow[gi][0] = lrow[gi][1] = 0.f;
+#pragma unroll
+        for (int n = 0; n < NTO; ++n) oacc[gi][n][0] = oacc[gi][n][1] = oacc[gi][n][2] = oacc[gi][n][3] = 0.f;
+      }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    named_bar(bar, NT);
-    if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 1);
-    if (warp < nwarps_used) {
-      // ---- S = Q K^T for this warp's 16 rows x 64 keys
-      float sacc[8][4];
+    const int k0 = kbeg + s * kAttnStep;
+    const int buf = seq % kAttnStages;
+    mbar_wait(&bars[buf], (seq / kAttnStages) & 1);
+    PS_ATTN_LAP(tr_wait);
+    const uint32_t sb = ring_u32 + buf * attn_stage_bytes<HD>();
+    // ---- partial S over this warp's dims: 2 n-tiles (16 keys) per group
+    float sacc[kAttnNG][2][4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+    for (int gi = 0; gi < kAttnNG; ++gi)
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
+      for (int nt = 0; nt < 2; ++nt) sacc[gi][nt][0] = sacc[gi][nt][1] = sacc[gi][nt][2] = sacc[gi][nt][3] = 0.f;
 #pragma unroll
-        for (int jp = 0; jp < 4; ++jp) {   // pairs of 8-key n-tiles
-          const int krow = jp * 16 + (lane & 7) + ((lane >> 4) << 3);
-          const int kcol = kk * 16 + ((lane >> 3) & 1) * 8;
-          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
-          ldsm_x4(smem_u32(sKh + krow * LD + kcol), b0, b1, b2, b3);
-          ldsm_x4(smem_u32(sKl + krow * LD + kcol), c0, c1, c2, c3);
-          mma16816(sacc[2 * jp], qh[kk], b0, b1);
-          mma16816(sacc[2 * jp + 1], qh[kk], b2, b3);
-          mma16816(sacc[2 * jp], ql[kk], b0, b1);
-          mma16816(sacc[2 * jp + 1], ql[kk], b2, b3);
-          mma16816(sacc[2 * jp], qh[kk], c0, c1);
-          mma16816(sacc[2 * jp + 1], qh[kk], c2, c3);
+    for (int kk = 0; kk < KS; ++kk) {
+      const int kr = (lane & 7) + ((lane >> 4) << 3);
+      const int kd = d_own + kk * 16 + ((lane >> 3) & 1) * 8;
+      uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+      ldsm_x4(sb + attn_sw(0, kr, kd), b0, b1, b2, b3);   // K_hi
+      ldsm_x4(sb + attn_sw(1, kr, kd), c0, c1, c2, c3);   // K_lo
+#pragma unroll
+      for (int gi = 0; gi < kAttnNG; ++gi) {
+        if (gi < ngr) {
+          mma16816(sacc[gi][0], qh[gi][kk], b0, b1);
+          mma16816(sacc[gi][1], qh[gi][kk], b2, b3);
+          mma16816(sacc[gi][0], ql[gi][kk], b0, b1);
+          mma16816(sacc[gi][1], ql[gi][kk], b2, b3);
+          mma16816(sacc[gi][0], qh[gi][kk], c0, c1);
+          mma16816(sacc[gi][1], qh[gi][kk], c2, c3);
         }
       }
-      // ---- causal / length mask and chunk-local softmax (rows lane/4 and lane/4+8)
-      float mrow[2] = {-INFINITY, -INFINITY};
+    }
+    // ---- exchange: S = sum over the 4 warps' partials (fixed order).  Two
+    // buffers by stage parity: a warp writing stage s + 1's partials cannot
+    // overwrite stage s's before every warp has read them (it would have to
+    // pass stage s + 1's barrier first), so one barrier per stage suffices.
+    const uint32_t xb = xbuf_u32 + (seq & 1) * kAttnXBytes;
+#pragma unroll
+    for (int gi = 0; gi < kAttnNG; ++gi)
+      if (gi < ngr)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+          st_shared_v4(xb + ((((warp * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4), sacc[gi][nt][0], sacc[gi][nt][1],
+                       sacc[gi][nt][2], sacc[gi][nt][3]);
+    named_bar(2, 128);
+    // every warp is past its PV of stage seq - 1: that buffer (only) is free,
+    // so stage seq + 3 at the latest may be issued (3 in flight beside seq)
+    if (tid == 0 && pu.more && pseq < seq + kAttnStages) {
+      attn_issue<HD>(p, ring_u32, bars_u32, pseq++, pu.row);
+      attn_producer_seek(p, gm, it_end, pu);
+    }
+#pragma unroll
+    for (int gi = 0; gi < kAttnNG; ++gi)
+      if (gi < ngr)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          float4 v = ld_shared_v4(xb + ((((0 * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4));
+#pragma unroll
+          for (int w = 1; w < 4; ++w) {
+            const float4 x = ld_shared_v4(xb + ((((w * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4));
+            v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+          }
+          sacc[gi][nt][0] = v.x; sacc[gi][nt][1] = v.y; sacc[gi][nt][2] = v.z; sacc[gi][nt][3] = v.w;
+        }
+    PS_ATTN_LAP(tr_qk);
+    // ---- V fragments (own dims) for the P V MMAs
+    uint32_t vh[NTO / 2][4], vl[NTO / 2][4];
+#pragma unroll
+    for (int np = 0; np < NTO / 2; ++np) {
+      const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int vd = d_own + np * 16 + (lane >> 4) * 8;
+      ldsm_x4_t(sb + attn_sw(2, vr, vd), vh[np][0], vh[np][1], vh[np][2], vh[np][3]);   // V_hi
+      ldsm_x4_t(sb + attn_sw(3, vr, vd), vl[np][0], vl[np][1], vl[np][2], vl[np][3]);   // V_lo
+    }
+#pragma unroll
+    for (int gi = 0; gi < kAttnNG; ++gi) {
+      if (gi >= ngr) continue;
+      // ---- causal / length mask, online softmax (rows lane/4 and lane/4 + 8)
+      float scale[2];
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
-        const int m = warp * 16 + (lane >> 2) + hr * 8;
-        const int qpos = pos0 + (m0 + m) / g;
+        float mx = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int e2 = 0; e2 < 2; ++e2) {
-            const int key = j * 8 + (lane & 3) * 2 + e2;
-            float& sv = sacc[j][hr * 2 + e2];
-            if (key >= nk || k0 + key > qpos) sv = -INFINITY;
-            mrow[hr] = fmaxf(mrow[hr], sv);
+            const int key = k0 + nt * 8 + (lane & 3) * 2 + e2;
+            float& sv = sacc[gi][nt][hr * 2 + e2];
+            if (key > qpos[gi][hr]) sv = -INFINITY;
+            mx = fmaxf(mx, sv);
           }
-        mrow[hr] = fmaxf(mrow[hr], __shfl_xor_sync(0xffffffffu, mrow[hr], 1));
-        mrow[hr] = fmaxf(mrow[hr], __shfl_xor_sync(0xffffffffu, mrow[hr], 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mn = fmaxf(mrow[gi][hr], mx);
+        scale[hr] = (mrow[gi][hr] == -INFINITY) ? 0.f : exp2f(mrow[gi][hr] - mn);
+        mrow[gi][hr] = mn;
       }
-      float lrow[2] = {0.f, 0.f};
-      uint32_t pah[4][4], pal[4][4];      // P as A fragments (hi / lo), 4 k-blocks of 16 keys
+      float lsum[2] = {0.f, 0.f};
+      uint32_t pah[4], pal[4];             // P as the A fragment (16 rows x 16 keys), hi / lo
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int nt = 0; nt < 2; ++nt) {
         float pv[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int hr = q4 >> 1;
-          pv[q4] = (mrow[hr] == -INFINITY) ? 0.f : exp2f(sacc[j][q4] - mrow[hr]);
-          lrow[hr] += pv[q4];
+          pv[q4] = (mrow[gi][hr] == -INFINITY) ? 0.f : exp2f(sacc[gi][nt][q4] - mrow[gi][hr]);
+          lsum[hr] += pv[q4];
         }
-        const int kb = j >> 1, half2 = j & 1;
-        split_pack(pv[0], pv[1], pah[kb][half2 * 2 + 0], pal[kb][half2 * 2 + 0]);
-        split_pack(pv[2], pv[3], pah[kb][half2 * 2 + 1], pal[kb][half2 * 2 + 1]);
+        split_pack(pv[0], pv[1], pah[nt * 2 + 0], pal[nt * 2 + 0]);
+        split_pack(pv[2], pv[3], pah[nt * 2 + 1], pal[nt * 2 + 1]);
       }
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
-        lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 1);
-        lrow[hr] += __shfl_xor_sync(0xffffffffu, lrow[hr], 2);
+        lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 1);
+        lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 2);
+        lrow[gi][hr] = lrow[gi][hr] * scale[hr] + lsum[hr];
       }
-      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 2);
-      // ---- O = P V  (16 rows x HD)
-      float oacc[HD / 8][4];
+      // ---- O (own dims) = O * scale + P V
 #pragma unroll
-      for (int n = 0; n < HD / 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
-#pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-#pragma unroll
-        for (int np = 0; np < HD / 16; ++np) {
-          const int vrow = kb * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-          const int vcol = np * 16 + (lane >> 4) * 8;
-          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
-          ldsm_x4_t(smem_u32(sVh + vrow * LD + vcol), b0, b1, b2, b3);
-          ldsm_x4_t(smem_u32(sVl + vrow * LD + vcol), c0, c1, c2, c3);
-          mma16816(oacc[2 * np], pah[kb], b0, b1);
-          mma16816(oacc[2 * np + 1], pah[kb], b2, b3);
-          mma16816(oacc[2 * np], pal[kb], b0, b1);
-          mma16816(oacc[2 * np + 1], pal[kb], b2, b3);
-          mma16816(oacc[2 * np], pah[kb], c0, c1);
-          mma16816(oacc[2 * np + 1], pah[kb], c2, c3);
-        }
+      for (int n = 0; n < NTO; ++n) {
+        oacc[gi][n][0] *= scale[0]; oacc[gi][n][1] *= scale[0];
+        oacc[gi][n][2] *= scale[1]; oacc[gi][n][3] *= scale[1];
       }
-      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 3);
-      // ---- chunk partials -> workspace
-      const size_t base = ((size_t)((kh * p.max_rb + rb) * p.max_chunks + c) * kRB);
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        const int m = warp * 16 + (lane >> 2) + hr * 8;
-        float* op = p.ws_o + (base + m) * HD;
-#pragma unroll
-        for (int n = 0; n < HD / 8; ++n)
-          __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2),
-                 make_float2(oacc[n][hr * 2], oacc[n][hr * 2 + 1]));
-        if ((lane & 3) == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[hr], lrow[hr]));
+      for (int np = 0; np < NTO / 2; ++np) {
+        mma16816(oacc[gi][2 * np], pah, vh[np][0], vh[np][1]);
+        mma16816(oacc[gi][2 * np + 1], pah, vh[np][2], vh[np][3]);
+        mma16816(oacc[gi][2 * np], pal, vh[np][0], vh[np][1]);
+        mma16816(oacc[gi][2 * np + 1], pal, vh[np][2], vh[np][3]);
+        mma16816(oacc[gi][2 * np], pah, vl[np][0], vl[np][1]);
+        mma16816(oacc[gi][2 * np + 1], pah, vl[np][2], vl[np][3]);
       }
     }
-    if constexpr (!kInlineCombine) {    // partials only; attn_combine runs after a grid barrier
-      named_bar(bar, NT);
-      if (stamp) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
-      continue;
-    }
-    fence_acq_rel_gpu();
-    named_bar(bar, NT);
-    if (tid == 0) s_last = atomicAdd(&p.counters[kh * p.max_rb + rb], 1u) == (unsigned)(nchunks - 1);
-    named_bar(bar, NT);
-    if (s_last) {
-      fence_acq_rel_gpu();
-      // combine: per row M = max_c m_c, L = sum_c 2^(m_c-M) l_c, O = sum_c 2^(m_c-M) O_c / L
-      const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
-      for (int m = warp; m < mrows; m += NW) {
-        float M = -INFINITY;
-        for (int cc = lane; cc < nchunks; cc += 32)
-          M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
+    PS_ATTN_LAP(tr_pv);
+    ++seq;
+    if (++s == ns) {
+      // ---- item partial -> workspace [kh][rb][j][kAttnRB rows][HD] (own dims; m, l by warp 0)
+      const size_t base = (size_t)((kh * p.max_rb + rb) * p.max_chunks + j) * kAttnRB;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        float Lp = 0.f;
-        for (int cc = lane; cc < nchunks; cc += 32) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cc) * kRB + m) * 2));
-          Lp += (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M) * ml.y;
+      for (int gi = 0; gi < kAttnNG; ++gi) {
+        if (gi >= ngr) continue;
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+          const int m = gi * 16 + (lane >> 2) + hr * 8;
+          float* op = p.ws_o + (base + m) * HD + d_own;
+#pragma unroll
+          for (int n = 0; n < NTO; ++n)
+            __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2),
+                   make_float2(oacc[gi][n][hr * 2], oacc[gi][n][hr * 2 + 1]));
+          if (warp == 0 && (lane & 3) == 0)
+            __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[gi][hr], lrow[gi][hr]));
         }
-        // fixed-order sum over chunks: lanes hold chunk-strided partials, reduce by tree
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
-        const float invL = 1.0f / Lp;
-        constexpr int DPL = HD / 32;   // dims per lane
-        float acc[DPL];
-#pragma unroll
-        for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
-#pragma unroll 8
-        for (int cc = 0; cc < nchunks; ++cc) {
-          const float mc = __ldcg(p.ws_ml + ((rbase + cc) * kRB + m) * 2);
-          const float sc = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
-          const float* op = p.ws_o + ((rbase + cc) * kRB + m) * HD + lane * DPL;
-          if constexpr (DPL == 4) {
-            const float4 o4 = __ldcg(reinterpret_cast<const float4*>(op));
-            acc[0] += sc * o4.x; acc[1] += sc * o4.y; acc[2] += sc * o4.z; acc[3] += sc * o4.w;
-          } else {
-            const float2 o2 = __ldcg(reinterpret_cast<const float2*>(op));
-            acc[0] += sc * o2.x; acc[1] += sc * o2.y;
-          }
-        }
-        const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-        __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
-#pragma unroll
-        for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kRowsCap * p.ld_out]);
       }
-      if (tid == 0) p.counters[kh * p.max_rb + rb] = 0u;
+      if (++item >= it_end) break;
+      s = 0;
     }
-    named_bar(bar, NT);
   }
+  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
+#if PS_TRACE
+  if (tid == 0 && p.dbg) {
+    p.dbg[cta * 8 + 5] = tr_wait;
+    p.dbg[cta * 8 + 6] = tr_qk;
+    p.dbg[cta * 8 + 7] = tr_pv;
+  }
+#endif
+#undef PS_ATTN_LAP
 }
 
-// Combine of the chunk partials written by attn_run<.., false>: one warp per
-// output row (kh, m); lanes hold HD/32 dims.  Per row M = max_c m_c, L = sum_c
-// 2^(m_c - M) l_c, O = sum_c 2^(m_c - M) O_c / L in chunk order.  Lane c loads
-// chunk c's (m, l) once (its scale reaches the other lanes by shuffles) and
-// the O loads of 4 chunks are issued before any is used.
-template <int HD, int kRB>
-PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
+// Combine of the item partials (next phase): one CTA per output row (kh, m),
+// its 4 warps take the partials c = w, w + 4, ... (a split independent of the
+// partial count, so the extra all-masked partials of a longer window add exact
+// zeros: row-bucket invariance).  Per row M = max_c m_c, L = sum_c 2^(m_c - M)
+// l_c, O = sum_c 2^(m_c - M) O_c / L; each warp sums its partials in order
+// (8 O loads in flight), the 4 warp sums are added in warp order.
+template <int HD>
+PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int ncta) {
   const StepIn* st = p.step;
   const int R = st->R, pos0 = st->pos0;
   const int g = p.H / p.hkv;
   const int rows = R * g;
-  const int nchunks = (pos0 + R + kAttnChunk - 1) / kAttnChunk;
-  const int lane = threadIdx.x & 31;
+  const int np = ((pos0 + R + kAttnChunk - 1) / kAttnChunk + p.sc - 1) / p.sc;   // item partials
+  const int warp = tid >> 5, lane = tid & 31;
   constexpr int DPL = HD / 32;
   using VecT = typename std::conditional<DPL == 4, float4, float2>::type;
-  for (int item = gwarp; item < p.hkv * rows; item += nwarps_total) {
-    const int kh = item / rows, mg = item % rows;
-    const int rb = mg / kRB, m = mg % kRB;
+  constexpr int kIF = 8;                  // O loads in flight per warp
+  for (int it = cta; it < p.hkv * rows; it += ncta) {
+    const int kh = it / rows, mg = it % rows;
+    const int rb = mg / kAttnRB, m = mg % kAttnRB;
     const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
+    float M = -INFINITY;
+    for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + c) * kAttnRB + m) * 2));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float acc[DPL];
 #pragma unroll
     for (int t = 0; t < DPL; ++t) acc[t] = 0.f;
-    float M = -INFINITY;
-    for (int c0 = 0; c0 < nchunks; c0 += 32)
-      if (c0 + lane < nchunks) M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + c0 + lane) * kRB + m) * 2));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float Lp = 0.f;
-    for (int c0 = 0; c0 < nchunks; c0 += 32) {
-      float sc = 0.f;                    // 2^(m_c - M) of chunk c0 + lane
-      if (c0 + lane < nchunks) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + c0 + lane) * kRB + m) * 2));
+    // this warp's partials c = warp + 4 i; 32 of them per round (lane i holds c's scale)
+    for (int i0 = 0; warp + 4 * i0 < np; i0 += 32) {
+      const int cl = warp + 4 * (i0 + lane);
+      float sc = 0.f;
+      if (cl < np) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cl) * kAttnRB + m) * 2));
         sc = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
         Lp += sc * ml.y;
       }
-      const int nh = min(32, nchunks - c0);
-      for (int q0 = 0; q0 < nh; q0 += 4) {
-        VecT ov[4];
+      const int nh = min(32, (np - warp + 3) / 4 - i0);
+      for (int q0 = 0; q0 < nh; q0 += kIF) {
+        VecT ov[kIF];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < kIF; ++q)
           if (q0 + q < nh)
-            ov[q] = __ldcg(reinterpret_cast<const VecT*>(p.ws_o + ((rbase + c0 + q0 + q) * kRB + m) * HD + lane * DPL));
+            ov[q] = __ldcg(reinterpret_cast<const VecT*>(p.ws_o + ((rbase + warp + 4 * (i0 + q0 + q)) * kAttnRB + m) * HD +
+                                                         lane * DPL));
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kIF; ++q) {
           const float sq = __shfl_sync(0xffffffffu, sc, (q0 + q) & 31);
           if (q0 + q < nh) {
             if constexpr (DPL == 4) {
@@ -1069,14 +1183,31 @@ PS_DEV void attn_combine(const AttnParams& p, int gwarp, int nwarps_total) {
         }
       }
     }
-    // fixed-order sum over chunks: lanes hold chunk-strided partials, reduce by tree
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Lp += __shfl_xor_sync(0xffffffffu, Lp, o);
-    const float invL = 1.0f / Lp;
-    const int r = mg / g, h = kh * g + mg % g;
-    __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
+    // ---- the 4 warp sums, in warp order
 #pragma unroll
-    for (int t = 0; t < DPL; ++t) split_bf16(acc[t] * invL, dst[t], dst[t + (size_t)kRowsCap * p.ld_out]);
+    for (int t = 0; t < DPL; ++t) xs[(warp * DPL + t) * 32 + lane] = acc[t];
+    if (lane == 0) xs[4 * DPL * 32 + warp] = Lp;
+    named_bar(1, 128);
+    if (warp == 0) {
+      float o[DPL];
+#pragma unroll
+      for (int t = 0; t < DPL; ++t) {
+        o[t] = xs[(0 * DPL + t) * 32 + lane];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) o[t] += xs[(w * DPL + t) * 32 + lane];
+      }
+      float L = xs[4 * DPL * 32 + 0];
+#pragma unroll
+      for (int w = 1; w < 4; ++w) L += xs[4 * DPL * 32 + w];
+      const float invL = 1.0f / L;
+      const int r = mg / g, h = kh * g + mg % g;
+      __nv_bfloat16* dst = p.out + (size_t)r * p.ld_out + h * HD + lane * DPL;
+#pragma unroll
+      for (int t = 0; t < DPL; ++t) split_bf16(o[t] * invL, dst[t], dst[t + (size_t)kRowsCap * p.ld_out]);
+    }
+    named_bar(1, 128);
   }
 }
 

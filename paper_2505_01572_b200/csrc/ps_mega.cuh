@@ -72,7 +72,8 @@ struct MegaSmem {
   static constexpr int kOffRed = kOffScratch + 128 * (epi_rows<RP>() + 1) * 4;
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
-  static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 127) / 128 * 128;
+  static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 1023) / 1024 * 1024;   // TMA 128B-swizzle dst
+  static_assert(128 * (epi_rows<RP>() + 1) * 4 >= 2 * kAttnXBytes, "attention S exchange lives in the scratch area");
   static constexpr int kAttnBytes = attn_smem_bytes(4);
   static constexpr int kOffBar = kOffAttn + kAttnBytes;
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
@@ -112,16 +113,15 @@ PS_DEV bool poll_ready(const unsigned* p, unsigned target) {
   fence_acquire_gpu();
   return true;
 }
-// Generic-proxy global writes of another CTA (epilogue st.global) must be
-// visible to this CTA's async-proxy (TMA) reads of the same buffers.
-PS_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 template <int RP, int STAGES = mega_stages<RP>()>
 __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_constant__ MegaParams P) {
   using L = MegaSmem<RP, STAGES>;
   constexpr int kMegaStages = L::kMegaStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned, derived from smem_raw by an offset (keeps the shared
+  // address space visible to the compiler: LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sX = smem + L::kOffX;
   float* scratch = (float*)(smem + L::kOffScratch);
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   float* rstd = (float*)(smem + L::kOffRstd);
   long long* kvrow = (long long*)(smem + L::kOffKvRow);
   uint8_t* attn_smem = smem + L::kOffAttn;
+  uint64_t* abars = (uint64_t*)(attn_smem + kAttnStages * attn_stage_bytes<128>());   // attention ring full barriers
   uint64_t* full = (uint64_t*)(smem + L::kOffBar);
   uint64_t* empty = full + kMegaStages;
   uint64_t* tfull = empty + kMegaStages;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMegaStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < kAttnStages; ++s) mbar_init(&abars[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -272,11 +274,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     }
   } else {
     // ================= epilogue / attention / embed / argmax (warps 2-5) =================
-    const int quarter = warp & 3;
-    const int e = quarter * 32 + lane;
-    const int et = threadIdx.x - 64;                   // 0..127 in warp order 2..5
+    const int et0 = threadIdx.x - 64;                  // 0..127 in warp order 2..5
     uint32_t nacc = 0;
-    int pref_item = -1;                                // attention chunk prefetched during QKV
+    uint32_t attn_seq = 0;                             // attention ring stages consumed so far
+    int attn_npref = 0;                                // ... and issued ahead during QKV (thread et 0)
     // StepIn -> smem once: every later read of the step (rows, positions,
     // generation, flags) in the epilogues / attention / argmax is a shared-
     // memory hit instead of a global round trip on a phase's critical path.
@@ -284,12 +285,19 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       static_assert(sizeof(StepIn) % 4 == 0, "StepIn words");
       const int* src = reinterpret_cast<const int*>(P.step);
       int* dst = reinterpret_cast<int*>(sstep);
-      for (int i = et; i < (int)(sizeof(StepIn) / 4); i += 128) dst[i] = src[i];
+      for (int i = et0; i < (int)(sizeof(StepIn) / 4); i += 128) dst[i] = src[i];
     }
     const StepIn* st = P.step;
     const int R = st->R;
     const int pos0 = st->pos0;
     for (int ph = 0; ph < P.n_ph; ++ph) {
+      // per-thread indices re-read every phase (opaque to the compiler): values
+      // derived from them are not hoisted out of the loop and kept live
+      // across the attention call
+      const int et = (int)opaque_tid_x() - 64;
+      const int lane = et & 31;
+      const int quarter = (et >> 5) ^ 2;               // warps 2..5 -> TMEM lane quarters 2, 3, 0, 1
+      const int e = quarter * 32 + lane;
       // phase descriptor -> smem (one batch of 8-byte loads; every later
       // parameter access is a shared-memory hit instead of an L2 round trip)
       {
@@ -321,12 +329,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (Q.a.hd == 128) attn_run<128, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
-        else attn_run<64, 4, false>(Q.a, attn_smem, et, c, G, 1, pref_item);
-        pref_item = -1;
+        if (Q.a.hd == 128) attn_run<128>(Q.a, attn_smem, abars, (float4*)scratch, et, c, G, attn_seq, attn_npref);
+        else attn_run<64>(Q.a, attn_smem, abars, (float4*)scratch, et, c, G, attn_seq, attn_npref);
+        attn_npref = 0;
       } else if (kind == PH_ACOMB) {
-        if (Q.a.hd == 128) attn_combine<128, 64>(Q.a, c * 4 + (et >> 5), G * 4);
-        else attn_combine<64, 64>(Q.a, c * 4 + (et >> 5), G * 4);
+        if (Q.a.hd == 128) attn_combine<128>(Q.a, scratch, et, c, G);
+        else attn_combine<64>(Q.a, scratch, et, c, G);
       } else if (kind == PH_TPRED) {
         const int nt = Q.tp.d >> 7;
         for (int u = c * 4 + (et >> 5); u < R * nt; u += G * 4) tp_reduce_unit(Q.tp, u / nt, u % nt, lane);
@@ -339,10 +347,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const int Gp = (int)min((long long)min(G, Q.g.grid), U);
         if (gp.mode == EPI_QKV && ph + 1 < P.n_ph && P.ph[ph + 1].kind == PH_ATTN) {
           // the attention phase's context K/V does not depend on this phase:
-          // stream this CTA's first chunk into smem while QKV runs
-          const AttnParams& an = P.ph[ph + 1].a;
-          pref_item = an.hd == 128 ? attn_prefetch_kv<128, 4>(an, attn_smem, et, c)
-                                   : attn_prefetch_kv<64, 4>(an, attn_smem, et, c);
+          // start this CTA's first ring stages while QKV runs
+          if (et == 0) {
+            const AttnParams& an = P.ph[ph + 1].a;
+            attn_npref = an.hd == 128 ? attn_prefetch_kv<128>(an, attn_smem, abars, attn_seq, c, G)
+                                      : attn_prefetch_kv<64>(an, attn_smem, abars, attn_seq, c, G);
+          }
         }
         if (c < Gp) {
           epi_prepare<RP>(gp, e, R, pos0, scratch, rstd, kvrow);

@@ -51,6 +51,7 @@ struct ps_stage {
   std::vector<const __nv_bfloat16*> lw;   // [L][9]
   std::vector<LayerMaps> maps;
   CUtensorMap map_lm;
+  CUtensorMap map_kv;      // the KV pool as [rows][hd] bf16 rows (attention TMA, box 16 rows)
   CUtensorMap map_xg[3], map_att[3], map_h[3];   // per rows bucket (16, 32, 64)
   // KV pool (borrowed) + paging
   __nv_bfloat16* kv = nullptr;
@@ -111,7 +112,7 @@ struct ps_stage {
   SynthParams h_syn{};
   int32_t* d_S = nullptr;
   int n_prompt = 0;
-  int ss_ld = 0, xg_ld = 0, max_chunks = 0, max_rb = 0, attn_grid = 0;
+  int ss_ld = 0, xg_ld = 0, max_chunks = 0, max_rb = 0, attn_grid = 0, attn_sc = 1;
   GemmShape gs_qkv, gs_o, gs_gu, gs_d, gs_lm;
   int lm_tiles = 0;
   // token buffer O_i
@@ -230,13 +231,15 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
     case K_ATTN: {  // split-KV decode attention (a6)
       P.kind = PH_ATTN;
       AttnParams& a = P.a;
-      a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.kv = S->kv; a.page_table = S->d_page_table;
-      a.page_size = S->page_size; a.page_stride = S->page_elems; a.layer = l; a.hkv = sh.n_kv_heads;
+      a.step = S->d_in; a.q = S->q; a.ld_q = hq; a.page_table = S->d_page_table;
+      a.page_size = S->page_size; a.page_shift = __builtin_ctz((unsigned)S->page_size);
+      a.rows_per_page = S->page_elems / sh.head_dim; a.layer = l; a.hkv = sh.n_kv_heads;
       a.H = sh.n_heads; a.hd = sh.head_dim; a.scale_log2 = 1.4426950408889634f / std::sqrt((float)sh.head_dim);
-      a.max_chunks = S->max_chunks; a.max_rb = S->max_rb;
-      a.ws_o = S->attn_o; a.ws_ml = S->attn_ml; a.counters = S->attn_counters;
+      a.max_chunks = S->max_chunks; a.max_rb = S->max_rb; a.sc = S->attn_sc;
+      a.ws_o = S->attn_o; a.ws_ml = S->attn_ml;
       a.out = S->att; a.ld_out = hq;
       a.dbg = S->attn_dbg;   // PS_TRACE builds only (null otherwise)
+      hm = HostMaps{&S->map_kv, &S->map_kv, &S->map_kv, &S->map_kv};
       return;
     }
     case K_O: {     // O projection + residual; writes x∘g_mlp and sumsq (a7)
@@ -319,6 +322,10 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     MegaPhase P;
     HostMaps hm;
     build_phase(S, b, kind, l, P, hm);
+    if (P.kind == PH_ATTN) {   // the KV map; index patched to a pointer below
+      P.a.kvmap = reinterpret_cast<const CUtensorMap*>(maps.size() + 1);
+      maps.push_back(*hm.a0);
+    }
     if (P.kind == PH_GEMM) {   // device map indices, patched to pointers below
       const size_t base = maps.size();
       maps.push_back(*hm.a0);
@@ -380,6 +387,7 @@ static ps_status build_mega(ps_stage* S, int b, bool with_head) {
     for (size_t i = 0; i < ph.size(); ++i) ph[i].g.dbg = S->epi_dbg + i * g_num_sms * 4;
   const CUtensorMap* dm = S->mega_maps[key];
   for (auto& P : ph) {
+    if (P.kind == PH_ATTN) P.a.kvmap = dm + (reinterpret_cast<size_t>(P.a.kvmap) - 1);
     if (P.kind != PH_GEMM) continue;
     const size_t base = reinterpret_cast<size_t>(P.mA0) - 1;
     P.mA0 = dm + base;
@@ -803,17 +811,23 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMalloc(&S->amax, (size_t)kMaxRows * 8));
   S_TRY(cudaMemset(S->amax, 0, (size_t)kMaxRows * 8));
   // --- attention workspace
-  S->max_chunks = (S->max_seq + kRowsCap + kAttnChunk - 1) / kAttnChunk;
+  // keys per attention work item: sc 64-key chunks, a per-stage constant
+  // (results must not depend on R or on the context length): one chunk up to
+  // 16K keys, then fewer, longer items (fewer partials for the combine) with
+  // >= 128 items per KV head at max_seq
+  {
+    const int chunks = (S->max_seq + kRowsCap + kAttnChunk - 1) / kAttnChunk;
+    S->attn_sc = std::max(1, std::min(8, chunks / 128));
+    S->max_chunks = (chunks + S->attn_sc - 1) / S->attn_sc;   // item partials per (head, row block)
+  }
   {
     const int g = sh.n_heads / sh.n_kv_heads;
-    S->max_rb = (kRowsCap * g + 63) / 64;   // attention row blocks of 64 query rows
+    S->max_rb = (kRowsCap * g + kAttnRB - 1) / kAttnRB;   // attention row blocks of kAttnRB query rows
   }
   S->attn_grid = std::min(sh.n_kv_heads * S->max_rb * S->max_chunks, 2 * n);
-  const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * 128;
+  const size_t attn_rows = (size_t)sh.n_kv_heads * S->max_rb * S->max_chunks * kAttnRB;
   S_TRY(cudaMalloc(&S->attn_o, attn_rows * sh.head_dim * 4));
   S_TRY(cudaMalloc(&S->attn_ml, attn_rows * 2 * 4));
-  S_TRY(cudaMalloc(&S->attn_counters, (size_t)sh.n_kv_heads * S->max_rb * 4));
-  S_TRY(cudaMemset(S->attn_counters, 0, (size_t)sh.n_kv_heads * S->max_rb * 4));
   // --- RoPE table
   {
     std::vector<float2> cs;
@@ -826,6 +840,14 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->page_elems = (long long)sh.n_layers * kKvPlanes * sh.n_kv_heads * S->page_size * sh.head_dim;
   const int lpages = (S->max_seq + kRowsCap + S->page_size - 1) / S->page_size;
   S->pages_total = S->page_elems ? (int)(o->kv_pool_bytes / (S->page_elems * 2)) : lpages;   // 0 layers: no KV
+  if (S->page_elems) {
+    // Attention stages load whole 16-key groups and mask the keys past the
+    // context: those must hold finite values (0 * NaN = NaN in P V), so the
+    // pool's pages start zeroed (later stale rows are finite K/V).
+    S_TRY(cudaMemset(S->kv, 0, (size_t)S->pages_total * S->page_elems * 2));
+    P_TRY(make_map_kv(&S->map_kv, S->kv, (uint64_t)S->pages_total * (S->page_elems / sh.head_dim), sh.head_dim,
+                      (uint64_t)sh.n_kv_heads * S->page_size));
+  }
   S->page_of.assign(lpages, -1);
   for (int p = S->pages_total - 1; p >= 0; --p) S->free_pages.push_back(p);
   S_TRY(cudaMalloc(&S->d_page_table, (size_t)lpages * 4));
@@ -1153,6 +1175,7 @@ ps_status ps_stage_get_info(const ps_stage* S, ps_stage_info* info) {
   info->n_fwd = S->n_fwd;
   info->max_window = S->max_window;
   info->max_seq = S->max_seq;
+  info->attn_sc = S->attn_sc;
   return PS_OK;
 }
 

@@ -383,3 +383,72 @@ extern "C" ps_status ps_test_tc_probe2(int32_t iters, int32_t depth, double* ns_
   *ns_per_unit = m / iters;   // per pair-unit: 4 MMAs of M = 256 (16 KB of weights per SM)
   return PS_OK;
 }
+
+// ============================================================================ mma.sync probe
+// 148 CTAs x `warps` warps; every warp issues iters x 8 m16n8k16 bf16 HMMAs
+// in `chains` independent accumulator chains (1, 2, 4 or 8).  Returns ns per
+// HMMA per warp (the issue interval one warp sees).
+template <int CH>
+__global__ void hmma_probe_kernel(int iters, unsigned long long* out) {
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  uint32_t a[4] = {0x3f803f80u ^ threadIdx.x, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u};
+  uint32_t b0 = 0x3c003c00u, b1 = 0x3c003c00u ^ threadIdx.x;
+  __syncthreads();
+  const unsigned long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float* d = acc[i % CH];
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+          "{%0,%1,%2,%3};"
+          : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+    }
+  }
+  const unsigned long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+  if ((threadIdx.x & 31) == 0 && blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+  if (s == 1234.5f) out[1] = 1;
+}
+
+extern "C" ps_status ps_test_hmma_probe(int32_t warps, int32_t chains, int32_t iters, double* ns_per_hmma,
+                                        double* cycles_per_hmma) {
+  unsigned long long* d;
+  CU_TRY(cudaMalloc(&d, 16));
+  int dev = 0, sms = 0, khz = 0;
+  CU_TRY(cudaGetDevice(&dev));
+  CU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU_TRY(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev));
+  auto launch = [&](int n) {
+    switch (chains) {
+      case 1: hmma_probe_kernel<1><<<sms, warps * 32>>>(n, d); break;
+      case 2: hmma_probe_kernel<2><<<sms, warps * 32>>>(n, d); break;
+      case 4: hmma_probe_kernel<4><<<sms, warps * 32>>>(n, d); break;
+      default: hmma_probe_kernel<8><<<sms, warps * 32>>>(n, d); break;
+    }
+  };
+  launch(100);
+  cudaEvent_t e0, e1;
+  CU_TRY(cudaEventCreate(&e0));
+  CU_TRY(cudaEventCreate(&e1));
+  CU_TRY(cudaEventRecord(e0, 0));
+  launch(iters);
+  CU_TRY(cudaEventRecord(e1, 0));
+  CU_TRY(cudaEventSynchronize(e1));
+  float ms;
+  CU_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  unsigned long long cyc = 0;
+  CU_TRY(cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost));
+  *ns_per_hmma = ms * 1e6 / ((double)iters * 8);
+  *cycles_per_hmma = (double)cyc / ((double)iters * 8);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  (void)khz;
+  return PS_OK;
+}

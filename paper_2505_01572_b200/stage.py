@@ -198,7 +198,7 @@ class Stage:
         return dict(n_tokens=i.n_tokens, kv_len=i.kv_len, pages_in_use=i.pages_in_use,
                     pages_total=i.pages_total, launches_per_verify=i.launches_per_verify,
                     last_fwd_ms=i.last_fwd_ms, sum_fwd_ms=i.sum_fwd_ms, n_fwd=i.n_fwd,
-                    max_window=i.max_window, max_seq=i.max_seq)
+                    max_window=i.max_window, max_seq=i.max_seq, attn_sc=i.attn_sc)
 
     def reset_timers(self):
         abi.check(abi.lib().ps_stage_reset_timers(self._h))

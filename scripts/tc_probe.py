@@ -18,3 +18,11 @@ for mode, name in MODES[int(sys.argv[1]) if len(sys.argv) > 1 else 0:]:
 ns = C.c_double()
 abi.test_check(L.ps_test_tc_probe2(50000, 4, C.byref(ns)))
 print(f"{'2-CTA M256 N32 4 MMA':18s} depth  4: {ns.value:8.1f} ns/unit (16 KB per SM)", flush=True)
+
+# mma.sync (legacy HMMA path, used by the decode attention): issue interval
+for warps in (1, 4):
+    for chains in (1, 2, 4, 8):
+        ns, cyc = C.c_double(), C.c_double()
+        abi.test_check(L.ps_test_hmma_probe(warps, chains, 20000, C.byref(ns), C.byref(cyc)))
+        print(f"HMMA m16n8k16 warps {warps} chains {chains}: {ns.value:6.2f} ns, {cyc.value:6.2f} cycles per HMMA per warp",
+              flush=True)

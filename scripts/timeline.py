@@ -106,7 +106,8 @@ for rep in range(a.reps + 1):
     ok = (at[:, 0] > done[pa - 1]) & (at[:, 0] < done[pa])
     if ok.any():
         rel = at[ok, :5] - done[pa - 1]
-        attn_st.append([np.median(rel[:, j]) for j in range(5)] + [rel[:, 4].max(), ok.sum()])
+        attn_st.append([np.median(rel[:, j]) for j in range(5)] + [rel[:, 4].max(), ok.sum()]
+                       + [np.median(at[ok, j]) for j in (5, 6, 7)])
 
 R = a.w + 1
 d, f, hq, hkv = s.d_model, s.d_ffn, s.n_heads * s.head_dim, s.n_kv_heads * s.head_dim
@@ -127,8 +128,9 @@ for k, v in mil.items():
     print(f"{k:8s} " + " ".join(f"{v[2*i]:6.2f}/{v[2*i+1]:6.2f}" for i in range(6)))
 if attn_st:
     v = np.array(attn_st, dtype=np.float64).mean(axis=0)
-    print(f"ATTN items (last layer, us after QKV done, median): start {v[0]/1e3:.2f} loaded {v[1]/1e3:.2f} "
-          f"softmax {v[2]/1e3:.2f} pv {v[3]/1e3:.2f} stored {v[4]/1e3:.2f} (max {v[5]/1e3:.2f}, {v[6]:.0f} CTAs)")
+    print(f"ATTN (last layer, us after QKV done, median over CTAs): start {v[0]/1e3:.2f} "
+          f"first softmax {v[2]/1e3:.2f} end {v[4]/1e3:.2f} (max {v[5]/1e3:.2f}, {v[6]:.0f} CTAs); "
+          f"warp 0 time in: wait+bar {v[7]/1e3:.2f} QK {v[8]/1e3:.2f} softmax+PV {v[9]/1e3:.2f}")
 print("stream-K reducers (us after the previous phase; max over reducer CTAs; wait/reduce med/max; epi after reduce max):")
 for k, v in sk.items():
     v = np.nanmean(np.array(v, dtype=np.float64), axis=0) / 1e3

@@ -37,16 +37,14 @@ ctxs = [int(x) for x in a.ctxs.split(",")]
 gammas = [int(x) for x in a.gammas.split(",")]
 s = synth.preset(a.shape)
 w = synth.make_weights(s, seed=1, device="cuda")
-max_seq = max(ctxs) + max(gammas) + 64
-st = Stage(s, w, max_seq=max_seq, max_window=max(1, max(gammas)))
 toks = [int(x) for x in synth.make_prompt(s.vocab, max(ctxs) + 1, seed=2)]
 win = [int(x) for x in synth.make_prompt(s.vocab, max(gammas), seed=3)]
-st.prefill(toks[:ctxs[0]])
 rows = []
 for c in ctxs:
-    st.resync(toks[:c])          # lazy catch-up to c tokens ...
-    st.verify([])                # ... folded into one untimed forward
-    st.kv_rollback(c)
+    # one stage per context, sized for it (max_seq sets the attention work-item
+    # size, DESIGN §5 "long context"); prompt through the 64-row prefill bucket
+    st = Stage(s, w, max_seq=c + max(gammas) + 64, max_window=max(1, max(gammas)))
+    st.prefill(toks[:c])
     for g in gammas:
         for _ in range(2):
             st.verify(win[:g])
@@ -63,7 +61,7 @@ for c in ctxs:
         gbs = byts / (ms * 1e-3) / 1e9
         rows.append({"ctx": c, "gamma": g, "rows": R, "ms": ms, "bytes": byts, "GB/s": gbs, "frac": gbs / peak})
         print(f"ctx {c:6d} gamma {g:2d} R {R:2d}: {ms:7.3f} ms  {gbs:7.0f} GB/s  {gbs / peak:.3f}", flush=True)
-st.close()
+    st.close()
 res = {"shape": a.shape, "peak_gbs": peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 7700",
        "reps": a.reps, "rows": rows}
 if a.out:

@@ -307,3 +307,50 @@ def test_prefill_64_row_chunks(name, layers, n):
     check_logits(l1, ref["logits"])
     check_verify((a1, n1), ref, 0)
     st.close()
+
+
+def _oracle_verify_incremental(w64, shape, x, d, chunk=512):
+    """oracle.llama.verify computed through the oracle's incremental Session
+    (prompt fed in `chunk`-token pieces, pinned equal to the full forward in
+    the CPU suite), so a 16K context never builds a 16K x 16K score matrix."""
+    sess = L.Session(w64, shape)
+    for i in range(0, len(x) - 1, chunk):
+        sess.hidden(x[i:min(i + chunk, len(x) - 1)])
+    z = sess.forward([x[-1]] + list(d))
+    pred = [L.greedy(r) for r in z]
+    a = L.first_mismatch(pred, d)
+    return dict(a=a, next=pred[a], pred=pred, logits=z, gaps=[L.top2_gap(r) for r in z])
+
+
+def test_long_context_16k_multichunk_items():
+    """a 16.6K context with the long-context attention items
+    (sc = 4 chunks = 256 keys per work item, streamed through the 16-key TMA
+    ring with an online softmax).  The window's rows straddle an item
+    boundary (position 16640 = 65 * 256): a verify over accepted drafts equals
+    the AR steps bit-exactly, and a verify with a rejection matches the oracle."""
+    from paper_2505_01572_b200 import Stage
+    s = replace(synth.preset("llama3.1-8b"), name="hd128-16k", n_layers=2, d_model=1024, n_heads=8,
+                n_kv_heads=2, d_ffn=1024, vocab=4096)
+    wt = synth.make_weights(s, seed=41, device="cuda")
+    w64 = synth.weights_to_numpy(wt)
+    n = 65 * 256 - 2
+    st = Stage(s, wt, max_seq=32768)         # sc = 4: 256-key items
+    assert st.info()["attn_sc"] == 4
+    prompt = list(synth.make_prompt(s.vocab, n, seed=42))
+    st.prefill(prompt)
+    rows = []
+    for _ in range(5):
+        a, nxt, lg = st.verify([], want_logits=True)
+        rows.append(lg[0])
+    stream = st.tokens()[n:]
+    st.prefill(prompt)
+    a, nxt, logits = st.verify(stream[:4], want_logits=True)
+    assert a == 4 and nxt == stream[4]
+    assert np.array_equal(logits, np.stack(rows))
+    st.prefill(prompt)
+    window = stream[:2] + [(stream[2] + 5) % s.vocab]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = _oracle_verify_incremental(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
