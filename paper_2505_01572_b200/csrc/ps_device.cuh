@@ -295,6 +295,12 @@ PS_DEV unsigned opaque_tid_x() {
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(v));
   return v;
 }
+// 2^x, ex2.approx.ftz (2 ulp; no denormal range fix-up)
+PS_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 PS_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 // Greedy key: larger logit wins, equal logits -> lower index wins (reading R12).

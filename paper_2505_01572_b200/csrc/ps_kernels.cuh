@@ -747,7 +747,8 @@ template <int HD> __host__ __device__ constexpr int attn_stage_bytes() { return 
 // smem: the ring (kAttnStages x [hd/64][plane][16 keys][128 B], 128B-swizzled
 // by TMA) + its full barriers; the S exchange uses the epilogue scratch area
 constexpr int attn_smem_bytes(int /*nw*/) { return kAttnStages * attn_stage_bytes<128>() + 64; }
-constexpr int kAttnXBytes = 4 * kAttnNG * 2 * 32 * 16;   // S exchange: [warp][group][n-tile][lane] float4 (x2 buffers)
+constexpr int kAttnXBytes = 4 * kAttnNG * 2 * 32 * 16;   // S exchange: [warp][group][n-tile][lane] float4
+constexpr int kAttnXBufs = kAttnNG == 1 ? 2 : 1;          // exchange buffers (in the 8.7 KB+ scratch area)
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -794,8 +795,10 @@ struct AttnGeom {
   PS_DEV int first(int c, int G) const { return (int)((long long)c * n_items / G); }
   // item -> KV head, row block, item index j, key range [kbeg, kend), stages
   PS_DEV void item(const AttnParams& p, int it, int& kh, int& rb, int& j, int& kbeg, int& kend, int& ns) const {
-    j = it % nsc;
-    rb = (it / nsc) % n_rb;
+    // row blocks fastest: the row blocks of one key range run back to back
+    // (mostly on one CTA), so the second read of those K/V stages hits L2
+    rb = it % n_rb;
+    j = (it / n_rb) % nsc;
     kh = it / (nsc * n_rb);
     kbeg = j * p.sc * kAttnChunk;
     kend = min(n_keys, (j + 1) * p.sc * kAttnChunk);
@@ -803,9 +806,8 @@ struct AttnGeom {
   }
 };
 
-// Ring producer state (one thread): the stream position of the next stage to
-// issue and the KV row of its first key (plane 0); the page is looked up one
-// stage ahead, so an issue never waits on the page table.
+// Ring producer state (one thread of the X-loader warp): the stream position
+// of the next stage to issue and the KV row of its first key (plane 0).
 struct AttnProducer {
   int item, s, ns, kbeg, kh;
   long long row;                       // pool row of key kbeg + 16 s, plane 0 (valid if more)
@@ -842,9 +844,9 @@ PS_DEV void attn_producer_seek(const AttnParams& p, const AttnGeom& gm, int it_e
 // per 64 dims.  Keys past the context are loaded too (finite: the pool is
 // zeroed at stage creation) and masked.
 template <int HD>
-PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t bars_u32, uint32_t seq, long long row) {
+PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t full_u32, uint32_t seq, long long row) {
   const int buf = seq % kAttnStages;
-  const uint32_t bar = bars_u32 + buf * 8;
+  const uint32_t bar = full_u32 + buf * 8;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(attn_stage_bytes<HD>())
                : "memory");
 #pragma unroll
@@ -853,30 +855,11 @@ PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t bars_u32
                 (int)row, 0, kEvictFirst);
 }
 
-// During the QKV phase: issue the first ring stages (up to kAttnStages) of this
-// CTA's stream whose keys all lie below pos0 (not rewritten by QKV).  Returns
-// how many were issued (they are the stream's stages seq .. seq + n - 1).
-template <int HD>
-PS_DEV int attn_prefetch_kv(const AttnParams& p, uint8_t* ring, uint64_t* bars, uint32_t seq, int cta, int ncta) {
-  const AttnGeom gm(p);
-  const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
-  AttnProducer u;
-  attn_producer_init(p, gm, it0, it_end, u);
-  int n = 0;
-  const int pos0 = p.step->pos0;
-  while (u.more && n < kAttnStages && u.kbeg + (u.s + 1) * kAttnStep <= pos0) {
-    attn_issue<HD>(p, smem_u32(ring), smem_u32(bars), seq + n, u.row);
-    ++n;
-    attn_producer_seek(p, gm, it_end, u);
-  }
-  return n;
-}
-
 // (noinline: ptxas allocates a called function's registers beside the
 // caller's live ones, so the megakernel keeps little live across the call)
 template <int HD>
-__device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* bars, float4* xbuf, int tid, int cta, int ncta,
-                     uint32_t& seq, int npref) {
+__device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, float4* xbuf,
+                                      int tid, int cta, int ncta, uint32_t& seq) {
   constexpr int DW = HD / 4;          // dims per warp
   constexpr int KS = DW / 16;         // k steps of QK per warp
   constexpr int NTO = DW / 8;         // output n-tiles per warp
@@ -889,23 +872,7 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   const float qscale = p.scale_log2;
   const int warp = tid >> 5, lane = tid & 31;
   const int d_own = warp * DW;
-  const uint32_t ring_u32 = smem_u32(ring), bars_u32 = smem_u32(bars), xbuf_u32 = smem_u32(xbuf);
-  // producer (thread 0): the next stage to issue, up to kAttnStages ahead
-  AttnProducer pu;
-  pu.more = false;
-  uint32_t pseq = seq;
-  if (tid == 0) {
-    attn_producer_init(p, gm, it0, it_end, pu);
-    for (int n = 0; n < npref && pu.more; ++n) {
-      attn_producer_seek(p, gm, it_end, pu);
-      ++pseq;
-    }
-    fence_proxy_async_global();          // this forward's new K/V rows (QKV epilogue stores) -> TMA
-    while (pu.more && pseq < seq + kAttnStages) {
-      attn_issue<HD>(p, ring_u32, bars_u32, pseq++, pu.row);
-      attn_producer_seek(p, gm, it_end, pu);
-    }
-  }
+  const uint32_t ring_u32 = smem_u32(ring), xbuf_u32 = smem_u32(xbuf);
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
 #if PS_TRACE
   unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
@@ -960,39 +927,47 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
     }
     const int k0 = kbeg + s * kAttnStep;
     const int buf = seq % kAttnStages;
-    mbar_wait(&bars[buf], (seq / kAttnStages) & 1);
+    mbar_wait(&full[buf], (seq / kAttnStages) & 1);
     PS_ATTN_LAP(tr_wait);
     const uint32_t sb = ring_u32 + buf * attn_stage_bytes<HD>();
     // ---- partial S over this warp's dims: 2 n-tiles (16 keys) per group
+    // (three accumulator sets -- q_hi k_hi, q_lo k_hi, q_hi k_lo -- summed in
+    // that order: dependent HMMA chains of KS instead of 3 KS)
     float sacc[kAttnNG][2][4];
 #pragma unroll
-    for (int gi = 0; gi < kAttnNG; ++gi)
+    for (int gi = 0; gi < kAttnNG; ++gi) {
+      float s3[3][2][4];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) sacc[gi][nt][0] = sacc[gi][nt][1] = sacc[gi][nt][2] = sacc[gi][nt][3] = 0.f;
+      for (int t = 0; t < 3; ++t)
 #pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-      const int kr = (lane & 7) + ((lane >> 4) << 3);
-      const int kd = d_own + kk * 16 + ((lane >> 3) & 1) * 8;
-      uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
-      ldsm_x4(sb + attn_sw(0, kr, kd), b0, b1, b2, b3);   // K_hi
-      ldsm_x4(sb + attn_sw(1, kr, kd), c0, c1, c2, c3);   // K_lo
+        for (int nt = 0; nt < 2; ++nt) s3[t][nt][0] = s3[t][nt][1] = s3[t][nt][2] = s3[t][nt][3] = 0.f;
+      if (gi < ngr) {
 #pragma unroll
-      for (int gi = 0; gi < kAttnNG; ++gi) {
-        if (gi < ngr) {
-          mma16816(sacc[gi][0], qh[gi][kk], b0, b1);
-          mma16816(sacc[gi][1], qh[gi][kk], b2, b3);
-          mma16816(sacc[gi][0], ql[gi][kk], b0, b1);
-          mma16816(sacc[gi][1], ql[gi][kk], b2, b3);
-          mma16816(sacc[gi][0], qh[gi][kk], c0, c1);
-          mma16816(sacc[gi][1], qh[gi][kk], c2, c3);
+        for (int kk = 0; kk < KS; ++kk) {
+          const int kr = (lane & 7) + ((lane >> 4) << 3);
+          const int kd = d_own + kk * 16 + ((lane >> 3) & 1) * 8;
+          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+          ldsm_x4(sb + attn_sw(0, kr, kd), b0, b1, b2, b3);   // K_hi
+          ldsm_x4(sb + attn_sw(1, kr, kd), c0, c1, c2, c3);   // K_lo
+          mma16816(s3[0][0], qh[gi][kk], b0, b1);
+          mma16816(s3[0][1], qh[gi][kk], b2, b3);
+          mma16816(s3[1][0], ql[gi][kk], b0, b1);
+          mma16816(s3[1][1], ql[gi][kk], b2, b3);
+          mma16816(s3[2][0], qh[gi][kk], c0, c1);
+          mma16816(s3[2][1], qh[gi][kk], c2, c3);
         }
       }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) sacc[gi][nt][q4] = (s3[0][nt][q4] + s3[1][nt][q4]) + s3[2][nt][q4];
     }
-    // ---- exchange: S = sum over the 4 warps' partials (fixed order).  Two
-    // buffers by stage parity: a warp writing stage s + 1's partials cannot
+    // ---- exchange: S = sum over the 4 warps' partials (fixed order).  With two
+    // buffers (by stage parity) a warp writing stage s + 1's partials cannot
     // overwrite stage s's before every warp has read them (it would have to
-    // pass stage s + 1's barrier first), so one barrier per stage suffices.
-    const uint32_t xb = xbuf_u32 + (seq & 1) * kAttnXBytes;
+    // pass stage s + 1's barrier first): one barrier per stage.  One buffer
+    // needs a second barrier after the reads.
+    const uint32_t xb = xbuf_u32 + (kAttnXBufs == 2 ? (seq & 1) * kAttnXBytes : 0);
 #pragma unroll
     for (int gi = 0; gi < kAttnNG; ++gi)
       if (gi < ngr)
@@ -1001,12 +976,6 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
           st_shared_v4(xb + ((((warp * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4), sacc[gi][nt][0], sacc[gi][nt][1],
                        sacc[gi][nt][2], sacc[gi][nt][3]);
     named_bar(2, 128);
-    // every warp is past its PV of stage seq - 1: that buffer (only) is free,
-    // so stage seq + 3 at the latest may be issued (3 in flight beside seq)
-    if (tid == 0 && pu.more && pseq < seq + kAttnStages) {
-      attn_issue<HD>(p, ring_u32, bars_u32, pseq++, pu.row);
-      attn_producer_seek(p, gm, it_end, pu);
-    }
 #pragma unroll
     for (int gi = 0; gi < kAttnNG; ++gi)
       if (gi < ngr)
@@ -1020,6 +989,7 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
           }
           sacc[gi][nt][0] = v.x; sacc[gi][nt][1] = v.y; sacc[gi][nt][2] = v.z; sacc[gi][nt][3] = v.w;
         }
+    if (kAttnXBufs == 1) named_bar(3, 128);   // single exchange buffer: all reads done before the next write
     PS_ATTN_LAP(tr_qk);
     // ---- V fragments (own dims) for the P V MMAs
     uint32_t vh[NTO / 2][4], vl[NTO / 2][4];
@@ -1050,7 +1020,7 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         const float mn = fmaxf(mrow[gi][hr], mx);
-        scale[hr] = (mrow[gi][hr] == -INFINITY) ? 0.f : exp2f(mrow[gi][hr] - mn);
+        scale[hr] = (mrow[gi][hr] == -INFINITY) ? 0.f : ex2_approx(mrow[gi][hr] - mn);
         mrow[gi][hr] = mn;
       }
       float lsum[2] = {0.f, 0.f};
@@ -1061,7 +1031,7 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int hr = q4 >> 1;
-          pv[q4] = (mrow[gi][hr] == -INFINITY) ? 0.f : exp2f(sacc[gi][nt][q4] - mrow[gi][hr]);
+          pv[q4] = (mrow[gi][hr] == -INFINITY) ? 0.f : ex2_approx(sacc[gi][nt][q4] - mrow[gi][hr]);
           lsum[hr] += pv[q4];
         }
         split_pack(pv[0], pv[1], pah[nt * 2 + 0], pal[nt * 2 + 0]);
@@ -1089,6 +1059,9 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
         mma16816(oacc[gi][2 * np + 1], pah, vl[np][2], vl[np][3]);
       }
     }
+    // this warp is done with the stage's buffer (K/V fragments are in registers)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[buf]);
     PS_ATTN_LAP(tr_pv);
     ++seq;
     if (++s == ns) {

@@ -73,7 +73,7 @@ struct MegaSmem {
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
   static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 1023) / 1024 * 1024;   // TMA 128B-swizzle dst
-  static_assert(128 * (epi_rows<RP>() + 1) * 4 >= 2 * kAttnXBytes, "attention S exchange lives in the scratch area");
+  static_assert(128 * (epi_rows<RP>() + 1) * 4 >= kAttnXBufs * kAttnXBytes, "attention S exchange lives in the scratch area");
   static constexpr int kAttnBytes = attn_smem_bytes(4);
   static constexpr int kOffBar = kOffAttn + kAttnBytes;
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
@@ -114,6 +114,36 @@ PS_DEV bool poll_ready(const unsigned* p, unsigned target) {
   return true;
 }
 
+// Attention K/V ring producer (one thread of the X-loader warp): this CTA's
+// stream of 16-key stages of attention phase pa, each issued once its buffer
+// is released by the 4 consumer warps.  Stages whose keys are all below pos0
+// go out immediately; the first one reaching the window's rows waits for the
+// QKV phase (pa - 1) to be published grid-wide (its K/V rows are new).
+template <int HD>
+__device__ __noinline__ void attn_produce(const MegaParams& P, int pa, const AttnParams& p, uint8_t* ring,
+                                          uint64_t* full, uint64_t* empty, uint32_t& seq, int cta, int ncta,
+                                          unsigned tgt_head, unsigned tgt_body) {
+  const AttnGeom gm(p);
+  const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
+  AttnProducer u;
+  attn_producer_init(p, gm, it0, it_end, u);
+  const int pos0 = p.step->pos0;
+  const uint32_t ring_u32 = smem_u32(ring), full_u32 = smem_u32(full);
+  bool qkv_seen = false;
+  while (u.more) {
+    if (!qkv_seen && u.kbeg + (u.s + 1) * kAttnStep > pos0) {
+      spin_until(P.done + (pa - 1), P.ph[pa - 1].head ? tgt_head : tgt_body, kSpinCapNs);
+      fence_proxy_async_global();
+      qkv_seen = true;
+    }
+    const int buf = seq % kAttnStages;
+    mbar_wait(&empty[buf], ((seq / kAttnStages) & 1) ^ 1);
+    attn_issue<HD>(p, ring_u32, full_u32, seq, u.row);
+    ++seq;
+    attn_producer_seek(p, gm, it_end, u);
+  }
+}
+
 template <int RP, int STAGES = mega_stages<RP>()>
 __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_constant__ MegaParams P) {
   using L = MegaSmem<RP, STAGES>;
@@ -129,7 +159,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   float* rstd = (float*)(smem + L::kOffRstd);
   long long* kvrow = (long long*)(smem + L::kOffKvRow);
   uint8_t* attn_smem = smem + L::kOffAttn;
-  uint64_t* abars = (uint64_t*)(attn_smem + kAttnStages * attn_stage_bytes<128>());   // attention ring full barriers
+  uint64_t* afull = (uint64_t*)(attn_smem + kAttnStages * attn_stage_bytes<128>());   // attention ring barriers
+  uint64_t* aempty = afull + kAttnStages;
   uint64_t* full = (uint64_t*)(smem + L::kOffBar);
   uint64_t* empty = full + kMegaStages;
   uint64_t* tfull = empty + kMegaStages;
@@ -147,7 +178,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMegaStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
-    for (int s = 0; s < kAttnStages; ++s) mbar_init(&abars[s], 1);
+    for (int s = 0; s < kAttnStages; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], 4); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -207,10 +238,19 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     // counter: relaxed polls, one acquire, then a proxy fence so this CTA's
     // TMA (async proxy) sees the other CTAs' generic-proxy epilogue stores).
     if (lane == 0) {
-      uint32_t it = 0;
+      uint32_t it = 0, aseq = 0;
       int cur_ph = -1;
       for_units([&](int ph, const MegaPhase& Q, long long, int, int kb) {
         if (ph != cur_ph) {
+          // attention phases between the last GEMM phase and this one: this
+          // warp feeds their K/V ring (keys below pos0 at once, while QKV still
+          // runs; the rest once QKV is published)
+          for (int pa = cur_ph + 1; pa < ph; ++pa)
+            if (P.ph[pa].kind == PH_ATTN) {
+              const AttnParams& ap = P.ph[pa].a;
+              if (ap.hd == 128) attn_produce<128>(P, pa, ap, attn_smem, afull, aempty, aseq, c, G, tgt_head, tgt_body);
+              else attn_produce<64>(P, pa, ap, attn_smem, afull, aempty, aseq, c, G, tgt_head, tgt_body);
+            }
           tma_prefetch_desc(Q.mX);
           cur_ph = ph;
           spin_until(P.done + (ph - 1), P.ph[ph - 1].head ? tgt_head : tgt_body, kSpinCapNs);
@@ -224,6 +264,14 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         tma_load_2d(sX + slot * L::kXBytes + RP * 128, Q.mX, &full[slot], kb * 64, kRowsCap, kEvictLast);
         ++it;
       });
+      // attention phases after this CTA's last GEMM unit (none in the current
+      // phase tables; kept so a CTA without later GEMM units still feeds them)
+      for (int pa = cur_ph + 1; pa < P.n_ph; ++pa)
+        if (P.ph[pa].kind == PH_ATTN) {
+          const AttnParams& ap = P.ph[pa].a;
+          if (ap.hd == 128) attn_produce<128>(P, pa, ap, attn_smem, afull, aempty, aseq, c, G, tgt_head, tgt_body);
+          else attn_produce<64>(P, pa, ap, attn_smem, afull, aempty, aseq, c, G, tgt_head, tgt_body);
+        }
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
@@ -277,7 +325,6 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
     const int et0 = threadIdx.x - 64;                  // 0..127 in warp order 2..5
     uint32_t nacc = 0;
     uint32_t attn_seq = 0;                             // attention ring stages consumed so far
-    int attn_npref = 0;                                // ... and issued ahead during QKV (thread et 0)
     // StepIn -> smem once: every later read of the step (rows, positions,
     // generation, flags) in the epilogues / attention / argmax is a shared-
     // memory hit instead of a global round trip on a phase's critical path.
@@ -329,9 +376,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (Q.a.hd == 128) attn_run<128>(Q.a, attn_smem, abars, (float4*)scratch, et, c, G, attn_seq, attn_npref);
-        else attn_run<64>(Q.a, attn_smem, abars, (float4*)scratch, et, c, G, attn_seq, attn_npref);
-        attn_npref = 0;
+        if (Q.a.hd == 128) attn_run<128>(Q.a, attn_smem, afull, aempty, (float4*)scratch, et, c, G, attn_seq);
+        else attn_run<64>(Q.a, attn_smem, afull, aempty, (float4*)scratch, et, c, G, attn_seq);
       } else if (kind == PH_ACOMB) {
         if (Q.a.hd == 128) attn_combine<128>(Q.a, scratch, et, c, G);
         else attn_combine<64>(Q.a, scratch, et, c, G);
@@ -345,15 +391,6 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const int kbt = gp.kb_total;
         const long long U = (long long)gp.n_tiles * kbt;
         const int Gp = (int)min((long long)min(G, Q.g.grid), U);
-        if (gp.mode == EPI_QKV && ph + 1 < P.n_ph && P.ph[ph + 1].kind == PH_ATTN) {
-          // the attention phase's context K/V does not depend on this phase:
-          // start this CTA's first ring stages while QKV runs
-          if (et == 0) {
-            const AttnParams& an = P.ph[ph + 1].a;
-            attn_npref = an.hd == 128 ? attn_prefetch_kv<128>(an, attn_smem, abars, attn_seq, c, G)
-                                      : attn_prefetch_kv<64>(an, attn_smem, abars, attn_seq, c, G);
-          }
-        }
         if (c < Gp) {
           epi_prepare<RP>(gp, e, R, pos0, scratch, rstd, kvrow);
           const long long ub = sk_begin(U, Gp, c), ue = sk_begin(U, Gp, c + 1);
