@@ -857,12 +857,21 @@ PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t full_u32
 
 // (noinline: ptxas allocates a called function's registers beside the
 // caller's live ones, so the megakernel keeps little live across the call)
+//
+// Software-pipelined over the CTA's stage stream: iteration t sums stage t's
+// S partials, computes stage t + 1's partial Q K^T (its HMMAs overlap stage
+// t's softmax), then runs stage t's online softmax and P V; one barrier per
+// iteration publishes the t + 1 partials.  Stage t + 1 may start the next
+// item: its geometry and query fragments are loaded before its Q K^T, while
+// stage t's item state is finished (partial written) after its P V.
 template <int HD>
 __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, float4* xbuf,
                                       int tid, int cta, int ncta, uint32_t& seq) {
+  static_assert(kAttnNG == 1, "one 16-row MMA group per item");
   constexpr int DW = HD / 4;          // dims per warp
   constexpr int KS = DW / 16;         // k steps of QK per warp
   constexpr int NTO = DW / 8;         // output n-tiles per warp
+  constexpr uint32_t SB = attn_stage_bytes<HD>();
   const AttnGeom gm(p);
   const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
   if (it0 >= it_end) return;
@@ -873,8 +882,20 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   const int warp = tid >> 5, lane = tid & 31;
   const int d_own = warp * DW;
   const uint32_t ring_u32 = smem_u32(ring), xbuf_u32 = smem_u32(xbuf);
-  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
+  // per-lane ldmatrix offsets inside a stage (K: non-transposed, V: transposed)
+  uint32_t koff[KS], voff[NTO / 2];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk)
+    koff[kk] = attn_sw(0, (lane & 7) + ((lane >> 4) << 3), d_own + kk * 16 + ((lane >> 3) & 1) * 8);
+#pragma unroll
+  for (int np = 0; np < NTO / 2; ++np)
+    voff[np] = attn_sw(2, (lane & 7) + ((lane >> 3) & 1) * 8, d_own + np * 16 + (lane >> 4) * 8);
+  constexpr uint32_t PL = kAttnStep * 128;   // plane stride inside a 64-dim block
+  // exchange slot of this thread (buffer 0; buffer 1 at + kAttnXBytes)
+  const uint32_t xw = xbuf_u32 + ((warp * 2) * 32 + lane) * 16;   // this warp's n-tile 0 slot
+  const uint32_t xr = xbuf_u32 + lane * 16;                          // warp 0's n-tile 0 slot
 #if PS_TRACE
+  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
   unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
 #define PS_ATTN_LAP(acc)                         \
   do {                                           \
@@ -887,207 +908,198 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   do {                   \
   } while (0)
 #endif
-  // consumer cursor
-  int item = it0, s = 0, ns = 0, kbeg = 0, kend = 0, kh = 0, rb = 0, j = 0, ngr = 0;
-  int qpos[kAttnNG][2];
-  uint32_t qh[kAttnNG][KS][4], ql[kAttnNG][KS][4];
-  float mrow[kAttnNG][2], lrow[kAttnNG][2];
-  float oacc[kAttnNG][NTO][4];
+  // ---- item state: cur (stage t) and nxt (stage t + 1)
+  int c_item = it0, c_s = 0, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_ok;
+  int c_qpos[2];
+  int n_item = it0, n_s = 0, n_ns = 0, n_kbeg = 0, n_kend = 0, n_kh = 0, n_rb = 0, n_j = 0, n_ok = 0;
+  int n_qpos[2];
+  uint32_t qh[KS][4], ql[KS][4];
+  auto load_item = [&](int it, int& ns, int& kbeg, int& kend, int& kh, int& rb, int& j, int& ok, int* qpos) {
+    gm.item(p, it, kh, rb, j, kbeg, kend, ns);
+    const int m0 = rb * kAttnRB;
+    const int mrows = min(kAttnRB, gm.rows - m0);
+    ok = 1;
+    int qoff[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int m = (lane >> 2) + hr * 8;
+      const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
+      qoff[hr] = m < mrows ? r * ld_q + h * HD : -1;
+      qpos[hr] = min(kend - 1, pos0 + r);     // last key this row sees in this item
+    }
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+      for (int jq = 0; jq < 4; ++jq) {
+        const int o = qoff[jq & 1];
+        const int d = d_own + kk * 16 + (lane & 3) * 2 + (jq >> 1) * 8;
+        const float2 qv = o >= 0 ? *reinterpret_cast<const float2*>(qp + o + d) : make_float2(0.f, 0.f);
+        split_pack(qv.x * qscale, qv.y * qscale, qh[kk][jq], ql[kk][jq]);
+      }
+  };
+  // partial S of stage `u` (ring sequence number) over this warp's dims -> exchange buffer u & 1
+  auto qk_partial = [&](uint32_t u) {
+    const int buf = u % kAttnStages;
+    mbar_wait(&full[buf], (u / kAttnStages) & 1);
+    const uint32_t sb = ring_u32 + buf * SB;
+    float s3[3][2][4];
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) s3[t][nt][0] = s3[t][nt][1] = s3[t][nt][2] = s3[t][nt][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+      ldsm_x4(sb + koff[kk], b0, b1, b2, b3);        // K_hi
+      ldsm_x4(sb + PL + koff[kk], c0, c1, c2, c3);   // K_lo
+      mma16816(s3[0][0], qh[kk], b0, b1);
+      mma16816(s3[0][1], qh[kk], b2, b3);
+      mma16816(s3[1][0], ql[kk], b0, b1);
+      mma16816(s3[1][1], ql[kk], b2, b3);
+      mma16816(s3[2][0], qh[kk], c0, c1);
+      mma16816(s3[2][1], qh[kk], c2, c3);
+    }
+    const uint32_t xb = xw + (u & 1) * kAttnXBytes;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+      st_shared_v4(xb + nt * 512, (s3[0][nt][0] + s3[1][nt][0]) + s3[2][nt][0],
+                   (s3[0][nt][1] + s3[1][nt][1]) + s3[2][nt][1], (s3[0][nt][2] + s3[1][nt][2]) + s3[2][nt][2],
+                   (s3[0][nt][3] + s3[1][nt][3]) + s3[2][nt][3]);
+  };
+  float mrow[2], lrow[2];
+  float oacc[NTO][4];
+  auto reset_state = [&]() {
+    mrow[0] = mrow[1] = -INFINITY;
+    lrow[0] = lrow[1] = 0.f;
+#pragma unroll
+    for (int n = 0; n < NTO; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+  };
+  // ---- prologue: stage 0's partial S
+  load_item(c_item, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_ok, c_qpos);
+  reset_state();
+  qk_partial(seq);
+  named_bar(2, 128);
   while (true) {
-    if (s == 0) {
-      // ---- new item: geometry, this warp's query fragments (own dims), state
-      gm.item(p, item, kh, rb, j, kbeg, kend, ns);
-      const int m0 = rb * kAttnRB;
-      const int mrows = min(kAttnRB, gm.rows - m0);
-      ngr = (mrows + 15) >> 4;
+    // ---- S of stage t (fixed warp order)
+    float sacc[2][4];
+    {
+      const uint32_t xb = xr + (seq & 1) * kAttnXBytes;
 #pragma unroll
-      for (int gi = 0; gi < kAttnNG; ++gi) {
-        int qoff[2];
+      for (int nt = 0; nt < 2; ++nt) {
+        float4 v = ld_shared_v4(xb + nt * 512);
 #pragma unroll
-        for (int hr = 0; hr < 2; ++hr) {
-          const int m = gi * 16 + (lane >> 2) + hr * 8;
-          const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-          qoff[hr] = m < mrows ? r * ld_q + h * HD : -1;
-          qpos[gi][hr] = min(kend - 1, pos0 + r);    // last key this row sees in this item
+        for (int w = 1; w < 4; ++w) {
+          const float4 x = ld_shared_v4(xb + nt * 512 + w * 1024);
+          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
         }
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk)
-#pragma unroll
-          for (int jq = 0; jq < 4; ++jq) {
-            const int o = qoff[jq & 1];
-            const int d = d_own + kk * 16 + (lane & 3) * 2 + (jq >> 1) * 8;
-            const float2 qv = o >= 0 ? *reinterpret_cast<const float2*>(qp + o + d) : make_float2(0.f, 0.f);
-            split_pack(qv.x * qscale, qv.y * qscale, qh[gi][kk][jq], ql[gi][kk][jq]);
-          }
-        mrow[gi][0] = mrow[gi][1] = -INFINITY;
-        lrow[gi][0] = lrow[gi][1] = 0.f;
-#pragma unroll
-        for (int n = 0; n < NTO; ++n) oacc[gi][n][0] = oacc[gi][n][1] = oacc[gi][n][2] = oacc[gi][n][3] = 0.f;
+        sacc[nt][0] = v.x; sacc[nt][1] = v.y; sacc[nt][2] = v.z; sacc[nt][3] = v.w;
       }
     }
-    const int k0 = kbeg + s * kAttnStep;
-    const int buf = seq % kAttnStages;
-    mbar_wait(&full[buf], (seq / kAttnStages) & 1);
     PS_ATTN_LAP(tr_wait);
-    const uint32_t sb = ring_u32 + buf * attn_stage_bytes<HD>();
-    // ---- partial S over this warp's dims: 2 n-tiles (16 keys) per group
-    // (three accumulator sets -- q_hi k_hi, q_lo k_hi, q_hi k_lo -- summed in
-    // that order: dependent HMMA chains of KS instead of 3 KS)
-    float sacc[kAttnNG][2][4];
-#pragma unroll
-    for (int gi = 0; gi < kAttnNG; ++gi) {
-      float s3[3][2][4];
-#pragma unroll
-      for (int t = 0; t < 3; ++t)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) s3[t][nt][0] = s3[t][nt][1] = s3[t][nt][2] = s3[t][nt][3] = 0.f;
-      if (gi < ngr) {
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int kr = (lane & 7) + ((lane >> 4) << 3);
-          const int kd = d_own + kk * 16 + ((lane >> 3) & 1) * 8;
-          uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
-          ldsm_x4(sb + attn_sw(0, kr, kd), b0, b1, b2, b3);   // K_hi
-          ldsm_x4(sb + attn_sw(1, kr, kd), c0, c1, c2, c3);   // K_lo
-          mma16816(s3[0][0], qh[gi][kk], b0, b1);
-          mma16816(s3[0][1], qh[gi][kk], b2, b3);
-          mma16816(s3[1][0], ql[gi][kk], b0, b1);
-          mma16816(s3[1][1], ql[gi][kk], b2, b3);
-          mma16816(s3[2][0], qh[gi][kk], c0, c1);
-          mma16816(s3[2][1], qh[gi][kk], c2, c3);
-        }
+    // ---- stage t + 1: next position in the stream; its partial S
+    const bool more = (c_s + 1 < c_ns) || (c_item + 1 < it_end);
+    if (more) {
+      if (c_s + 1 < c_ns) {
+        n_item = c_item; n_s = c_s + 1; n_ns = c_ns; n_kbeg = c_kbeg; n_kend = c_kend; n_kh = c_kh; n_rb = c_rb;
+        n_j = c_j; n_ok = c_ok; n_qpos[0] = c_qpos[0]; n_qpos[1] = c_qpos[1];
+      } else {
+        n_item = c_item + 1;
+        n_s = 0;
+        load_item(n_item, n_ns, n_kbeg, n_kend, n_kh, n_rb, n_j, n_ok, n_qpos);
       }
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) sacc[gi][nt][q4] = (s3[0][nt][q4] + s3[1][nt][q4]) + s3[2][nt][q4];
+      qk_partial(seq + 1);
     }
-    // ---- exchange: S = sum over the 4 warps' partials (fixed order).  With two
-    // buffers (by stage parity) a warp writing stage s + 1's partials cannot
-    // overwrite stage s's before every warp has read them (it would have to
-    // pass stage s + 1's barrier first): one barrier per stage.  One buffer
-    // needs a second barrier after the reads.
-    const uint32_t xb = xbuf_u32 + (kAttnXBufs == 2 ? (seq & 1) * kAttnXBytes : 0);
-#pragma unroll
-    for (int gi = 0; gi < kAttnNG; ++gi)
-      if (gi < ngr)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-          st_shared_v4(xb + ((((warp * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4), sacc[gi][nt][0], sacc[gi][nt][1],
-                       sacc[gi][nt][2], sacc[gi][nt][3]);
-    named_bar(2, 128);
-#pragma unroll
-    for (int gi = 0; gi < kAttnNG; ++gi)
-      if (gi < ngr)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          float4 v = ld_shared_v4(xb + ((((0 * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4));
-#pragma unroll
-          for (int w = 1; w < 4; ++w) {
-            const float4 x = ld_shared_v4(xb + ((((w * kAttnNG + gi) * 2 + nt) * 32 + lane) << 4));
-            v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
-          }
-          sacc[gi][nt][0] = v.x; sacc[gi][nt][1] = v.y; sacc[gi][nt][2] = v.z; sacc[gi][nt][3] = v.w;
-        }
-    if (kAttnXBufs == 1) named_bar(3, 128);   // single exchange buffer: all reads done before the next write
     PS_ATTN_LAP(tr_qk);
-    // ---- V fragments (own dims) for the P V MMAs
+    // ---- stage t: mask, online softmax, O (own dims) = O * scale + P V
+    const int k0 = c_kbeg + c_s * kAttnStep;
+    const uint32_t sb = ring_u32 + (seq % kAttnStages) * SB;
     uint32_t vh[NTO / 2][4], vl[NTO / 2][4];
 #pragma unroll
     for (int np = 0; np < NTO / 2; ++np) {
-      const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
-      const int vd = d_own + np * 16 + (lane >> 4) * 8;
-      ldsm_x4_t(sb + attn_sw(2, vr, vd), vh[np][0], vh[np][1], vh[np][2], vh[np][3]);   // V_hi
-      ldsm_x4_t(sb + attn_sw(3, vr, vd), vl[np][0], vl[np][1], vl[np][2], vl[np][3]);   // V_lo
+      ldsm_x4_t(sb + voff[np], vh[np][0], vh[np][1], vh[np][2], vh[np][3]);            // V_hi
+      ldsm_x4_t(sb + PL + voff[np], vl[np][0], vl[np][1], vl[np][2], vl[np][3]);       // V_lo
     }
+    float scale[2];
 #pragma unroll
-    for (int gi = 0; gi < kAttnNG; ++gi) {
-      if (gi >= ngr) continue;
-      // ---- causal / length mask, online softmax (rows lane/4 and lane/4 + 8)
-      float scale[2];
+    for (int hr = 0; hr < 2; ++hr) {
+      float mx = -INFINITY;
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        float mx = -INFINITY;
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int e2 = 0; e2 < 2; ++e2) {
-            const int key = k0 + nt * 8 + (lane & 3) * 2 + e2;
-            float& sv = sacc[gi][nt][hr * 2 + e2];
-            if (key > qpos[gi][hr]) sv = -INFINITY;
-            mx = fmaxf(mx, sv);
-          }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float mn = fmaxf(mrow[gi][hr], mx);
-        scale[hr] = (mrow[gi][hr] == -INFINITY) ? 0.f : ex2_approx(mrow[gi][hr] - mn);
-        mrow[gi][hr] = mn;
-      }
-      float lsum[2] = {0.f, 0.f};
-      uint32_t pah[4], pal[4];             // P as the A fragment (16 rows x 16 keys), hi / lo
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        float pv[4];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int hr = q4 >> 1;
-          pv[q4] = (mrow[gi][hr] == -INFINITY) ? 0.f : ex2_approx(sacc[gi][nt][q4] - mrow[gi][hr]);
-          lsum[hr] += pv[q4];
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int key = k0 + nt * 8 + (lane & 3) * 2 + e2;
+          float& sv = sacc[nt][hr * 2 + e2];
+          if (key > c_qpos[hr]) sv = -INFINITY;
+          mx = fmaxf(mx, sv);
         }
-        split_pack(pv[0], pv[1], pah[nt * 2 + 0], pal[nt * 2 + 0]);
-        split_pack(pv[2], pv[3], pah[nt * 2 + 1], pal[nt * 2 + 1]);
-      }
-#pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 1);
-        lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 2);
-        lrow[gi][hr] = lrow[gi][hr] * scale[hr] + lsum[hr];
-      }
-      // ---- O (own dims) = O * scale + P V
-#pragma unroll
-      for (int n = 0; n < NTO; ++n) {
-        oacc[gi][n][0] *= scale[0]; oacc[gi][n][1] *= scale[0];
-        oacc[gi][n][2] *= scale[1]; oacc[gi][n][3] *= scale[1];
-      }
-#pragma unroll
-      for (int np = 0; np < NTO / 2; ++np) {
-        mma16816(oacc[gi][2 * np], pah, vh[np][0], vh[np][1]);
-        mma16816(oacc[gi][2 * np + 1], pah, vh[np][2], vh[np][3]);
-        mma16816(oacc[gi][2 * np], pal, vh[np][0], vh[np][1]);
-        mma16816(oacc[gi][2 * np + 1], pal, vh[np][2], vh[np][3]);
-        mma16816(oacc[gi][2 * np], pah, vl[np][0], vl[np][1]);
-        mma16816(oacc[gi][2 * np + 1], pah, vl[np][2], vl[np][3]);
-      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(mrow[hr], mx);
+      scale[hr] = (mrow[hr] == -INFINITY) ? 0.f : ex2_approx(mrow[hr] - mn);
+      mrow[hr] = mn;
     }
-    // this warp is done with the stage's buffer (K/V fragments are in registers)
+    float lsum[2] = {0.f, 0.f};
+    uint32_t pah[4], pal[4];               // P as the A fragment (16 rows x 16 keys), hi / lo
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      float pv[4];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int hr = q4 >> 1;
+        pv[q4] = (mrow[hr] == -INFINITY) ? 0.f : ex2_approx(sacc[nt][q4] - mrow[hr]);
+        lsum[hr] += pv[q4];
+      }
+      split_pack(pv[0], pv[1], pah[nt * 2 + 0], pal[nt * 2 + 0]);
+      split_pack(pv[2], pv[3], pah[nt * 2 + 1], pal[nt * 2 + 1]);
+    }
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 1);
+      lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 2);
+      lrow[hr] = lrow[hr] * scale[hr] + lsum[hr];
+    }
+#pragma unroll
+    for (int n = 0; n < NTO; ++n) {
+      oacc[n][0] *= scale[0]; oacc[n][1] *= scale[0];
+      oacc[n][2] *= scale[1]; oacc[n][3] *= scale[1];
+    }
+#pragma unroll
+    for (int np = 0; np < NTO / 2; ++np) {
+      mma16816(oacc[2 * np], pah, vh[np][0], vh[np][1]);
+      mma16816(oacc[2 * np + 1], pah, vh[np][2], vh[np][3]);
+      mma16816(oacc[2 * np], pal, vh[np][0], vh[np][1]);
+      mma16816(oacc[2 * np + 1], pal, vh[np][2], vh[np][3]);
+      mma16816(oacc[2 * np], pah, vl[np][0], vl[np][1]);
+      mma16816(oacc[2 * np + 1], pah, vl[np][2], vl[np][3]);
+    }
+    // this warp is done with stage t's buffer (K/V fragments are in registers)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[buf]);
+    if (lane == 0) mbar_arrive(&empty[seq % kAttnStages]);
     PS_ATTN_LAP(tr_pv);
-    ++seq;
-    if (++s == ns) {
+    if (c_s + 1 == c_ns) {
       // ---- item partial -> workspace [kh][rb][j][kAttnRB rows][HD] (own dims; m, l by warp 0)
-      const size_t base = (size_t)((kh * p.max_rb + rb) * p.max_chunks + j) * kAttnRB;
+      const size_t base = (size_t)((c_kh * p.max_rb + c_rb) * p.max_chunks + c_j) * kAttnRB;
 #pragma unroll
-      for (int gi = 0; gi < kAttnNG; ++gi) {
-        if (gi >= ngr) continue;
+      for (int hr = 0; hr < 2; ++hr) {
+        const int m = (lane >> 2) + hr * 8;
+        float* op = p.ws_o + (base + m) * HD + d_own;
 #pragma unroll
-        for (int hr = 0; hr < 2; ++hr) {
-          const int m = gi * 16 + (lane >> 2) + hr * 8;
-          float* op = p.ws_o + (base + m) * HD + d_own;
-#pragma unroll
-          for (int n = 0; n < NTO; ++n)
-            __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2),
-                   make_float2(oacc[gi][n][hr * 2], oacc[gi][n][hr * 2 + 1]));
-          if (warp == 0 && (lane & 3) == 0)
-            __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[gi][hr], lrow[gi][hr]));
-        }
+        for (int n = 0; n < NTO; ++n)
+          __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2), make_float2(oacc[n][hr * 2], oacc[n][hr * 2 + 1]));
+        if (warp == 0 && (lane & 3) == 0)
+          __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[hr], lrow[hr]));
       }
-      if (++item >= it_end) break;
-      s = 0;
+      reset_state();
     }
+    ++seq;
+    if (!more) break;
+    c_item = n_item; c_s = n_s; c_ns = n_ns; c_kbeg = n_kbeg; c_kend = n_kend; c_kh = n_kh; c_rb = n_rb; c_j = n_j;
+    c_ok = n_ok; c_qpos[0] = n_qpos[0]; c_qpos[1] = n_qpos[1];
+    named_bar(2, 128);                       // stage t + 1's partials are published
   }
-  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
+  (void)c_ok;
 #if PS_TRACE
+  if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
   if (tid == 0 && p.dbg) {
     p.dbg[cta * 8 + 5] = tr_wait;
     p.dbg[cta * 8 + 6] = tr_qk;
