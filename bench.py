@@ -511,65 +511,77 @@ def k3_configs(args, peaks, reuse):
     async PipeSpec modes (synthetic alpha per link, ps_run_opts.alpha).  Each
     mode's output must equal M_K's autoregressive output.  Reports tokens/s
     (decode wall clock), the speedup over AR and the target's verify pass."""
+    import gc
+
     import torch
 
-    import synth
-    from paper_2505_01572_b200 import Stage, pipeline_run
-    from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
     out = {}
     for cname in ("c3", "c4"):
-        cfg = LAYOUT_CONFIGS[cname]
         t0 = time.perf_counter()
         try:
-            shapes = [synth.preset(m) for m in cfg["models"]]
-            gen, plen = args.k3_gen, cfg["prompt"]
-            max_seq = plen + gen + 128
-            ws = [reuse.get((m, args.seed + i)) or synth.make_weights(s, seed=args.seed + i, device="cuda")
-                  for i, (m, s) in enumerate(zip(cfg["models"], shapes))]
-            stages = [Stage(s, w, max_seq=max_seq, max_window=8) for s, w in zip(shapes, ws)]
-            prompt = [int(x) for x in synth.make_prompt(shapes[-1].vocab, plen, seed=args.seed + 17)]
-            gam = [0, 3, args.gamma]
-            res = {"models": cfg["models"], "prompt": plen, "gen": gen, "gammas": gam,
-                   "alpha_per_link": args.alpha, "workload": cfg["name"]}
-            ar_out, ar_st = pipeline_run([stages[-1]], prompt, gen, mode=PS_MODE_AR)
-            res["ar_tokens_per_s"] = gen / (ar_st.wall_ns / 1e9)
-            # Table 1's grid (P:200-204): {sync, async} x {2-model (M_1 -> M_2), 3-model}
-            grid = {}
-            for mname, mode, sel in (("sync_sd_2model", PS_MODE_SYNC_SD, [1, 2]), ("pipespec_async_2model",
-                                                                                  PS_MODE_PIPESPEC, [1, 2])):
-                sub = [stages[i] for i in sel]
-                o, st = pipeline_run(sub, prompt, gen, mode=mode, gammas=[0, args.gamma], alphas=[args.alpha],
-                                     seed=args.seed + 4321)
-                assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
-                grid[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns}
-            res["table1_grid"] = grid
-            for mname, mode in (("sync_sd_tiered", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
-                for st_ in stages:
-                    st_.reset_timers()
-                o, st = pipeline_run(stages, prompt, gen, mode=mode, gammas=gam, alphas=[args.alpha] * 2,
-                                     seed=args.seed + 4321)
-                assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
-                inf = stages[-1].info()
-                pass_ms = inf["sum_fwd_ms"] / max(1, inf["n_fwd"])
-                R = gam[-1] + 1
-                ts = shapes[-1]
-                byts = ts.streamed_bytes_per_pass(R) + (plen + gen / 2 + R) * ts.kv_bytes_per_token()
-                res[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns,
-                              "verify_steps": [int(x) for x in st.verify_steps[:3]],
-                              "target_verify_pass_ms": pass_ms,
-                              "target_verify_frac": byts / (pass_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
-                grid[mname.replace("sync_sd_tiered", "sync_sd_3model").replace("pipespec_async", "pipespec_async_3model")] = \
-                    {"tokens_per_s": res[mname]["tokens_per_s"], "speedup_vs_ar": res[mname]["speedup_vs_ar"]}
-            for st_ in stages:
-                st_.close()
-            del stages, ws
-            torch.cuda.empty_cache()
+            res = _k3_one(cname, args, peaks, reuse)
             res["seconds"] = time.perf_counter() - t0
             out[cname] = res
         except Exception as e:  # noqa: BLE001
             out[cname] = {"error": repr(e)[:300]}
-            torch.cuda.empty_cache()
+        # every Stage of the config (it holds its weights) must be gone before
+        # the next config's 160 GB are allocated
+        gc.collect()
+        torch.cuda.empty_cache()
     return out
+
+
+def _k3_one(cname, args, peaks, reuse):
+    """One k=3 config (see k3_configs); its stages and weights are locals, so
+    they are released when it returns."""
+    import synth
+    from paper_2505_01572_b200 import Stage, pipeline_run
+    from paper_2505_01572_b200.abi import PS_MODE_AR, PS_MODE_PIPESPEC, PS_MODE_SYNC_SD
+    cfg = LAYOUT_CONFIGS[cname]
+    shapes = [synth.preset(m) for m in cfg["models"]]
+    gen, plen = args.k3_gen, cfg["prompt"]
+    max_seq = plen + gen + 128
+    ws = [reuse.get((m, args.seed + i)) or synth.make_weights(s, seed=args.seed + i, device="cuda")
+          for i, (m, s) in enumerate(zip(cfg["models"], shapes))]
+    stages = [Stage(s, w, max_seq=max_seq, max_window=8) for s, w in zip(shapes, ws)]
+    try:
+        prompt = [int(x) for x in synth.make_prompt(shapes[-1].vocab, plen, seed=args.seed + 17)]
+        gam = [0, 3, args.gamma]
+        res = {"models": cfg["models"], "prompt": plen, "gen": gen, "gammas": gam,
+               "alpha_per_link": args.alpha, "workload": cfg["name"]}
+        ar_out, ar_st = pipeline_run([stages[-1]], prompt, gen, mode=PS_MODE_AR)
+        res["ar_tokens_per_s"] = gen / (ar_st.wall_ns / 1e9)
+        # Table 1's grid (P:200-204): {sync, async} x {2-model (M_1 -> M_2), 3-model}
+        grid = {}
+        for mname, mode, sel in (("sync_sd_2model", PS_MODE_SYNC_SD, [1, 2]), ("pipespec_async_2model",
+                                                                              PS_MODE_PIPESPEC, [1, 2])):
+            sub = [stages[i] for i in sel]
+            o, st = pipeline_run(sub, prompt, gen, mode=mode, gammas=[0, args.gamma], alphas=[args.alpha],
+                                 seed=args.seed + 4321)
+            assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
+            grid[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns}
+        res["table1_grid"] = grid
+        for mname, mode in (("sync_sd_tiered", PS_MODE_SYNC_SD), ("pipespec_async", PS_MODE_PIPESPEC)):
+            for st_ in stages:
+                st_.reset_timers()
+            o, st = pipeline_run(stages, prompt, gen, mode=mode, gammas=gam, alphas=[args.alpha] * 2,
+                                 seed=args.seed + 4321)
+            assert o == ar_out, f"{cname} {mname}: output differs from M_K autoregressive decoding"
+            inf = stages[-1].info()
+            pass_ms = inf["sum_fwd_ms"] / max(1, inf["n_fwd"])
+            R = gam[-1] + 1
+            ts = shapes[-1]
+            byts = ts.streamed_bytes_per_pass(R) + (plen + gen / 2 + R) * ts.kv_bytes_per_token()
+            res[mname] = {"tokens_per_s": gen / (st.wall_ns / 1e9), "speedup_vs_ar": ar_st.wall_ns / st.wall_ns,
+                          "verify_steps": [int(x) for x in st.verify_steps[:3]],
+                          "target_verify_pass_ms": pass_ms,
+                          "target_verify_frac": byts / (pass_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0)}
+            grid[mname.replace("sync_sd_tiered", "sync_sd_3model").replace("pipespec_async", "pipespec_async_3model")] = \
+                {"tokens_per_s": res[mname]["tokens_per_s"], "speedup_vs_ar": res[mname]["speedup_vs_ar"]}
+        return res
+    finally:
+        for st_ in stages:
+            st_.close()
 
 
 # ----------------------------------------------------------------------------- ours

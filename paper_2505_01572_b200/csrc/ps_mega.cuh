@@ -129,6 +129,15 @@ __device__ __noinline__ void attn_produce(const MegaParams& P, int pa, const Att
   attn_producer_init(p, gm, it0, it_end, u);
   const int pos0 = p.step->pos0;
   const uint32_t ring_u32 = smem_u32(ring), full_u32 = smem_u32(full);
+  // The ring shares its shared memory with the stream-K staging of > 16-row
+  // epilogues (every GEMM phase but QKV).  A CTA without units in the phases
+  // just before this attention reaches it early, while its own epilogue warps
+  // may still be in the phase before QKV: wait until that phase is published
+  // grid-wide (then this CTA's epilogue is in QKV or later, which stages
+  // nothing until the attention is consumed).  A CTA with units everywhere
+  // gets here only after that point anyway.
+  if (it0 < it_end && pa >= 2)
+    spin_until(P.done + (pa - 2), P.ph[pa - 2].head ? tgt_head : tgt_body, kSpinCapNs);
   bool qkv_seen = false;
   while (u.more) {
     if (!qkv_seen && u.kbeg + (u.s + 1) * kAttnStep > pos0) {
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
               epi_segment<RP, true>(gp, t, seg_begin, seg_end, U, Gp, c, kbt, v, e, lane, quarter, R, pos0, scratch,
                                     red, rstd, kvrow, flag,
                                     gp.mode == EPI_QKV ? nullptr : reinterpret_cast<float4*>(attn_smem),
-                                    L::kAttnBytes / 16);
+                                    kAttnStages * attn_stage_bytes<128>() / 16);   // not the ring barriers
             } else {
               // 64-row bucket: the epilogue in 16-row chunks (hi columns [16q, 16q + 16),
               // lo columns RP + 16q ..); the accumulator is released after the last chunk
