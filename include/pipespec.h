@@ -159,8 +159,23 @@ ps_status ps_tp_connect_local(ps_stage* const* stages, int32_t n);
  * Keeps the KV of the longest common prefix with the current O_i, then runs
  * the forward over the remaining positions so KV covers 0..n-2 and tokens[n-1]
  * is pending.  Serves as prefill, as catch-up after a resync, and as the
- * extend half of "rollback O_i to match O_j". */
+ * extend half of "rollback O_i to match O_j".
+ * Path (ps_set_prefill_path): runs of >= 64 positions go in chunks of up to
+ * 512 tokens through the prefill kernels (tcgen05 GEMMs with the tokens as
+ * the M = 128 side, causal prefill attention; "the prefill phase
+ * processes the initial input prompt") on single-GPU
+ * stages; shorter runs, and tensor-parallel stages, use the decode
+ * megakernel's 64-row bucket. */
 ps_status ps_prefill(ps_stage* stage, const int32_t* tokens, int32_t n);
+
+/* Prefill path of ps_prefill.  PS_PREFILL_AUTO (default): as described
+ * there.  PS_PREFILL_ROWS: always the megakernel's 64-row bucket, whose KV is
+ * bit-identical to KV written by decode forwards (row-bucket invariance); the
+ * GEMM path's KV agrees with it within fp32 rounding (another summation order).
+ * PS_E_INVALID for any other value. */
+#define PS_PREFILL_AUTO 0
+#define PS_PREFILL_ROWS 1
+ps_status ps_set_prefill_path(ps_stage* stage, int32_t path);
 
 /* Lazy form of ps_prefill for the rollback cascade ("Rollback O_i to match
  * O_j's last token"; reading R2): O_i := tokens[0:n] (host), keeping the

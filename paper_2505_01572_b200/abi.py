@@ -20,6 +20,7 @@ STATUS_NAMES = {0: "PS_OK", -1: "PS_E_INVALID", -2: "PS_E_CONTRACT", -3: "PS_E_C
                 -5: "PS_E_NCCL", -6: "PS_E_STALE"}
 PS_WQ, PS_WK, PS_WV, PS_WO, PS_WG, PS_WU, PS_WD, PS_N_ATTN, PS_N_MLP, PS_LAYER_SLOTS = range(10)
 PS_MODE_AR, PS_MODE_SYNC_SD, PS_MODE_PIPESPEC = 0, 1, 2
+PS_PREFILL_AUTO, PS_PREFILL_ROWS = 0, 1
 PS_EV_DRAFT, PS_EV_VERIFY, PS_EV_AR, PS_EV_RESYNC, PS_EV_STALE = 0, 1, 2, 3, 4
 PS_TP_HANDLE_BYTES = 256
 
@@ -103,6 +104,7 @@ _PROTOS = {
                                     C.POINTER(StageOpts), C.POINTER(C.c_void_p)]),
     "ps_stage_destroy": (C.c_int32, [C.c_void_p]),
     "ps_prefill": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "ps_set_prefill_path": (C.c_int32, [C.c_void_p, C.c_int32]),
     "ps_draft": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
     "ps_verify": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, _I32P, _I32P, C.c_void_p]),
     "ps_verify_async": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(VerifyTicket)]),

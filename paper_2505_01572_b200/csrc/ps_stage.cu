@@ -18,6 +18,7 @@
 
 #include "../../include/pipespec.h"
 #include "ps_host.cuh"
+#include "ps_prefill.cuh"
 
 // ============================================================================ errors
 static thread_local std::string g_err;
@@ -120,6 +121,17 @@ struct ps_stage {
   long long kv_len = 0;
   int onpath = 0;                    // generated tokens matching the synthetic target S
   std::vector<int32_t> S_host;
+  // NEXT-3 prefill kernels (ps_prefill.cuh; single-GPU stages): chunk buffers
+  // of kPfRows tokens and the per-layer GEMM parameter templates
+  int prefill_path = PS_PREFILL_AUTO;
+  bool pf_ready = false;
+  float *pf_x = nullptr, *pf_q = nullptr;
+  __nv_bfloat16 *pf_xs = nullptr, *pf_att = nullptr, *pf_h = nullptr;
+  int32_t* pf_tok = nullptr;            // device tokens of the chunk
+  int32_t* h_pf_tok = nullptr;          // pinned staging
+  cudaEvent_t pf_tok_ev = nullptr;      // the staging buffer's previous copy ran
+  std::vector<PfGemmParams> pf_gemm;    // [L][4]: QKV, O, gate/up, down
+  double sum_prefill_ms = 0;
 };
 
 // rows buckets: 16 and 32 (forwards with the lm_head: verify / draft), 64 (prefill chunks)
@@ -134,6 +146,13 @@ static ps_status init_stage_device(int device) {
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<64>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_smem_bytes<PF_QKV>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<PF_RESID>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<PF_SWIGLU>()));
+  CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<64>()));
+  CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<128>()));
   return PS_OK;
 }
 static int bucket_of(int R) { return R <= 16 ? 0 : R <= 32 ? 1 : 2; }
@@ -526,6 +545,11 @@ ps_status ps_stage_destroy(ps_stage* S) {
                  S->amax, S->counters, S->attn_counters, S->attn_o, S->attn_ml, S->rope_cs, S->d_syn, S->d_S};
   for (void* p : dev)
     if (p) cudaFree(p);
+  void* pf[] = {S->pf_x, S->pf_q, S->pf_xs, S->pf_att, S->pf_h, S->pf_tok};
+  for (void* p : pf)
+    if (p) cudaFree(p);
+  if (S->h_pf_tok) cudaFreeHost(S->h_pf_tok);
+  if (S->pf_tok_ev) cudaEventDestroy(S->pf_tok_ev);
   if (S->h_page_table) cudaFreeHost(S->h_page_table);
   if (S->h_in) cudaFreeHost(S->h_in);
   for (auto& ev : S->in_ev)
@@ -875,6 +899,55 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S->h_syn = SynthParams{};
   S_TRY(cudaMemcpy(S->d_syn, &S->h_syn, sizeof(SynthParams), cudaMemcpyHostToDevice));
   S_TRY(cudaStreamSynchronize(S->stream));
+  // --- NEXT-3 prefill kernels (single-GPU stages with layers)
+  if (tp == 1 && sh.n_layers > 0) {
+    const size_t R = kPfRows;
+    S_TRY(cudaMalloc(&S->pf_x, R * d * 4));
+    S_TRY(cudaMalloc(&S->pf_q, R * hq * 4));
+    S_TRY(cudaMalloc(&S->pf_xs, 2 * R * d * 2));
+    S_TRY(cudaMalloc(&S->pf_att, 2 * R * hq * 2));
+    S_TRY(cudaMalloc(&S->pf_h, 2 * R * f * 2));
+    S_TRY(cudaMalloc(&S->pf_tok, R * 4));
+    S_TRY(cudaMemset(S->pf_xs, 0, 2 * R * d * 2));
+    S_TRY(cudaMemset(S->pf_att, 0, 2 * R * hq * 2));
+    S_TRY(cudaMemset(S->pf_h, 0, 2 * R * f * 2));
+    S_TRY(cudaHostAlloc(&S->h_pf_tok, R * 4, cudaHostAllocDefault));
+    S_TRY(cudaEventCreateWithFlags(&S->pf_tok_ev, cudaEventDisableTiming));
+    CUtensorMap mxs, matt, mh;
+    P_TRY(make_map(&mxs, S->pf_xs, 2 * R, d, 128));
+    P_TRY(make_map(&matt, S->pf_att, 2 * R, hq, 128));
+    P_TRY(make_map(&mh, S->pf_h, 2 * R, f, 128));
+    int shift = 0;
+    while ((1 << shift) < S->page_size) ++shift;
+    S->pf_gemm.resize((size_t)sh.n_layers * 4);
+    for (int l = 0; l < sh.n_layers; ++l) {
+      const __nv_bfloat16* const* W = &S->lw[(size_t)l * 9];
+      const LayerMaps& M = S->maps[l];
+      PfGemmParams* g = &S->pf_gemm[(size_t)l * 4];
+      for (int k = 0; k < 4; ++k) memset(&g[k], 0, sizeof(PfGemmParams));
+      // QKV: q tiles, then k, then v (each matrix's rows padded to 128)
+      g[0].mX = mxs; g[0].mW0 = M.q; g[0].mW1 = M.k; g[0].mW2 = M.v;
+      g[0].K = d;
+      g[0].t1 = (hq + 127) / 128;
+      g[0].t2 = g[0].t1 + (hkv + 127) / 128;
+      g[0].N = g[0].t2 + (hkv + 127) / 128;          // (QKV: n_tiles)
+      g[0].nq = hq; g[0].nk = hkv;
+      g[0].q = S->pf_q; g[0].ld_q = hq;
+      g[0].kv = S->kv; g[0].page_table = S->d_page_table; g[0].page_size = S->page_size; g[0].page_shift = shift;
+      g[0].layer = l; g[0].hkv = sh.n_kv_heads; g[0].hd = sh.head_dim; g[0].page_stride = S->page_elems;
+      g[0].rope_cs = S->rope_cs;
+      // O (+ residual): x += att Wo^T
+      g[1].mX = matt; g[1].mW0 = M.o; g[1].K = hq; g[1].N = d; g[1].x = S->pf_x; g[1].ld_x = d;
+      // gate/up (+ SiLU * mul): 128-row boxes of Wg and Wu
+      g[2].mX = mxs; g[2].K = d; g[2].N = f; g[2].h = S->pf_h; g[2].ld_h = f;
+      P_TRY(make_map(&g[2].mW0, W[PS_WG], f, d, 128));
+      P_TRY(make_map(&g[2].mW1, W[PS_WU], f, d, 128));
+      // down (+ residual)
+      g[3].mX = mh; g[3].mW0 = M.d; g[3].K = f; g[3].N = d; g[3].x = S->pf_x; g[3].ld_x = d;
+    }
+    S->pf_ready = (d % 64 == 0) && (hq % 64 == 0) && (f % 64 == 0) && (sh.head_dim == 64 || sh.head_dim == 128) &&
+                  64 % (sh.n_heads / sh.n_kv_heads) == 0;
+  }
   // phase tables now (tensor-parallel groups build theirs at connect time)
   if (tp == 1) P_TRY(build_all_tables(S));
   *out = S;
@@ -936,6 +1009,72 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   return PS_OK;
 }
 
+// NEXT-3: positions [pos0, pos0 + T) (T <= kPfRows) through the prefill
+// kernels (ps_prefill.cuh): per layer norm, QKV GEMM (+ RoPE, KV append),
+// causal attention, O GEMM (+ residual), norm, gate/up GEMM (+ SwiGLU), down
+// GEMM (+ residual).  No lm_head (prefill predicts nothing: the last prompt
+// token stays pending).
+static ps_status prefill_chunk(ps_stage* S, const int32_t* toks, int T, long long pos0) {
+  ps_status st;
+  if ((st = ensure_pages(S, pos0 + T - 1)) != PS_OK) return st;
+  const ps_model_shape& sh = S->sh;
+  const int d = sh.d_model, hq = sh.n_heads * sh.head_dim;
+  const int mt = (T + 127) / 128;
+  CU_TRY(cudaEventSynchronize(S->pf_tok_ev));              // the staging buffer's previous copy ran
+  memcpy(S->h_pf_tok, toks, (size_t)T * 4);
+  CU_TRY(cudaMemcpyAsync(S->pf_tok, S->h_pf_tok, (size_t)T * 4, cudaMemcpyHostToDevice, S->stream));
+  CU_TRY(cudaEventRecord(S->pf_tok_ev, S->stream));
+  int shift = 0;
+  while ((1 << shift) < S->page_size) ++shift;
+  PfAttnParams ap{};
+  ap.q = S->pf_q; ap.ld_q = hq;
+  ap.kv = S->kv; ap.page_table = S->d_page_table; ap.page_size = S->page_size; ap.page_shift = shift;
+  ap.hkv = sh.n_kv_heads; ap.H = sh.n_heads; ap.page_stride = S->page_elems;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)sh.head_dim));
+  ap.T = T; ap.pos0 = (int)pos0; ap.out = S->pf_att; ap.ld_out = hq;
+  const int QB = 64 / (sh.n_heads / sh.n_kv_heads);
+  const dim3 agrid((T + QB - 1) / QB, sh.n_kv_heads);
+  auto gemm = [&](int mode, PfGemmParams& g, int n_tiles) -> ps_status {
+    g.T = T;
+    g.pos0 = (int)pos0;
+    const dim3 grid(mt, n_tiles);
+    if (mode == PF_QKV) pf_gemm_kernel<PF_QKV><<<grid, kPfThreads, pf_smem_bytes<PF_QKV>(), S->stream>>>(g);
+    else if (mode == PF_RESID) pf_gemm_kernel<PF_RESID><<<grid, kPfThreads, pf_smem_bytes<PF_RESID>(), S->stream>>>(g);
+    else pf_gemm_kernel<PF_SWIGLU><<<grid, kPfThreads, pf_smem_bytes<PF_SWIGLU>(), S->stream>>>(g);
+    g_launches++;
+    CU_TRY(cudaGetLastError());
+    return PS_OK;
+  };
+  for (int l = 0; l < sh.n_layers; ++l) {
+    const __nv_bfloat16* const* W = &S->lw[(size_t)l * 9];
+    PfGemmParams* g = &S->pf_gemm[(size_t)l * 4];
+    // h = RMSNorm(x) (layer 0: x = E[tok] first)
+    pf_norm_kernel<<<T, kPfNormThreads, 0, S->stream>>>(l == 0 ? S->pf_tok : nullptr, S->embed, S->vocab_full, S->pf_x,
+                                                         d, W[PS_N_ATTN], sh.rms_eps, S->pf_xs);
+    g_launches++;
+    if ((st = gemm(PF_QKV, g[0], g[0].N)) != PS_OK) return st;
+    ap.layer = l;
+    if (sh.head_dim == 128) pf_attn_kernel<128><<<agrid, 128, pf_attn_smem_bytes<128>(), S->stream>>>(ap);
+    else pf_attn_kernel<64><<<agrid, 128, pf_attn_smem_bytes<64>(), S->stream>>>(ap);
+    g_launches++;
+    if ((st = gemm(PF_RESID, g[1], (d + 127) / 128)) != PS_OK) return st;
+    pf_norm_kernel<<<T, kPfNormThreads, 0, S->stream>>>(nullptr, S->embed, S->vocab_full, S->pf_x, d, W[PS_N_MLP],
+                                                         sh.rms_eps, S->pf_xs);
+    g_launches++;
+    if ((st = gemm(PF_SWIGLU, g[2], (sh.d_ffn + 127) / 128)) != PS_OK) return st;
+    if ((st = gemm(PF_RESID, g[3], (d + 127) / 128)) != PS_OK) return st;
+  }
+  CU_TRY(cudaGetLastError());
+  return PS_OK;
+}
+
+ps_status ps_set_prefill_path(ps_stage* S, int32_t path) {
+  if (!S) return fail(PS_E_INVALID, "NULL argument");
+  if (path != PS_PREFILL_AUTO && path != PS_PREFILL_ROWS) return fail(PS_E_INVALID, "unknown prefill path %d", path);
+  S->prefill_path = path;
+  return PS_OK;
+}
+
 ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   if (!S || !tokens) return fail(PS_E_INVALID, "NULL argument");
   PS_NOT_INFLIGHT(S);
@@ -952,11 +1091,22 @@ ps_status ps_prefill(ps_stage* S, const int32_t* tokens, int32_t n) {
   S->kv_len = keep_kv;
   free_pages_from(S, S->kv_len);
   update_onpath(S);
-  // forward positions [kv_len, n-1) in chunks of up to kRowsCap rows (no lm_head;
-  // the 64-row bucket: half the weight passes of 32-row chunks)
+  // forward positions [kv_len, n-1): runs of >= 64 positions in chunks of up to
+  // kPfRows tokens through the prefill kernels; the rest (and every position
+  // with PS_PREFILL_ROWS) in chunks of up to kRowsCap rows through the decode
+  // megakernel's 64-row bucket (no lm_head)
+  const bool gemm_path = S->pf_ready && S->prefill_path == PS_PREFILL_AUTO;
   while (S->kv_len < n - 1) {
-    const int R = (int)std::min<long long>(kRowsCap, n - 1 - S->kv_len);
-    ps_status st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
+    const long long left = n - 1 - S->kv_len;
+    ps_status st;
+    int R;
+    if (gemm_path && left >= kRowsCap) {
+      R = (int)std::min<long long>(kPfRows, left);
+      st = prefill_chunk(S, &S->tokens[S->kv_len], R, S->kv_len);
+    } else {
+      R = (int)std::min<long long>(kRowsCap, left);
+      st = forward_rows(S, &S->tokens[S->kv_len], R, S->kv_len, 0, false, false);
+    }
     if (st != PS_OK) {
       S->kv_len = 0;   // KV state unknown: force a full recompute next time
       free_pages_from(S, 0);

@@ -115,6 +115,11 @@ class Stage:
         t = _i32(tokens)
         abi.check(abi.lib().ps_prefill(self._h, t.ctypes.data, len(t)))
 
+    def set_prefill_path(self, path: int):
+        """abi.PS_PREFILL_AUTO (prefill kernels for runs of >= 64 tokens) or
+        abi.PS_PREFILL_ROWS (the megakernel's 64-row bucket only)."""
+        abi.check(abi.lib().ps_set_prefill_path(self._h, int(path)))
+
     def resync(self, tokens):
         """Lazy rollback-and-extend to `tokens` (KV catch-up folded into the next forward)."""
         t = _i32(tokens)

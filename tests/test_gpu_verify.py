@@ -293,7 +293,9 @@ def test_prefill_64_row_chunks(name, layers, n):
     chunks + a ragged tail, split-bf16 N = 128 MMAs, 16-row epilogue chunks).
     Its KV is bit-identical to a one-token-at-a-time prefill (row-bucket
     invariance), and the next verify matches the oracle."""
+    from paper_2505_01572_b200 import abi
     s, w, st = make(name, 31, layers=layers, max_seq=n + 40)
+    st.set_prefill_path(abi.PS_PREFILL_ROWS)   # the decode megakernel's bucket (not the prefill kernels)
     w64 = synth.weights_to_numpy(w)
     prompt = list(synth.make_prompt(s.vocab, n, seed=32))
     st.prefill(prompt)                       # 64 + 64 + 21 (+ ragged) rows
@@ -306,6 +308,46 @@ def test_prefill_64_row_chunks(name, layers, n):
     ref = L.verify(w64, s, prompt, [])
     check_logits(l1, ref["logits"])
     check_verify((a1, n1), ref, 0)
+    st.close()
+
+
+@pytest.mark.parametrize("name,layers,n", [("toy-verifier", None, 150), ("llama-68m", None, 1030),
+                                            ("llama3.2-1b", 2, 700), ("llama3.1-8b", 2, 512)])
+def test_prefill_gemm_path(name, layers, n):
+    """NEXT-3: runs of >= 64 prompt positions go through the prefill
+    kernels -- tcgen05 GEMMs with the tokens as the M = 128 side (split-bf16
+    operand, fused RoPE/KV-append, residual and SwiGLU epilogues) and the
+    causal prefill attention -- in chunks of <= 512 tokens (1030: 512 + 512 +
+    5 through the megakernel; 150, 700: ragged M tiles).  The next verify
+    matches the oracle, and its logits agree with those after a prefill
+    through the megakernel's 64-row bucket (PS_PREFILL_ROWS) within the
+    parity tolerance (the two paths sum in different orders)."""
+    from paper_2505_01572_b200 import Stage, abi
+    s, w, st = make(name, 41, layers=layers, max_seq=n + 40)
+    w64 = synth.weights_to_numpy(w)
+    prompt = list(synth.make_prompt(s.vocab, n, seed=42))
+    ar, _ = L.ar_decode(w64, s, prompt, 2)
+    window = ar[:2] + [(ar[1] + 7) % s.vocab]
+    st.prefill(prompt)
+    a1, n1, l1 = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(l1, ref["logits"])
+    check_verify((a1, n1), ref, len(window))
+    assert st.info()["kv_len"] == n + a1
+    st.close()
+    st2 = Stage(s, w, max_seq=n + 40)
+    st2.set_prefill_path(abi.PS_PREFILL_ROWS)
+    st2.prefill(prompt)
+    a2, n2, l2 = st2.verify(window, want_logits=True)
+    check_logits(l1, np.asarray(l2, dtype=np.float64))
+    st2.close()
+
+
+def test_prefill_path_rejects_unknown():
+    from paper_2505_01572_b200 import abi
+    s, w, st = make("toy-verifier", 5, max_seq=128)
+    with pytest.raises(abi.PipeSpecError):
+        st.set_prefill_path(7)
     st.close()
 
 
