@@ -13,7 +13,7 @@ greedy stream, which the bench checks on every run.
 
 value    tokens/s of the whole job (device time, CUDA events, max over ranks)
 e2e      the same through the C ABI with host buffers, wall clock
-roofline the dominant kernel (gate/up GEMM of M_1) timed live with CUDA events
+roofline the dominant kernel (M_1's verify megakernel) timed live with CUDA events
 cpu_baseline / --impl reference: the fp64 oracle on the host cores (bounded
          sample, extrapolated in depth)
 
@@ -504,6 +504,27 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def prefill_timing(st, shape, prompt):
+    """ps_prefill of `prompt` on a stage holding none of it, timed with CUDA
+    events on the stage stream.  FLOPs: 2 x linear-layer params x positions +
+    causal attention 4 x L x q_dim x n^2 / 2 (the split-bf16 operand's second
+    MMA is not counted)."""
+    import torch
+    st.prefill([(prompt[0] + 1) % shape.vocab])          # no common prefix: the whole prompt is forwarded
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(st.stream)
+    st.prefill(prompt)
+    p1.record(st.stream)
+    p1.synchronize()
+    ms = p0.elapsed_time(p1)
+    n = len(prompt) - 1                                    # positions forwarded (the last token is pending)
+    lin = shape.n_params() - shape.vocab * shape.d_model * (1 if shape.tied else 2)
+    flops = 2.0 * lin * n + 4.0 * shape.n_layers * shape.q_dim * n * n / 2
+    return {"ms": ms, "tokens": n, "chunks": -(-n // 512), "TFLOP/s": flops / (ms * 1e-3) / 1e12,
+            "tokens_per_s": n / (ms * 1e-3)}
+
+
 def k3_configs(args, peaks, reuse):
     """N = 1, all stages co-resident: BASELINE configs[2] (68M -> 7B -> 13B,
     1K prompt) and configs[3] (1B -> 8B -> 70B, 2K prompt; 159.6 GB of bf16
@@ -549,6 +570,9 @@ def _k3_one(cname, args, peaks, reuse):
         gam = [0, 3, args.gamma]
         res = {"models": cfg["models"], "prompt": plen, "gen": gen, "gammas": gam,
                "alpha_per_link": args.alpha, "workload": cfg["name"]}
+        # NEXT-3: each stage's prompt prefill (the prefill kernels), device time on
+        # its stream; pipeline_run's own ps_prefill then keeps this KV (same prompt)
+        res["prefill"] = {m: prefill_timing(st_, sh, prompt) for m, st_, sh in zip(cfg["models"], stages, shapes)}
         ar_out, ar_st = pipeline_run([stages[-1]], prompt, gen, mode=PS_MODE_AR)
         res["ar_tokens_per_s"] = gen / (ar_st.wall_ns / 1e9)
         # Table 1's grid: {sync, async} x {2-model (M_1 -> M_2), 3-model}
@@ -619,19 +643,13 @@ def main():
 
     # --- prefill (NEXT-3): the prompt through the 64-row bucket, timed on
     # the stage stream (device time); reported beside, not in, decode tokens/s
-    def timed_prefill(st, shape):
-        torch.cuda.synchronize()
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(st.stream)
-        st.prefill(prompt)
-        p1.record(st.stream)
-        p1.synchronize()
-        ms = p0.elapsed_time(p1)
-        n = len(prompt) - 1                       # positions forwarded (the last token is pending)
-        flops = 2.0 * shape.n_params() * n + 4.0 * shape.n_layers * shape.q_dim * n * n / 2
-        return {"ms": ms, "tokens": n, "forwards": -(-n // 64), "TFLOP/s": flops / (ms * 1e-3) / 1e12,
-                "tokens_per_s": n / (ms * 1e-3)}
-    prefill = {"target": timed_prefill(target, ts), "drafter": timed_prefill(drafter, ds)}
+    # (the prefill kernels: 512-token chunks through tcgen05 GEMMs, P:36 / NEXT-3)
+    # (beside: the target's prompt through the decode megakernel's 64-row bucket, timed first)
+    target.set_prefill_path(abi.PS_PREFILL_ROWS)
+    rows_path = prefill_timing(target, ts, prompt)
+    target.set_prefill_path(abi.PS_PREFILL_AUTO)
+    prefill = {"target": prefill_timing(target, ts, prompt), "drafter": prefill_timing(drafter, ds, prompt),
+               "target_64row_megakernel": rows_path}
 
     # --- M_K autoregressive: the lossless reference stream S and the AR baseline
     target.prefill(prompt)
