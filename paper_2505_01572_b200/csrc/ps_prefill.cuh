@@ -9,13 +9,16 @@
 // one per step of the layer:
 //
 //   pf_norm_kernel     (embed +) RMSNorm: xs = split(x * rstd * g)
-//   pf_gemm_kernel     tcgen05 GEMM, TOKENS as the M = 128 side, 128 weight
-//                      rows as N, K in 64-wide TMA blocks; the split-bf16
-//                      operand (DESIGN R28) as two MMAs into ONE accumulator
-//                      (W x_hi + W x_lo); fused epilogues:
+//   pf_gemm_kernel     persistent tcgen05 GEMM, TOKENS as the M = 128 side,
+//                      128 or 256 weight rows as N, K in 64-wide TMA blocks;
+//                      the split-bf16 operand (DESIGN R28) as two MMAs into
+//                      ONE accumulator (x_hi W^T + x_lo W^T); two TMEM
+//                      accumulators, so a tile's epilogue overlaps the next
+//                      tile's mainloop; fused epilogues:
 //                        PF_QKV    RoPE + paged split-bf16 KV append + fp32 q
 //                        PF_RESID  residual add into x (O and down)
-//                        PF_SWIGLU SiLU(gate) * up (gate and up: two accumulators)
+//                        PF_SWIGLU SiLU(gate) * up (gate and up rows stacked in
+//                                  one N operand: one accumulator holds both)
 //   pf_attn_kernel     causal GQA attention of the chunk's queries over the
 //                      paged KV (prompt prefix + this chunk), mma.sync with
 //                      split operands, online softmax in the exp2 domain
@@ -37,19 +40,23 @@ constexpr int kPfTile = 128 * 64 * 2;            // one 128-row x 64-col bf16 TM
 
 enum { PF_QKV = 0, PF_RESID = 1, PF_SWIGLU = 2 };
 
-template <int MODE> __host__ __device__ constexpr int pf_stages() { return MODE == PF_SWIGLU ? 3 : 4; }
-// per stage: x_hi, x_lo (128 tokens x 64) and one (two for SwiGLU) 128-row weight boxes
-template <int MODE> __host__ __device__ constexpr int pf_stage_bytes() { return (MODE == PF_SWIGLU ? 4 : 3) * kPfTile; }
-template <int MODE> __host__ __device__ constexpr int pf_smem_bytes() {
-  return pf_stages<MODE>() * pf_stage_bytes<MODE>() + 1024 + 256;
+// Tile = 128 tokens x BN output features (BN = 128 or 256; SwiGLU: BN / 2 gate
+// rows + BN / 2 up rows of the same features, stacked into one N = BN operand).
+// Per stage: x_hi, x_lo (128 tokens x 64) and the BN-row weight block.
+template <int BN> __host__ __device__ constexpr int pf_stages() { return BN == 256 ? 3 : 4; }
+template <int BN> __host__ __device__ constexpr int pf_stage_bytes() { return 2 * kPfTile + BN * 128; }
+template <int BN> __host__ __device__ constexpr int pf_smem_bytes() {
+  return pf_stages<BN>() * pf_stage_bytes<BN>() + 1024 + 256;
 }
 
 struct PfGemmParams {
   CUtensorMap mX;                  // split-bf16 operand [2 kPfRows][K] (hi rows, then lo rows), box {64, 128}
   CUtensorMap mW0, mW1, mW2;       // weights [out][K], box {64, 128}: QKV q/k/v; SwiGLU gate/up; else mW0
+  CUtensorMap mG64, mU64;          // SwiGLU with 128-wide tiles: gate / up, box {64, 64}
   int K;                           // reduction length (multiple of 64)
   int N;                           // output features (QKV: all three; SwiGLU: d_ffn)
-  int t1, t2;                      // QKV: tiles [0, t1) q, [t1, t2) k, [t2, ..) v
+  int n_tiles, m_tiles;            // output tiles: BN-feature blocks x 128-token blocks
+  int t1, t2;                      // QKV: BN-feature tiles [0, t1) q, [t1, t2) k, [t2, ..) v
   int nq, nk;                      // QKV: rows of Wq, of Wk (= Wv)
   int T;                           // valid tokens of the chunk
   int pos0;                        // absolute position of token 0
@@ -78,172 +85,206 @@ PS_DEV void store_split8(__nv_bfloat16* hi, __nv_bfloat16* lo, const float* v) {
   *reinterpret_cast<uint4*>(lo) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
 }
 
-// One 128-token x 128-feature output tile per CTA (grid: M tiles fastest, so
-// the M tiles sharing a weight tile run together and re-read it from L2).
-template <int MODE>
+// Persistent: CTA b of G takes tiles b, b + G, ... (tile i = (token block
+// i % m_tiles, feature block i / m_tiles): the token blocks sharing a weight
+// block run side by side and re-read it from L2).  Warp 0 streams every
+// tile's k-blocks through one ring; warp 1 issues the MMAs into two TMEM
+// accumulators alternately, so the epilogue of tile j (warps 2-5) overlaps the
+// mainloop of tile j + 1.
+template <int MODE, int BN>
 __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfGemmParams p) {
-  constexpr bool GU = MODE == PF_SWIGLU;
-  constexpr int kStages = pf_stages<MODE>();
-  constexpr int kSB = pf_stage_bytes<MODE>();
+  static_assert(BN == 128 || BN == 256, "tile width");
+  constexpr int kStages = pf_stages<BN>();
+  constexpr int kSB = pf_stage_bytes<BN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kSB);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128, nt = blockIdx.y;
   const int nkb = p.K / 64;
+  const int n_all = p.n_tiles * p.m_tiles;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tslot);
+  if (warp == 1) tmem_alloc<2 * BN>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  // which weight matrix / local tile this output tile reads
-  int kind = 0, lt = nt;
-  if (MODE == PF_QKV) {
-    if (nt >= p.t2) { kind = 2; lt = nt - p.t2; }
-    else if (nt >= p.t1) { kind = 1; lt = nt - p.t1; }
-  }
+  // which weight matrix / local block a feature tile reads
+  auto tile_kind = [&](int nt, int& kind, int& lt) {
+    kind = 0;
+    lt = nt;
+    if (MODE == PF_QKV) {
+      if (nt >= p.t2) { kind = 2; lt = nt - p.t2; }
+      else if (nt >= p.t1) { kind = 1; lt = nt - p.t1; }
+    }
+  };
   if (warp == 0) {
     if (lane == 0) {
-      const CUtensorMap* w0 = kind == 0 ? &p.mW0 : kind == 1 ? &p.mW1 : &p.mW2;
       tma_prefetch_desc(&p.mX);
-      tma_prefetch_desc(w0);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
-        uint8_t* st = smem + s * kSB;
-        mbar_arrive_expect_tx(&full[s], kSB);
-        tma_load_2d(st, &p.mX, &full[s], kb * 64, m0, kEvictLast);
-        tma_load_2d(st + kPfTile, &p.mX, &full[s], kb * 64, kPfRows + m0, kEvictLast);
-        tma_load_2d(st + 2 * kPfTile, w0, &full[s], kb * 64, lt * 128, kEvictNormal);
-        if (GU) tma_load_2d(st + 3 * kPfTile, &p.mW1, &full[s], kb * 64, lt * 128, kEvictNormal);
+      uint32_t it = 0;
+      for (int i = blockIdx.x; i < n_all; i += gridDim.x) {
+        const int m0 = (i % p.m_tiles) * 128, nt = i / p.m_tiles;
+        int kind, lt;
+        tile_kind(nt, kind, lt);
+        const CUtensorMap* w0 = kind == 0 ? &p.mW0 : kind == 1 ? &p.mW1 : &p.mW2;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          uint8_t* st = smem + s * kSB;
+          mbar_arrive_expect_tx(&full[s], kSB);
+          tma_load_2d(st, &p.mX, &full[s], kb * 64, m0, kEvictLast);
+          tma_load_2d(st + kPfTile, &p.mX, &full[s], kb * 64, kPfRows + m0, kEvictLast);
+          if (MODE == PF_SWIGLU && BN == 256) {         // 128 gate rows, then 128 up rows
+            tma_load_2d(st + 2 * kPfTile, &p.mW0, &full[s], kb * 64, lt * 128, kEvictNormal);
+            tma_load_2d(st + 3 * kPfTile, &p.mW1, &full[s], kb * 64, lt * 128, kEvictNormal);
+          } else if (MODE == PF_SWIGLU) {               // 64 gate rows, then 64 up rows
+            tma_load_2d(st + 2 * kPfTile, &p.mG64, &full[s], kb * 64, lt * 64, kEvictNormal);
+            tma_load_2d(st + 2 * kPfTile + kPfTile / 2, &p.mU64, &full[s], kb * 64, lt * 64, kEvictNormal);
+          } else {
+#pragma unroll
+            for (int h = 0; h < BN / 128; ++h)
+              tma_load_2d(st + (2 + h) * kPfTile, w0, &full[s], kb * 64, lt * BN + h * 128, kEvictNormal);
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t kI = idesc_bf16_f32<128, 128>();
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      constexpr uint32_t kI = idesc_bf16_f32<128, BN>();
+      uint32_t it = 0, j = 0;
+      for (int i = blockIdx.x; i < n_all; i += gridDim.x, ++j) {
+        const int a = j & 1;
+        mbar_wait(&tempty[a], ((j >> 1) & 1) ^ 1);      // the epilogue has drained this accumulator
         tc_fence_after();
-        const uint32_t xh = smem_u32(smem + s * kSB), xl = xh + kPfTile, w0 = xh + 2 * kPfTile, w1 = xh + 3 * kPfTile;
+        const uint32_t d = tmem + a * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t xh = smem_u32(smem + s * kSB), xl = xh + kPfTile, w = xh + 2 * kPfTile;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-          // D[token][feature] += x_hi W^T, then += x_lo W^T (fixed order)
-          mma_bf16(tmem, smem_desc_sw128(xh + 32 * k), smem_desc_sw128(w0 + 32 * k), kI, acc);
-          mma_bf16(tmem, smem_desc_sw128(xl + 32 * k), smem_desc_sw128(w0 + 32 * k), kI, 1u);
-          if (GU) {
-            mma_bf16(tmem + 128, smem_desc_sw128(xh + 32 * k), smem_desc_sw128(w1 + 32 * k), kI, acc);
-            mma_bf16(tmem + 128, smem_desc_sw128(xl + 32 * k), smem_desc_sw128(w1 + 32 * k), kI, 1u);
+          for (int k = 0; k < 4; ++k) {
+            // D[token][feature] += x_hi W^T, then += x_lo W^T (fixed order)
+            mma_bf16(d, smem_desc_sw128(xh + 32 * k), smem_desc_sw128(w + 32 * k), kI, (kb > 0 || k > 0) ? 1u : 0u);
+            mma_bf16(d, smem_desc_sw128(xl + 32 * k), smem_desc_sw128(w + 32 * k), kI, 1u);
           }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[a]);
       }
-      mma_commit(tfull);
     }
   } else {
     // ---- epilogue: warp w reads TMEM lanes [32 (w % 4), +32) = tokens m0 + that range
     const int quarter = warp & 3;
-    const int tok = m0 + quarter * 32 + lane;
-    const bool ok = tok < p.T;
-    const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16);
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    if (MODE == PF_RESID) {
+    uint32_t j = 0;
+    for (int i = blockIdx.x; i < n_all; i += gridDim.x, ++j) {
+      const int a = j & 1;
+      const int m0 = (i % p.m_tiles) * 128, nt = i / p.m_tiles;
+      int kind, lt;
+      tile_kind(nt, kind, lt);
+      const int tok = m0 + quarter * 32 + lane;
+      const bool ok = tok < p.T;
+      const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + a * BN;
+      mbar_wait(&tfull[a], (j >> 1) & 1);
+      tc_fence_after();
+      if (MODE == PF_RESID) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        float v[32];
-        tmem_ld32(tq + c0, v);
-        const int f0 = nt * 128 + c0;
-        if (ok && f0 < p.N) {
-          float4* xr = reinterpret_cast<float4*>(p.x + (size_t)tok * p.ld_x + f0);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tq + c0, v);
+          const int f0 = nt * BN + c0;
+          if (ok && f0 < p.N) {
+            float4* xr = reinterpret_cast<float4*>(p.x + (size_t)tok * p.ld_x + f0);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 o = xr[i];
-            o.x += v[4 * i]; o.y += v[4 * i + 1]; o.z += v[4 * i + 2]; o.w += v[4 * i + 3];
-            xr[i] = o;
-          }
-        }
-      }
-    } else if (MODE == PF_SWIGLU) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        float g[32], u[32];
-        tmem_ld32(tq + c0, g);
-        tmem_ld32(tq + 128 + c0, u);
-        const int f0 = nt * 128 + c0;
-        if (ok && f0 < p.N) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) g[i] = g[i] / (1.0f + __expf(-g[i])) * u[i];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            store_split8(p.h + (size_t)tok * p.ld_h + f0 + 8 * i, p.h + (size_t)(kPfRows + tok) * p.ld_h + f0 + 8 * i,
-                         g + 8 * i);
-        }
-      }
-    } else {
-      // QKV: the tile's 128 features of kind q / k / v = 128 / hd whole heads;
-      // rotate-half RoPE pairs dims (j, j + hd/2) of a head: columns c and c + hd/2
-      const int hd = p.hd, half = hd >> 1;
-      const int nrows = kind == 0 ? p.nq : p.nk;
-      const int pos = p.pos0 + tok;
-#pragma unroll 1
-      for (int h0 = 0; h0 < 128; h0 += hd) {
-#pragma unroll 1
-        for (int c = 0; c < half; c += 32) {
-          float a[32], b[32];
-          tmem_ld32(tq + h0 + c, a);
-          tmem_ld32(tq + h0 + half + c, b);
-          const int fa = lt * 128 + h0 + c;          // feature of a[0] within q / k / v
-          // (no early exit: every lane of the warp must reach the next tcgen05.ld)
-          if (ok && fa < nrows && kind < 2) {
-            const float4* cs = reinterpret_cast<const float4*>(p.rope_cs + (size_t)pos * half + c);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float4 t = cs[i];            // (cos, sin) of dims c + 2i, c + 2i + 1
-              const float a0 = a[2 * i], b0 = b[2 * i], a1 = a[2 * i + 1], b1 = b[2 * i + 1];
-              a[2 * i] = a0 * t.x - b0 * t.y;
-              b[2 * i] = b0 * t.x + a0 * t.y;
-              a[2 * i + 1] = a1 * t.z - b1 * t.w;
-              b[2 * i + 1] = b1 * t.z + a1 * t.w;
-            }
-          }
-          if (!ok || fa >= nrows) {
-          } else if (kind == 0) {
-            float4* qa = reinterpret_cast<float4*>(p.q + (size_t)tok * p.ld_q + fa);
-            float4* qb = reinterpret_cast<float4*>(p.q + (size_t)tok * p.ld_q + fa + half);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              qa[i] = make_float4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
-              qb[i] = make_float4(b[4 * i], b[4 * i + 1], b[4 * i + 2], b[4 * i + 3]);
-            }
-          } else {
-            const int kh = fa / hd;
-            const size_t plane = (size_t)p.hkv * p.page_size * hd;   // elements per (layer, plane)
-            const size_t base = (size_t)p.page_table[pos >> p.page_shift] * p.page_stride +
-                                ((size_t)(p.layer * kKvPlanes + 2 * (kind - 1)) * p.hkv + kh) * p.page_size * hd +
-                                (size_t)(pos & (p.page_size - 1)) * hd + c;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              store_split8(p.kv + base + 8 * i, p.kv + base + plane + 8 * i, a + 8 * i);
-              store_split8(p.kv + base + half + 8 * i, p.kv + base + plane + half + 8 * i, b + 8 * i);
+            for (int q = 0; q < 8; ++q) {
+              float4 o = xr[q];
+              o.x += v[4 * q]; o.y += v[4 * q + 1]; o.z += v[4 * q + 2]; o.w += v[4 * q + 3];
+              xr[q] = o;
             }
           }
         }
+      } else if (MODE == PF_SWIGLU) {
+        constexpr int HB = BN / 2;                   // gate columns [0, HB), up columns [HB, BN)
+#pragma unroll 1
+        for (int c0 = 0; c0 < HB; c0 += 32) {
+          float g[32], u[32];
+          tmem_ld32(tq + c0, g);
+          tmem_ld32(tq + HB + c0, u);
+          const int f0 = lt * HB + c0;
+          if (ok && f0 < p.N) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) g[q] = g[q] / (1.0f + __expf(-g[q])) * u[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              store_split8(p.h + (size_t)tok * p.ld_h + f0 + 8 * q, p.h + (size_t)(kPfRows + tok) * p.ld_h + f0 + 8 * q,
+                           g + 8 * q);
+          }
+        }
+      } else {
+        // QKV: the tile's BN features of kind q / k / v = BN / hd whole heads;
+        // rotate-half RoPE pairs dims (j, j + hd/2) of a head: columns c and c + hd/2
+        const int hd = p.hd, half = hd >> 1;
+        const int nrows = kind == 0 ? p.nq : p.nk;
+        const int pos = p.pos0 + tok;
+#pragma unroll 1
+        for (int h0 = 0; h0 < BN; h0 += hd) {
+#pragma unroll 1
+          for (int c = 0; c < half; c += 32) {
+            float x0[32], x1[32];
+            tmem_ld32(tq + h0 + c, x0);
+            tmem_ld32(tq + h0 + half + c, x1);
+            const int fa = lt * BN + h0 + c;          // feature of x0[0] within q / k / v
+            // (no early exit: every lane of the warp must reach the next tcgen05.ld)
+            if (ok && fa < nrows && kind < 2) {
+              const float4* cs = reinterpret_cast<const float4*>(p.rope_cs + (size_t)pos * half + c);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const float4 t = cs[q];            // (cos, sin) of dims c + 2q, c + 2q + 1
+                const float a0 = x0[2 * q], b0 = x1[2 * q], a1 = x0[2 * q + 1], b1 = x1[2 * q + 1];
+                x0[2 * q] = a0 * t.x - b0 * t.y;
+                x1[2 * q] = b0 * t.x + a0 * t.y;
+                x0[2 * q + 1] = a1 * t.z - b1 * t.w;
+                x1[2 * q + 1] = b1 * t.z + a1 * t.w;
+              }
+            }
+            if (!ok || fa >= nrows) {
+            } else if (kind == 0) {
+              float4* qa = reinterpret_cast<float4*>(p.q + (size_t)tok * p.ld_q + fa);
+              float4* qb = reinterpret_cast<float4*>(p.q + (size_t)tok * p.ld_q + fa + half);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                qa[q] = make_float4(x0[4 * q], x0[4 * q + 1], x0[4 * q + 2], x0[4 * q + 3]);
+                qb[q] = make_float4(x1[4 * q], x1[4 * q + 1], x1[4 * q + 2], x1[4 * q + 3]);
+              }
+            } else {
+              const int kh = fa / hd;
+              const size_t plane = (size_t)p.hkv * p.page_size * hd;   // elements per (layer, plane)
+              const size_t base = (size_t)p.page_table[pos >> p.page_shift] * p.page_stride +
+                                  ((size_t)(p.layer * kKvPlanes + 2 * (kind - 1)) * p.hkv + kh) * p.page_size * hd +
+                                  (size_t)(pos & (p.page_size - 1)) * hd + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                store_split8(p.kv + base + 8 * q, p.kv + base + plane + 8 * q, x0 + 8 * q);
+                store_split8(p.kv + base + half + 8 * q, p.kv + base + plane + half + 8 * q, x1 + 8 * q);
+              }
+            }
+          }
+        }
       }
+      tc_fence_before();
+      mbar_arrive(&tempty[a]);                       // this accumulator may be overwritten
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<2 * BN>(tmem);
 }
 
 // ------------------------------------------------------------------ RMSNorm (+ embed)

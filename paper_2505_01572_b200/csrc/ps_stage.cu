@@ -146,11 +146,18 @@ static ps_status init_stage_device(int device) {
   CU_TRY(cudaFuncSetAttribute(mega_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<32>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<64>::kBytes));
   CU_TRY(cudaFuncSetAttribute(mega_kernel<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, MegaSmem<16, 6>::kBytes));
-  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_smem_bytes<PF_QKV>()));
-  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              pf_smem_bytes<PF_RESID>()));
-  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              pf_smem_bytes<PF_SWIGLU>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_QKV, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<128>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_QKV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<256>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_RESID, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<128>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_RESID, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<256>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<256>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<128>()));
   CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<64>()));
   CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<128>()));
   return PS_OK;
@@ -928,9 +935,7 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
       // QKV: q tiles, then k, then v (each matrix's rows padded to 128)
       g[0].mX = mxs; g[0].mW0 = M.q; g[0].mW1 = M.k; g[0].mW2 = M.v;
       g[0].K = d;
-      g[0].t1 = (hq + 127) / 128;
-      g[0].t2 = g[0].t1 + (hkv + 127) / 128;
-      g[0].N = g[0].t2 + (hkv + 127) / 128;          // (QKV: n_tiles)
+      g[0].N = hq + 2 * hkv;                          // (tiles per matrix set at launch, per tile width)
       g[0].nq = hq; g[0].nk = hkv;
       g[0].q = S->pf_q; g[0].ld_q = hq;
       g[0].kv = S->kv; g[0].page_table = S->d_page_table; g[0].page_size = S->page_size; g[0].page_shift = shift;
@@ -942,6 +947,8 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
       g[2].mX = mxs; g[2].K = d; g[2].N = f; g[2].h = S->pf_h; g[2].ld_h = f;
       P_TRY(make_map(&g[2].mW0, W[PS_WG], f, d, 128));
       P_TRY(make_map(&g[2].mW1, W[PS_WU], f, d, 128));
+      g[2].mG64 = M.g;                                 // (the megakernel's 64-row boxes)
+      g[2].mU64 = M.u;
       // down (+ residual)
       g[3].mX = mh; g[3].mW0 = M.d; g[3].K = f; g[3].N = d; g[3].x = S->pf_x; g[3].ld_x = d;
     }
@@ -1034,13 +1041,35 @@ static ps_status prefill_chunk(ps_stage* S, const int32_t* toks, int T, long lon
   ap.T = T; ap.pos0 = (int)pos0; ap.out = S->pf_att; ap.ld_out = hq;
   const int QB = 64 / (sh.n_heads / sh.n_kv_heads);
   const dim3 agrid((T + QB - 1) / QB, sh.n_kv_heads);
-  auto gemm = [&](int mode, PfGemmParams& g, int n_tiles) -> ps_status {
+  // Tile width: 256 features (half the activation re-reads per FLOP) unless the
+  // 128-wide tiling finishes in fewer tile-times on the persistent grid (wave
+  // quantisation: cost = ceil(tiles / SMs) x width, by at least 25%); a SwiGLU tile holds
+  // width / 2 gate rows and the same up rows.
+  auto gemm = [&](int mode, PfGemmParams& g) -> ps_status {
     g.T = T;
     g.pos0 = (int)pos0;
-    const dim3 grid(mt, n_tiles);
-    if (mode == PF_QKV) pf_gemm_kernel<PF_QKV><<<grid, kPfThreads, pf_smem_bytes<PF_QKV>(), S->stream>>>(g);
-    else if (mode == PF_RESID) pf_gemm_kernel<PF_RESID><<<grid, kPfThreads, pf_smem_bytes<PF_RESID>(), S->stream>>>(g);
-    else pf_gemm_kernel<PF_SWIGLU><<<grid, kPfThreads, pf_smem_bytes<PF_SWIGLU>(), S->stream>>>(g);
+    g.m_tiles = mt;
+    const int hkv = sh.n_kv_heads * sh.head_dim;
+    auto tiles = [&](int bn) {
+      return mode == PF_QKV ? (hq + bn - 1) / bn + 2 * ((hkv + bn - 1) / bn)
+             : mode == PF_SWIGLU ? (g.N + bn / 2 - 1) / (bn / 2) : (g.N + bn - 1) / bn;
+    };
+    int bn = 256;
+    const long long c256 = (long long)((tiles(256) * mt + g_num_sms - 1) / g_num_sms) * 256;
+    const long long c128 = (long long)((tiles(128) * mt + g_num_sms - 1) / g_num_sms) * 128;
+    if (4 * c128 <= 3 * c256) bn = 128;   // (a 128-wide tile moves more operand bytes per FLOP: measured
+                                          // 8B gate/up 128-wide on 7 waves slower than 256-wide on 4)
+    g.n_tiles = tiles(bn);
+    g.t1 = (hq + bn - 1) / bn;
+    g.t2 = g.t1 + (hkv + bn - 1) / bn;
+    const int grid = std::min(g.n_tiles * mt, g_num_sms);
+    if (mode == PF_QKV && bn == 128) pf_gemm_kernel<PF_QKV, 128><<<grid, kPfThreads, pf_smem_bytes<128>(), S->stream>>>(g);
+    else if (mode == PF_QKV) pf_gemm_kernel<PF_QKV, 256><<<grid, kPfThreads, pf_smem_bytes<256>(), S->stream>>>(g);
+    else if (mode == PF_RESID && bn == 128)
+      pf_gemm_kernel<PF_RESID, 128><<<grid, kPfThreads, pf_smem_bytes<128>(), S->stream>>>(g);
+    else if (mode == PF_RESID) pf_gemm_kernel<PF_RESID, 256><<<grid, kPfThreads, pf_smem_bytes<256>(), S->stream>>>(g);
+    else if (bn == 128) pf_gemm_kernel<PF_SWIGLU, 128><<<grid, kPfThreads, pf_smem_bytes<128>(), S->stream>>>(g);
+    else pf_gemm_kernel<PF_SWIGLU, 256><<<grid, kPfThreads, pf_smem_bytes<256>(), S->stream>>>(g);
     g_launches++;
     CU_TRY(cudaGetLastError());
     return PS_OK;
@@ -1052,17 +1081,17 @@ static ps_status prefill_chunk(ps_stage* S, const int32_t* toks, int T, long lon
     pf_norm_kernel<<<T, kPfNormThreads, 0, S->stream>>>(l == 0 ? S->pf_tok : nullptr, S->embed, S->vocab_full, S->pf_x,
                                                          d, W[PS_N_ATTN], sh.rms_eps, S->pf_xs);
     g_launches++;
-    if ((st = gemm(PF_QKV, g[0], g[0].N)) != PS_OK) return st;
+    if ((st = gemm(PF_QKV, g[0])) != PS_OK) return st;
     ap.layer = l;
     if (sh.head_dim == 128) pf_attn_kernel<128><<<agrid, 128, pf_attn_smem_bytes<128>(), S->stream>>>(ap);
     else pf_attn_kernel<64><<<agrid, 128, pf_attn_smem_bytes<64>(), S->stream>>>(ap);
     g_launches++;
-    if ((st = gemm(PF_RESID, g[1], (d + 127) / 128)) != PS_OK) return st;
+    if ((st = gemm(PF_RESID, g[1])) != PS_OK) return st;
     pf_norm_kernel<<<T, kPfNormThreads, 0, S->stream>>>(nullptr, S->embed, S->vocab_full, S->pf_x, d, W[PS_N_MLP],
                                                          sh.rms_eps, S->pf_xs);
     g_launches++;
-    if ((st = gemm(PF_SWIGLU, g[2], (sh.d_ffn + 127) / 128)) != PS_OK) return st;
-    if ((st = gemm(PF_RESID, g[3], (d + 127) / 128)) != PS_OK) return st;
+    if ((st = gemm(PF_SWIGLU, g[2])) != PS_OK) return st;
+    if ((st = gemm(PF_RESID, g[3])) != PS_OK) return st;
   }
   CU_TRY(cudaGetLastError());
   return PS_OK;
