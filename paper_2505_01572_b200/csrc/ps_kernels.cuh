@@ -712,43 +712,66 @@ struct AttnParams {
   long long rows_per_page;         // page_stride / hd
   int layer, hkv, H, hd;
   float scale_log2;                // log2(e) / sqrt(hd)
-  int max_chunks, max_rb;          // max_chunks: item partials per (head, row block)
+  int max_chunks, rows_cap;        // item partials per (head, row); query rows per head (kRowsCap * g)
   int sc;                          // 64-key chunks per work item (a per-stage constant)
-  float* ws_o;                     // [hkv][max_rb][max_chunks][kAttnRB][hd]
-  float* ws_ml;                    // [hkv][max_rb][max_chunks][kAttnRB][2]
+  float* ws_o;                     // [hkv][max_chunks][rows_cap][hd]
+  float* ws_ml;                    // [hkv][max_chunks][rows_cap][2]
   __nv_bfloat16* out; int ld_out;
   unsigned long long* dbg;         // optional per-CTA stamps [cta][8] (PS_TRACE builds)
 };
 
 // ---------------------------------------------------------------- decode attention (a6)
-// Work items: (KV head kh, block rb of kAttnRB = 32 query rows, item j = sc
-// consecutive 64-key chunks at absolute positions [64 sc j, 64 sc (j + 1))).
-// sc is a per-stage constant (ps_stage: from max_seq), so a row's arithmetic
-// does not depend on R or on the context length (row-bucket invariance: a
-// verify row equals the AR step at that position bit for bit).  CTA c of G
-// owns the contiguous item range [c n / G, (c + 1) n / G) and streams the
-// items' 16-key stages back to back through a 4-deep TMA ring (3 stages in
-// flight while one is used), so the schedule never changes an item's math.
+// Work items: (KV head kh, row block rb, item j = sc consecutive 64-key chunks
+// at absolute positions [64 sc j, 64 sc (j + 1))).  sc is a per-stage constant
+// (ps_stage: from max_seq), so a row's arithmetic does not depend on R or on
+// the context length (row-bucket invariance: a verify row equals the AR step
+// at that position bit for bit).  CTA c of G owns the contiguous item range
+// [c n / G, (c + 1) n / G) and streams the items' 16-key stages back to back
+// through a 4-deep TMA ring (3 stages in flight while one is used), so the
+// schedule never changes an item's math.
 //
-// Inside a stage the 4 warps split the head dimension: warp w owns dims
-// [w hd/4, (w+1) hd/4).  S = Q K^T is summed from the 4 warps' partial dot
-// products (smem exchange, fixed order w = 0..3, identical in every warp);
-// every warp runs the same online softmax (running max m, sum l) and
-// accumulates O for its own dims.  All 128 threads work at any R (a decode
-// row block of 4 rows is one 16-row MMA group), instead of one warp per 16
-// rows.  Split-bf16 operands on mma.sync m16n8k16: (q_hi + q_lo)(k_hi +
-// k_lo)^T ~ q_hi k_hi + q_lo k_hi + q_hi k_lo (the lo*lo term ~2^-16
-// relative), likewise P V.
-constexpr int kAttnNG = 1;                  // 16-row MMA groups per item
-constexpr int kAttnRB = 16 * kAttnNG;       // query rows per item
+// Keys on the MMA's M side: per 16-key stage S^T = K Q^T (A = K, 16 keys x 16
+// dims by ldmatrix from the ring; B = Q^T, 16 dims x 8 query rows per n-tile,
+// in registers) and O^T = V^T P^T (A = V^T by ldmatrix.trans; B = P^T, the S^T
+// accumulator transposed in registers by movmatrix).  A row block is NR = 1..3
+// n-tiles of 8 rows (query row m of a block = window row m / g, head kh g +
+// m % g): a decode step (R = 1, g = 4: 4 rows) costs one 8-row n-tile, and up
+// to 24 rows (R <= 6 at g = 4, the bench's verify window) take ONE pass over
+// the keys.  The 4 warps split the head dimension (warp w owns dims [w hd/4,
+// (w+1) hd/4)); S^T is summed from the 4 warps' partial dot products (smem
+// exchange, fixed order w = 0..3, identical in every warp); every warp runs the
+// same online softmax and accumulates O^T for its own dims.  Split-bf16
+// operands on mma.sync m16n8k16: (k_hi + k_lo)(q_hi + q_lo) ~ k_hi q_hi +
+// k_hi q_lo + k_lo q_hi (the lo*lo term ~2^-16 relative), likewise V P.
+// Every per-row operation (the MMA's per-element dot products, the fixed-order
+// warp sums, the xor-4/8/16 shuffle trees over a row's 8 key lanes) is the
+// same whichever n-tile column holds the row, so rows are bit-identical for
+// any R.
+constexpr int kAttnRB = 8;                  // query rows per n-tile (row blocks: NR n-tiles)
+constexpr int kAttnMaxNR = 3;
 constexpr int kAttnStep = 16;               // keys per ring stage
 constexpr int kAttnStages = 4;              // ring depth
 template <int HD> __host__ __device__ constexpr int attn_stage_bytes() { return kKvPlanes * kAttnStep * HD * 2; }
 // smem: the ring (kAttnStages x [hd/64][plane][16 keys][128 B], 128B-swizzled
-// by TMA) + its full barriers; the S exchange uses the epilogue scratch area
+// by TMA) + its full barriers; the S exchange lives in the GEMM ring's
+// activation slots (idle during an attention phase, see ps_mega.cuh)
 constexpr int attn_smem_bytes(int /*nw*/) { return kAttnStages * attn_stage_bytes<128>() + 64; }
-constexpr int kAttnXBytes = 4 * kAttnNG * 2 * 32 * 16;   // S exchange: [warp][group][n-tile][lane] float4
-constexpr int kAttnXBufs = kAttnNG == 1 ? 2 : 1;          // exchange buffers (in the 8.7 KB+ scratch area)
+constexpr int kAttnXBytes = 4 * kAttnMaxNR * 32 * 16;   // S exchange buffer: [warp][n-tile][lane] float4
+constexpr int kAttnXBufs = 2;                            // double-buffered (stage t read, t + 1 written)
+// Q^T fragments of the current item, [warp][k step][n-tile][hi|lo][lane] uint2
+// (each thread reads back only its own: no barrier), after the exchange buffers
+constexpr int kAttnQOff = kAttnXBufs * kAttnXBytes;
+constexpr int kAttnQBytes = 4 * 2 * kAttnMaxNR * 2 * 32 * 8;
+constexpr int kAttnXAreaBytes = kAttnQOff + kAttnQBytes;
+// n-tiles per row block.  Any choice gives the same per-row arithmetic (see
+// above), so it is picked per forward for speed: up to 2K keys, one n-tile
+// (more, lighter items: the short phase is latency-bound); beyond, as many as
+// the rows need (one pass over the keys for up to 24 rows).  Measured on the
+// 8B (scripts/_ab_attn.sh): R = 5 at 600 keys 3.855 ms with 1 n-tile vs 3.89
+// with 3; at 8K 5.94 with 3 vs 6.22 with 1; R = 17 at 8K 9.25 vs 11.8.
+__host__ __device__ constexpr int attn_nr(int rows, int n_keys) {
+  return (rows <= 8 || n_keys <= 2048) ? 1 : rows <= 16 ? 2 : 3;
+}
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -764,6 +787,12 @@ PS_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// 8x8 b16 matrix transpose across the warp (lane l: row l / 4, columns 2 (l % 4) .. +1)
+PS_DEV uint32_t movm_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
 }
 // Split a pair of fp32 values into hi / lo packed bf16x2 registers.
 PS_DEV void split_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
@@ -782,12 +811,14 @@ PS_DEV uint32_t attn_sw(int pl, int r, int d) {
 }
 
 struct AttnGeom {
-  int rows, n_rb, n_keys, nsc, n_items;
+  int rows, nr, rb_rows, n_rb, n_keys, nsc, n_items;
   PS_DEV AttnGeom(const AttnParams& p) {
     const int R = p.step->R;
     rows = R * (p.H / p.hkv);
-    n_rb = (rows + kAttnRB - 1) / kAttnRB;
     n_keys = p.step->pos0 + R;
+    nr = attn_nr(rows, n_keys);
+    rb_rows = kAttnRB * nr;
+    n_rb = (rows + rb_rows - 1) / rb_rows;
     const int nchunks = (n_keys + kAttnChunk - 1) / kAttnChunk;
     nsc = (nchunks + p.sc - 1) / p.sc;
     n_items = p.hkv * n_rb * nsc;
@@ -859,19 +890,20 @@ PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t full_u32
 // caller's live ones, so the megakernel keeps little live across the call)
 //
 // Software-pipelined over the CTA's stage stream: iteration t sums stage t's
-// S partials, computes stage t + 1's partial Q K^T (its HMMAs overlap stage
-// t's softmax), then runs stage t's online softmax and P V; one barrier per
-// iteration publishes the t + 1 partials.  Stage t + 1 may start the next
-// item: its geometry and query fragments are loaded before its Q K^T, while
-// stage t's item state is finished (partial written) after its P V.
-template <int HD>
-__device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, float4* xbuf,
+// S^T partials, computes stage t + 1's partial K Q^T (its HMMAs overlap stage
+// t's softmax), then runs stage t's online softmax and V^T P^T; one barrier
+// per iteration publishes the t + 1 partials.  Stage t + 1 may start the next
+// item: its geometry and query fragments are loaded before its K Q^T, while
+// stage t's item state is finished (partial written) after its V^T P^T.
+// NR = attn_nr(R g): n-tiles of 8 query rows per item.
+template <int HD, int NR>
+__device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, uint8_t* xbuf,
                                       int tid, int cta, int ncta, uint32_t& seq) {
-  static_assert(kAttnNG == 1, "one 16-row MMA group per item");
   constexpr int DW = HD / 4;          // dims per warp
-  constexpr int KS = DW / 16;         // k steps of QK per warp
-  constexpr int NTO = DW / 8;         // output n-tiles per warp
+  constexpr int KS = DW / 16;         // 16-dim k steps of K Q^T per warp
+  constexpr int MT = DW / 16;         // 16-dim m tiles of V^T P^T per warp
   constexpr uint32_t SB = attn_stage_bytes<HD>();
+  constexpr uint32_t PL = kAttnStep * 128;   // plane stride inside a 64-dim block
   const AttnGeom gm(p);
   const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
   if (it0 >= it_end) return;
@@ -879,21 +911,20 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   const float* const qp = p.q;
   const int ld_q = p.ld_q;
   const float qscale = p.scale_log2;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int d_own = warp * DW;
   const uint32_t ring_u32 = smem_u32(ring), xbuf_u32 = smem_u32(xbuf);
-  // per-lane ldmatrix offsets inside a stage (K: non-transposed, V: transposed)
-  uint32_t koff[KS], voff[NTO / 2];
+  // per-lane ldmatrix offsets inside a stage: K as the A operand (key rows,
+  // non-transposed), V^T as the A operand (transposed)
+  uint32_t koff[KS], voff[MT];
 #pragma unroll
-  for (int kk = 0; kk < KS; ++kk)
-    koff[kk] = attn_sw(0, (lane & 7) + ((lane >> 4) << 3), d_own + kk * 16 + ((lane >> 3) & 1) * 8);
+  for (int kk = 0; kk < KS; ++kk) koff[kk] = attn_sw(0, (lane & 7) + ((lane >> 3) & 1) * 8, d_own + kk * 16 + (lane >> 4) * 8);
 #pragma unroll
-  for (int np = 0; np < NTO / 2; ++np)
-    voff[np] = attn_sw(2, (lane & 7) + ((lane >> 3) & 1) * 8, d_own + np * 16 + (lane >> 4) * 8);
-  constexpr uint32_t PL = kAttnStep * 128;   // plane stride inside a 64-dim block
-  // exchange slot of this thread (buffer 0; buffer 1 at + kAttnXBytes)
-  const uint32_t xw = xbuf_u32 + ((warp * 2) * 32 + lane) * 16;   // this warp's n-tile 0 slot
-  const uint32_t xr = xbuf_u32 + lane * 16;                          // warp 0's n-tile 0 slot
+  for (int mt = 0; mt < MT; ++mt) voff[mt] = attn_sw(2, (lane & 7) + (lane >> 4) * 8, d_own + mt * 16 + ((lane >> 3) & 1) * 8);
+  // exchange slot of (buffer b, warp w, n-tile n, this lane): xbuf + ((b * 4 + w) * NR + n) * 512 + lane * 16
+  const uint32_t xw = xbuf_u32 + (warp * NR) * 512 + lane * 16;
+  const uint32_t xr = xbuf_u32 + lane * 16;
+  constexpr uint32_t XB = 4 * NR * 512;      // one buffer
 #if PS_TRACE
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
   unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
@@ -909,195 +940,213 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   } while (0)
 #endif
   // ---- item state: cur (stage t) and nxt (stage t + 1)
-  int c_item = it0, c_s = 0, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_ok;
-  int c_qpos[2];
-  int n_item = it0, n_s = 0, n_ns = 0, n_kbeg = 0, n_kend = 0, n_kh = 0, n_rb = 0, n_j = 0, n_ok = 0;
-  int n_qpos[2];
-  uint32_t qh[KS][4], ql[KS][4];
-  auto load_item = [&](int it, int& ns, int& kbeg, int& kend, int& kh, int& rb, int& j, int& ok, int* qpos) {
+  int c_item = it0, c_s = 0, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_mrows;
+  int n_item = it0, n_s = 0, n_ns = 0, n_kbeg = 0, n_kend = 0, n_kh = 0, n_rb = 0, n_j = 0, n_mrows = 0;
+  // this thread's Q^T B fragment (hi / lo) of k step kk, n-tile n: a uint2 at qslot(kk, n, hl)
+  const uint32_t qs_u32 = xbuf_u32 + kAttnQOff + lane * 8;
+  auto qslot = [&](int kk, int n, int hl) { return qs_u32 + (uint32_t)((((warp * KS + kk) * NR + n) * 2 + hl) * 256); };
+  auto load_item = [&](int it, int& ns, int& kbeg, int& kend, int& kh, int& rb, int& j, int& mrows) {
     gm.item(p, it, kh, rb, j, kbeg, kend, ns);
-    const int m0 = rb * kAttnRB;
-    const int mrows = min(kAttnRB, gm.rows - m0);
-    ok = 1;
-    int qoff[2];
+    const int m0 = rb * gm.rb_rows;
+    mrows = min(gm.rb_rows, gm.rows - m0);
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int m = (lane >> 2) + hr * 8;
+    for (int n = 0; n < NR; ++n) {
+      // B fragment column n-index gq = query row 8 n + gq of the block
+      const int m = n * 8 + gq;
       const int mg = m0 + m, r = mg / g, h = kh * g + mg % g;
-      qoff[hr] = m < mrows ? r * ld_q + h * HD : -1;
-      qpos[hr] = min(kend - 1, pos0 + r);     // last key this row sees in this item
-    }
+      const int qo = m < mrows ? r * ld_q + h * HD : -1;
 #pragma unroll
-    for (int kk = 0; kk < KS; ++kk)
+      for (int kk = 0; kk < KS; ++kk) {
+        uint32_t bh[2], bl[2];
 #pragma unroll
-      for (int jq = 0; jq < 4; ++jq) {
-        const int o = qoff[jq & 1];
-        const int d = d_own + kk * 16 + (lane & 3) * 2 + (jq >> 1) * 8;
-        const float2 qv = o >= 0 ? *reinterpret_cast<const float2*>(qp + o + d) : make_float2(0.f, 0.f);
-        split_pack(qv.x * qscale, qv.y * qscale, qh[kk][jq], ql[kk][jq]);
+        for (int hf = 0; hf < 2; ++hf) {
+          const int d = d_own + kk * 16 + tq * 2 + hf * 8;
+          const float2 qv = qo >= 0 ? *reinterpret_cast<const float2*>(qp + qo + d) : make_float2(0.f, 0.f);
+          split_pack(qv.x * qscale, qv.y * qscale, bh[hf], bl[hf]);
+        }
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(qslot(kk, n, 0)), "r"(bh[0]), "r"(bh[1]) : "memory");
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(qslot(kk, n, 1)), "r"(bl[0]), "r"(bl[1]) : "memory");
       }
+    }
   };
-  // partial S of stage `u` (ring sequence number) over this warp's dims -> exchange buffer u & 1
+  // causal limit of S^T column (row 8 n + 2 tq + e of row block rb): the row's position, within the item
+  auto qpos_of = [&](int rb, int kend, int n, int e) {
+    return min(kend - 1, pos0 + (rb * gm.rb_rows + n * 8 + tq * 2 + e) / g);
+  };
+  // partial S^T of stage `u` (ring sequence number) over this warp's dims -> exchange buffer u & 1
   auto qk_partial = [&](uint32_t u) {
     const int buf = u % kAttnStages;
     mbar_wait(&full[buf], (u / kAttnStages) & 1);
     const uint32_t sb = ring_u32 + buf * SB;
-    float s3[3][2][4];
+    constexpr int NA = 1;   // (one chain per k step, summed at the end, measured no faster)
+    float a[NA][NR][4];
 #pragma unroll
-    for (int t = 0; t < 3; ++t)
+    for (int c = 0; c < NA; ++c)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) s3[t][nt][0] = s3[t][nt][1] = s3[t][nt][2] = s3[t][nt][3] = 0.f;
+      for (int n = 0; n < NR; ++n) a[c][n][0] = a[c][n][1] = a[c][n][2] = a[c][n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-      uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
-      ldsm_x4(sb + koff[kk], b0, b1, b2, b3);        // K_hi
-      ldsm_x4(sb + PL + koff[kk], c0, c1, c2, c3);   // K_lo
-      mma16816(s3[0][0], qh[kk], b0, b1);
-      mma16816(s3[0][1], qh[kk], b2, b3);
-      mma16816(s3[1][0], ql[kk], b0, b1);
-      mma16816(s3[1][1], ql[kk], b2, b3);
-      mma16816(s3[2][0], qh[kk], c0, c1);
-      mma16816(s3[2][1], qh[kk], c2, c3);
+      uint32_t kh4[4], kl4[4];
+      ldsm_x4(sb + koff[kk], kh4[0], kh4[1], kh4[2], kh4[3]);        // K_hi
+      ldsm_x4(sb + PL + koff[kk], kl4[0], kl4[1], kl4[2], kl4[3]);   // K_lo
+#pragma unroll
+      for (int n = 0; n < NR; ++n) {
+        uint32_t bh0, bh1, bl0, bl1;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(bh0), "=r"(bh1) : "r"(qslot(kk, n, 0)) : "memory");
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(bl0), "=r"(bl1) : "r"(qslot(kk, n, 1)) : "memory");
+        float* acc = a[kk % NA][n];
+        mma16816(acc, kh4, bh0, bh1);
+        mma16816(acc, kh4, bl0, bl1);
+        mma16816(acc, kl4, bh0, bh1);
+      }
     }
-    const uint32_t xb = xw + (u & 1) * kAttnXBytes;
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-      st_shared_v4(xb + nt * 512, (s3[0][nt][0] + s3[1][nt][0]) + s3[2][nt][0],
-                   (s3[0][nt][1] + s3[1][nt][1]) + s3[2][nt][1], (s3[0][nt][2] + s3[1][nt][2]) + s3[2][nt][2],
-                   (s3[0][nt][3] + s3[1][nt][3]) + s3[2][nt][3]);
+    for (int c = 1; c < NA; ++c)
+#pragma unroll
+      for (int n = 0; n < NR; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[0][n][i] += a[c][n][i];
+    const uint32_t xb = xw + (u & 1) * XB;
+#pragma unroll
+    for (int n = 0; n < NR; ++n) st_shared_v4(xb + n * 512, a[0][n][0], a[0][n][1], a[0][n][2], a[0][n][3]);
   };
-  float mrow[2], lrow[2];
-  float oacc[NTO][4];
+  float mrow[NR][2], lrow[NR][2];
+  float oacc[MT][NR][4];
   auto reset_state = [&]() {
-    mrow[0] = mrow[1] = -INFINITY;
-    lrow[0] = lrow[1] = 0.f;
 #pragma unroll
-    for (int n = 0; n < NTO; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+    for (int n = 0; n < NR; ++n) {
+      mrow[n][0] = mrow[n][1] = -INFINITY;
+      lrow[n][0] = lrow[n][1] = 0.f;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) oacc[mt][n][0] = oacc[mt][n][1] = oacc[mt][n][2] = oacc[mt][n][3] = 0.f;
+    }
   };
-  // ---- prologue: stage 0's partial S
-  load_item(c_item, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_ok, c_qpos);
+  // ---- prologue: stage 0's partial S^T
+  load_item(c_item, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_mrows);
   reset_state();
   qk_partial(seq);
   named_bar(2, 128);
   while (true) {
-    // ---- S of stage t (fixed warp order)
-    float sacc[2][4];
+    // ---- S^T of stage t (fixed warp order)
+    float sacc[NR][4];
     {
-      const uint32_t xb = xr + (seq & 1) * kAttnXBytes;
+      const uint32_t xb = xr + (seq & 1) * XB;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        float4 v = ld_shared_v4(xb + nt * 512);
+      for (int n = 0; n < NR; ++n) {
+        float4 v = ld_shared_v4(xb + n * 512);
 #pragma unroll
         for (int w = 1; w < 4; ++w) {
-          const float4 x = ld_shared_v4(xb + nt * 512 + w * 1024);
+          const float4 x = ld_shared_v4(xb + (w * NR + n) * 512);
           v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
         }
-        sacc[nt][0] = v.x; sacc[nt][1] = v.y; sacc[nt][2] = v.z; sacc[nt][3] = v.w;
+        sacc[n][0] = v.x; sacc[n][1] = v.y; sacc[n][2] = v.z; sacc[n][3] = v.w;
       }
     }
     PS_ATTN_LAP(tr_wait);
-    // ---- stage t + 1: next position in the stream; its partial S
+    // ---- stage t + 1: next position in the stream; its partial S^T
     const bool more = (c_s + 1 < c_ns) || (c_item + 1 < it_end);
     if (more) {
       if (c_s + 1 < c_ns) {
         n_item = c_item; n_s = c_s + 1; n_ns = c_ns; n_kbeg = c_kbeg; n_kend = c_kend; n_kh = c_kh; n_rb = c_rb;
-        n_j = c_j; n_ok = c_ok; n_qpos[0] = c_qpos[0]; n_qpos[1] = c_qpos[1];
+        n_j = c_j; n_mrows = c_mrows;
       } else {
         n_item = c_item + 1;
         n_s = 0;
-        load_item(n_item, n_ns, n_kbeg, n_kend, n_kh, n_rb, n_j, n_ok, n_qpos);
+        load_item(n_item, n_ns, n_kbeg, n_kend, n_kh, n_rb, n_j, n_mrows);
       }
       qk_partial(seq + 1);
     }
     PS_ATTN_LAP(tr_qk);
-    // ---- stage t: mask, online softmax, O (own dims) = O * scale + P V
+    // ---- stage t: mask, online softmax, O^T (own dims) = O^T * scale + V^T P^T
     const int k0 = c_kbeg + c_s * kAttnStep;
     const uint32_t sb = ring_u32 + (seq % kAttnStages) * SB;
-    uint32_t vh[NTO / 2][4], vl[NTO / 2][4];
+    uint32_t vh[MT][4], vl[MT][4];
 #pragma unroll
-    for (int np = 0; np < NTO / 2; ++np) {
-      ldsm_x4_t(sb + voff[np], vh[np][0], vh[np][1], vh[np][2], vh[np][3]);            // V_hi
-      ldsm_x4_t(sb + PL + voff[np], vl[np][0], vl[np][1], vl[np][2], vl[np][3]);       // V_lo
+    for (int mt = 0; mt < MT; ++mt) {
+      ldsm_x4_t(sb + voff[mt], vh[mt][0], vh[mt][1], vh[mt][2], vh[mt][3]);                        // V_hi
+      ldsm_x4_t(sb + PL + voff[mt], vl[mt][0], vl[mt][1], vl[mt][2], vl[mt][3]);                      // V_lo
     }
-    float scale[2];
+    float scale[NR][2];
+    uint32_t pbh[NR][2], pbl[NR][2];     // P^T as B fragments (keys 0-7 / 8-15 of the stage), hi / lo
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      float mx = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {
-          const int key = k0 + nt * 8 + (lane & 3) * 2 + e2;
-          float& sv = sacc[nt][hr * 2 + e2];
-          if (key > c_qpos[hr]) sv = -INFINITY;
-          mx = fmaxf(mx, sv);
-        }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float mn = fmaxf(mrow[hr], mx);
-      scale[hr] = (mrow[hr] == -INFINITY) ? 0.f : ex2_approx(mrow[hr] - mn);
-      mrow[hr] = mn;
-    }
-    float lsum[2] = {0.f, 0.f};
-    uint32_t pah[4], pal[4];               // P as the A fragment (16 rows x 16 keys), hi / lo
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
+    for (int n = 0; n < NR; ++n) {
       float pv[4];
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int hr = q4 >> 1;
-        pv[q4] = (mrow[hr] == -INFINITY) ? 0.f : ex2_approx(sacc[nt][q4] - mrow[hr]);
-        lsum[hr] += pv[q4];
+      for (int e = 0; e < 2; ++e) {
+        // this thread's S^T entries of row 8 n + 2 tq + e: keys gq (c_e) and gq + 8 (c_{2+e})
+        float sa = sacc[n][e], sb8 = sacc[n][2 + e];
+        const int qpos = qpos_of(c_rb, c_kend, n, e);
+        if (k0 + gq > qpos) sa = -INFINITY;
+        if (k0 + gq + 8 > qpos) sb8 = -INFINITY;
+        float mx = fmaxf(sa, sb8);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        const float mn = fmaxf(mrow[n][e], mx);
+        scale[n][e] = (mrow[n][e] == -INFINITY) ? 0.f : ex2_approx(mrow[n][e] - mn);
+        mrow[n][e] = mn;
+        const float pa = (mn == -INFINITY) ? 0.f : ex2_approx(sa - mn);
+        const float pb = (mn == -INFINITY) ? 0.f : ex2_approx(sb8 - mn);
+        float ls = pa + pb;
+        ls += __shfl_xor_sync(0xffffffffu, ls, 4);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 8);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 16);
+        lrow[n][e] = lrow[n][e] * scale[n][e] + ls;
+        pv[e] = pa;
+        pv[2 + e] = pb;
       }
-      split_pack(pv[0], pv[1], pah[nt * 2 + 0], pal[nt * 2 + 0]);
-      split_pack(pv[2], pv[3], pah[nt * 2 + 1], pal[nt * 2 + 1]);
+      uint32_t h01, l01, h23, l23;
+      split_pack(pv[0], pv[1], h01, l01);      // key gq, rows 2 tq, 2 tq + 1
+      split_pack(pv[2], pv[3], h23, l23);      // key gq + 8
+      pbh[n][0] = movm_t(h01);                 // -> row gq, keys 2 tq, 2 tq + 1 (the B layout)
+      pbh[n][1] = movm_t(h23);
+      pbl[n][0] = movm_t(l01);
+      pbl[n][1] = movm_t(l23);
     }
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 1);
-      lsum[hr] += __shfl_xor_sync(0xffffffffu, lsum[hr], 2);
-      lrow[hr] = lrow[hr] * scale[hr] + lsum[hr];
-    }
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int n = 0; n < NTO; ++n) {
-      oacc[n][0] *= scale[0]; oacc[n][1] *= scale[0];
-      oacc[n][2] *= scale[1]; oacc[n][3] *= scale[1];
-    }
+      for (int n = 0; n < NR; ++n) {
+        oacc[mt][n][0] *= scale[n][0]; oacc[mt][n][1] *= scale[n][1];
+        oacc[mt][n][2] *= scale[n][0]; oacc[mt][n][3] *= scale[n][1];
+      }
 #pragma unroll
-    for (int np = 0; np < NTO / 2; ++np) {
-      mma16816(oacc[2 * np], pah, vh[np][0], vh[np][1]);
-      mma16816(oacc[2 * np + 1], pah, vh[np][2], vh[np][3]);
-      mma16816(oacc[2 * np], pal, vh[np][0], vh[np][1]);
-      mma16816(oacc[2 * np + 1], pal, vh[np][2], vh[np][3]);
-      mma16816(oacc[2 * np], pah, vl[np][0], vl[np][1]);
-      mma16816(oacc[2 * np + 1], pah, vl[np][2], vl[np][3]);
-    }
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int n = 0; n < NR; ++n) {
+        mma16816(oacc[mt][n], vh[mt], pbh[n][0], pbh[n][1]);
+        mma16816(oacc[mt][n], vl[mt], pbh[n][0], pbh[n][1]);
+        mma16816(oacc[mt][n], vh[mt], pbl[n][0], pbl[n][1]);
+      }
     // this warp is done with stage t's buffer (K/V fragments are in registers)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[seq % kAttnStages]);
     PS_ATTN_LAP(tr_pv);
     if (c_s + 1 == c_ns) {
-      // ---- item partial -> workspace [kh][rb][j][kAttnRB rows][HD] (own dims; m, l by warp 0)
-      const size_t base = (size_t)((c_kh * p.max_rb + c_rb) * p.max_chunks + c_j) * kAttnRB;
+      // ---- item partial -> workspace [kh][j][row][HD] (own dims; m, l by warp 0)
+      const size_t base = ((size_t)c_kh * p.max_chunks + c_j) * p.rows_cap + (size_t)c_rb * gm.rb_rows;
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        const int m = (lane >> 2) + hr * 8;
-        float* op = p.ws_o + (base + m) * HD + d_own;
+      for (int n = 0; n < NR; ++n)
 #pragma unroll
-        for (int n = 0; n < NTO; ++n)
-          __stcg(reinterpret_cast<float2*>(op + n * 8 + (lane & 3) * 2), make_float2(oacc[n][hr * 2], oacc[n][hr * 2 + 1]));
-        if (warp == 0 && (lane & 3) == 0)
-          __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[hr], lrow[hr]));
-      }
+        for (int e = 0; e < 2; ++e) {
+          const int m = n * 8 + tq * 2 + e;
+          if (m >= c_mrows) continue;         // a later row block's row (or none)
+          float* op = p.ws_o + (base + m) * HD + d_own + gq;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            __stcg(op + mt * 16, oacc[mt][n][e]);
+            __stcg(op + mt * 16 + 8, oacc[mt][n][2 + e]);
+          }
+          if (warp == 0 && gq == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[n][e], lrow[n][e]));
+        }
       reset_state();
     }
     ++seq;
     if (!more) break;
     c_item = n_item; c_s = n_s; c_ns = n_ns; c_kbeg = n_kbeg; c_kend = n_kend; c_kh = n_kh; c_rb = n_rb; c_j = n_j;
-    c_ok = n_ok; c_qpos[0] = n_qpos[0]; c_qpos[1] = n_qpos[1];
+    c_mrows = n_mrows;
     named_bar(2, 128);                       // stage t + 1's partials are published
   }
-  (void)c_ok;
 #if PS_TRACE
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
   if (tid == 0 && p.dbg) {
@@ -1126,12 +1175,12 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
   constexpr int DPL = HD / 32;
   using VecT = typename std::conditional<DPL == 4, float4, float2>::type;
   constexpr int kIF = 8;                  // O loads in flight per warp
+  const size_t cstride = (size_t)p.rows_cap;   // rows between partial c and c + 1 of a row
   for (int it = cta; it < p.hkv * rows; it += ncta) {
     const int kh = it / rows, mg = it % rows;
-    const int rb = mg / kAttnRB, m = mg % kAttnRB;
-    const size_t rbase = (size_t)(kh * p.max_rb + rb) * p.max_chunks;
+    const size_t rbase = (size_t)kh * p.max_chunks * cstride + mg;   // partial c of this row: rbase + c * cstride
     float M = -INFINITY;
-    for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(p.ws_ml + ((rbase + c) * kAttnRB + m) * 2));
+    for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(p.ws_ml + (rbase + c * cstride) * 2));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float acc[DPL];
@@ -1143,7 +1192,7 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
       const int cl = warp + 4 * (i0 + lane);
       float sc = 0.f;
       if (cl < np) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((rbase + cl) * kAttnRB + m) * 2));
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (rbase + cl * cstride) * 2));
         sc = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
         Lp += sc * ml.y;
       }
@@ -1153,7 +1202,7 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
 #pragma unroll
         for (int q = 0; q < kIF; ++q)
           if (q0 + q < nh)
-            ov[q] = __ldcg(reinterpret_cast<const VecT*>(p.ws_o + ((rbase + warp + 4 * (i0 + q0 + q)) * kAttnRB + m) * HD +
+            ov[q] = __ldcg(reinterpret_cast<const VecT*>(p.ws_o + (rbase + (size_t)(warp + 4 * (i0 + q0 + q)) * cstride) * HD +
                                                          lane * DPL));
 #pragma unroll
         for (int q = 0; q < kIF; ++q) {

@@ -73,7 +73,8 @@ struct MegaSmem {
   static constexpr int kOffRstd = kOffRed + 4 * RP * 8;
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
   static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 1023) / 1024 * 1024;   // TMA 128B-swizzle dst
-  static_assert(128 * (epi_rows<RP>() + 1) * 4 >= kAttnXBufs * kAttnXBytes, "attention S exchange lives in the scratch area");
+  // the attention's S exchange lives in the activation slots (idle in an attention phase)
+  static_assert(kMegaStages * kXBytes >= kAttnXAreaBytes, "attention S exchange + Q fragments live in the X slots");
   static constexpr int kAttnBytes = attn_smem_bytes(4);
   static constexpr int kOffBar = kOffAttn + kAttnBytes;
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
@@ -385,8 +386,19 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        if (Q.a.hd == 128) attn_run<128>(Q.a, attn_smem, afull, aempty, (float4*)scratch, et, c, G, attn_seq);
-        else attn_run<64>(Q.a, attn_smem, afull, aempty, (float4*)scratch, et, c, G, attn_seq);
+        // (the S exchange uses the X slots: during an attention phase this CTA's
+        // previous GEMM phase is consumed, and the next one's X tiles load only
+        // after the combine phase is published)
+        const int nr = attn_nr(sstep->R * (Q.a.H / Q.a.hkv), sstep->pos0 + sstep->R);
+        if (Q.a.hd == 128) {
+          if (nr == 1) attn_run<128, 1>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+          else if (nr == 2) attn_run<128, 2>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+          else attn_run<128, 3>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+        } else {
+          if (nr == 1) attn_run<64, 1>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+          else if (nr == 2) attn_run<64, 2>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+          else attn_run<64, 3>(Q.a, attn_smem, afull, aempty, sX, et, c, G, attn_seq);
+        }
       } else if (kind == PH_ACOMB) {
         if (Q.a.hd == 128) attn_combine<128>(Q.a, scratch, et, c, G);
         else attn_combine<64>(Q.a, scratch, et, c, G);

@@ -261,7 +261,7 @@ static void build_phase(ps_stage* S, int b, int kind, int l, MegaPhase& P, HostM
       a.page_size = S->page_size; a.page_shift = __builtin_ctz((unsigned)S->page_size);
       a.rows_per_page = S->page_elems / sh.head_dim; a.layer = l; a.hkv = sh.n_kv_heads;
       a.H = sh.n_heads; a.hd = sh.head_dim; a.scale_log2 = 1.4426950408889634f / std::sqrt((float)sh.head_dim);
-      a.max_chunks = S->max_chunks; a.max_rb = S->max_rb; a.sc = S->attn_sc;
+      a.max_chunks = S->max_chunks; a.rows_cap = S->max_rb * kAttnRB; a.sc = S->attn_sc;
       a.ws_o = S->attn_o; a.ws_ml = S->attn_ml;
       a.out = S->att; a.ld_out = hq;
       a.dbg = S->attn_dbg;   // PS_TRACE builds only (null otherwise)
