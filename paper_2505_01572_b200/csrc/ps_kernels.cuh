@@ -1087,11 +1087,9 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
         mrow[n][e] = mn;
         const float pa = (mn == -INFINITY) ? 0.f : ex2_approx(sa - mn);
         const float pb = (mn == -INFINITY) ? 0.f : ex2_approx(sb8 - mn);
-        float ls = pa + pb;
-        ls += __shfl_xor_sync(0xffffffffu, ls, 4);
-        ls += __shfl_xor_sync(0xffffffffu, ls, 8);
-        ls += __shfl_xor_sync(0xffffffffu, ls, 16);
-        lrow[n][e] = lrow[n][e] * scale[n][e] + ls;
+        // this lane's share of the row sum (its two keys); the lanes' shares
+        // are added once per item (the max must be row-uniform, the sum not)
+        lrow[n][e] = lrow[n][e] * scale[n][e] + (pa + pb);
         pv[e] = pa;
         pv[2 + e] = pb;
       }
@@ -1125,6 +1123,16 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
     if (c_s + 1 == c_ns) {
       // ---- item partial -> workspace [kh][j][row][HD] (own dims; m, l by warp 0)
       const size_t base = ((size_t)c_kh * p.max_chunks + c_j) * p.rows_cap + (size_t)c_rb * gm.rb_rows;
+#pragma unroll
+      for (int n = 0; n < NR; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float ls = lrow[n][e];                // row sum over the 8 key lanes (fixed tree)
+          ls += __shfl_xor_sync(0xffffffffu, ls, 4);
+          ls += __shfl_xor_sync(0xffffffffu, ls, 8);
+          ls += __shfl_xor_sync(0xffffffffu, ls, 16);
+          lrow[n][e] = ls;
+        }
 #pragma unroll
       for (int n = 0; n < NR; ++n)
 #pragma unroll
