@@ -343,6 +343,23 @@ def test_prefill_gemm_path(name, layers, n):
     st2.close()
 
 
+@pytest.mark.parametrize("page_size", [128, 256])
+def test_prefill_gemm_path_page_sizes(page_size):
+    """The prefill kernels' KV append (per-token page lookup) and attention
+    tiles (32 keys inside one page) with 128- and 256-token pages; a prompt of
+    700 tokens = 512 + 187 positions spans several pages and two chunks."""
+    s, w, st = make("toy-verifier", 43, max_seq=760, page_size=page_size)
+    w64 = synth.weights_to_numpy(w)
+    prompt = list(synth.make_prompt(s.vocab, 700, seed=44))
+    st.prefill(prompt)
+    window = [int(t) for t in synth.make_prompt(s.vocab, 3, seed=45)]
+    a, nxt, lg = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(lg, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
+
+
 def test_prefill_path_rejects_unknown():
     from paper_2505_01572_b200 import abi
     s, w, st = make("toy-verifier", 5, max_seq=128)
