@@ -41,9 +41,11 @@ constexpr int kPfTile = 128 * 64 * 2;            // one 128-row x 64-col bf16 TM
 enum { PF_QKV = 0, PF_RESID = 1, PF_SWIGLU = 2 };
 
 // Tile = 128 tokens x BN output features (BN = 128 or 256; SwiGLU: BN / 2 gate
-// rows + BN / 2 up rows of the same features, stacked into one N = BN operand).
-// Per stage: x_hi, x_lo (128 tokens x 64) and the BN-row weight block.
-template <int BN> __host__ __device__ constexpr int pf_stages() { return BN == 256 ? 3 : 4; }
+// rows + BN / 2 up rows of the same features, stacked into one N = BN operand,
+// BN = 128, 224 or 256).  Per stage: x_hi, x_lo (128 tokens x 64) and the
+// BN-row weight block.
+template <int BN> __host__ __device__ constexpr int pf_stages() { return BN > 128 ? 3 : 4; }
+template <int BN> __host__ __device__ constexpr uint32_t pf_tmem_cols() { return BN > 128 ? 512 : 256; }
 template <int BN> __host__ __device__ constexpr int pf_stage_bytes() { return 2 * kPfTile + BN * 128; }
 template <int BN> __host__ __device__ constexpr int pf_smem_bytes() {
   return pf_stages<BN>() * pf_stage_bytes<BN>() + 1024 + 256;
@@ -53,6 +55,7 @@ struct PfGemmParams {
   CUtensorMap mX;                  // split-bf16 operand [2 kPfRows][K] (hi rows, then lo rows), box {64, 128}
   CUtensorMap mW0, mW1, mW2;       // weights [out][K], box {64, 128}: QKV q/k/v; SwiGLU gate/up; else mW0
   CUtensorMap mG64, mU64;          // SwiGLU with 128-wide tiles: gate / up, box {64, 64}
+  CUtensorMap mG112, mU112;        // SwiGLU with 224-wide tiles: gate / up, box {64, 112}
   int K;                           // reduction length (multiple of 64)
   int N;                           // output features (QKV: all three; SwiGLU: d_ffn)
   int n_tiles, m_tiles;            // output tiles: BN-feature blocks x 128-token blocks
@@ -93,7 +96,7 @@ PS_DEV void store_split8(__nv_bfloat16* hi, __nv_bfloat16* lo, const float* v) {
 // mainloop of tile j + 1.
 template <int MODE, int BN>
 __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfGemmParams p) {
-  static_assert(BN == 128 || BN == 256, "tile width");
+  static_assert(BN == 128 || BN == 256 || (BN == 224 && MODE == PF_SWIGLU), "tile width");
   constexpr int kStages = pf_stages<BN>();
   constexpr int kSB = pf_stage_bytes<BN>();
   extern __shared__ uint8_t smem_raw[];
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<2 * BN>(tslot);
+  if (warp == 1) tmem_alloc<pf_tmem_cols<BN>()>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -144,6 +147,9 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
           if (MODE == PF_SWIGLU && BN == 256) {         // 128 gate rows, then 128 up rows
             tma_load_2d(st + 2 * kPfTile, &p.mW0, &full[s], kb * 64, lt * 128, kEvictNormal);
             tma_load_2d(st + 3 * kPfTile, &p.mW1, &full[s], kb * 64, lt * 128, kEvictNormal);
+          } else if (MODE == PF_SWIGLU && BN == 224) {  // 112 gate rows, then 112 up rows
+            tma_load_2d(st + 2 * kPfTile, &p.mG112, &full[s], kb * 64, lt * 112, kEvictNormal);
+            tma_load_2d(st + 2 * kPfTile + 112 * 128, &p.mU112, &full[s], kb * 64, lt * 112, kEvictNormal);
           } else if (MODE == PF_SWIGLU) {               // 64 gate rows, then 64 up rows
             tma_load_2d(st + 2 * kPfTile, &p.mG64, &full[s], kb * 64, lt * 64, kEvictNormal);
             tma_load_2d(st + 2 * kPfTile + kPfTile / 2, &p.mU64, &full[s], kb * 64, lt * 64, kEvictNormal);
@@ -212,17 +218,23 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
         }
       } else if (MODE == PF_SWIGLU) {
         constexpr int HB = BN / 2;                   // gate columns [0, HB), up columns [HB, BN)
+        constexpr int CW = HB % 32 == 0 ? 32 : 16;   // columns per TMEM load
 #pragma unroll 1
-        for (int c0 = 0; c0 < HB; c0 += 32) {
-          float g[32], u[32];
-          tmem_ld32(tq + c0, g);
-          tmem_ld32(tq + HB + c0, u);
+        for (int c0 = 0; c0 < HB; c0 += CW) {
+          float g[CW], u[CW];
+          if constexpr (CW == 32) {
+            tmem_ld32(tq + c0, g);
+            tmem_ld32(tq + HB + c0, u);
+          } else {
+            tmem_ld16(tq + c0, g);
+            tmem_ld16(tq + HB + c0, u);
+          }
           const int f0 = lt * HB + c0;
           if (ok && f0 < p.N) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) g[q] = g[q] / (1.0f + __expf(-g[q])) * u[q];
+            for (int q = 0; q < CW; ++q) g[q] = g[q] / (1.0f + __expf(-g[q])) * u[q];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < CW / 8; ++q)
               store_split8(p.h + (size_t)tok * p.ld_h + f0 + 8 * q, p.h + (size_t)(kPfRows + tok) * p.ld_h + f0 + 8 * q,
                            g + 8 * q);
           }
@@ -284,7 +296,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<2 * BN>(tmem);
+  if (warp == 1) tmem_dealloc<pf_tmem_cols<BN>()>(tmem);
 }
 
 // ------------------------------------------------------------------ RMSNorm (+ embed)

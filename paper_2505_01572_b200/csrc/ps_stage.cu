@@ -158,6 +158,8 @@ static ps_status init_stage_device(int device) {
                               pf_smem_bytes<256>()));
   CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               pf_smem_bytes<128>()));
+  CU_TRY(cudaFuncSetAttribute(pf_gemm_kernel<PF_SWIGLU, 224>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              pf_smem_bytes<224>()));
   CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<64>()));
   CU_TRY(cudaFuncSetAttribute(pf_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf_attn_smem_bytes<128>()));
   return PS_OK;
@@ -949,6 +951,8 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
       P_TRY(make_map(&g[2].mW1, W[PS_WU], f, d, 128));
       g[2].mG64 = M.g;                                 // (the megakernel's 64-row boxes)
       g[2].mU64 = M.u;
+      P_TRY(make_map(&g[2].mG112, W[PS_WG], f, d, 112));
+      P_TRY(make_map(&g[2].mU112, W[PS_WU], f, d, 112));
       // down (+ residual)
       g[3].mX = mh; g[3].mW0 = M.d; g[3].K = f; g[3].N = d; g[3].x = S->pf_x; g[3].ld_x = d;
     }
@@ -1054,11 +1058,11 @@ static ps_status prefill_chunk(ps_stage* S, const int32_t* toks, int T, long lon
       return mode == PF_QKV ? (hq + bn - 1) / bn + 2 * ((hkv + bn - 1) / bn)
              : mode == PF_SWIGLU ? (g.N + bn / 2 - 1) / (bn / 2) : (g.N + bn - 1) / bn;
     };
+    auto cost = [&](int bn) { return (long long)((tiles(bn) * mt + g_num_sms - 1) / g_num_sms) * bn; };
     int bn = 256;
-    const long long c256 = (long long)((tiles(256) * mt + g_num_sms - 1) / g_num_sms) * 256;
-    const long long c128 = (long long)((tiles(128) * mt + g_num_sms - 1) / g_num_sms) * 128;
-    if (4 * c128 <= 3 * c256) bn = 128;   // (a 128-wide tile moves more operand bytes per FLOP: measured
-                                          // 8B gate/up 128-wide on 7 waves slower than 256-wide on 4)
+    if (mode == PF_SWIGLU && cost(224) < cost(256)) bn = 224;   // (gate/up: 112 + 112 rows)
+    if (4 * cost(128) <= 3 * cost(bn)) bn = 128;   // (a 128-wide tile moves more operand bytes per FLOP:
+                                                   // 8B gate/up 128-wide on 7 waves slower than 256-wide on 4)
     g.n_tiles = tiles(bn);
     g.t1 = (hq + bn - 1) / bn;
     g.t2 = g.t1 + (hkv + bn - 1) / bn;
@@ -1069,6 +1073,7 @@ static ps_status prefill_chunk(ps_stage* S, const int32_t* toks, int T, long lon
       pf_gemm_kernel<PF_RESID, 128><<<grid, kPfThreads, pf_smem_bytes<128>(), S->stream>>>(g);
     else if (mode == PF_RESID) pf_gemm_kernel<PF_RESID, 256><<<grid, kPfThreads, pf_smem_bytes<256>(), S->stream>>>(g);
     else if (bn == 128) pf_gemm_kernel<PF_SWIGLU, 128><<<grid, kPfThreads, pf_smem_bytes<128>(), S->stream>>>(g);
+    else if (bn == 224) pf_gemm_kernel<PF_SWIGLU, 224><<<grid, kPfThreads, pf_smem_bytes<224>(), S->stream>>>(g);
     else pf_gemm_kernel<PF_SWIGLU, 256><<<grid, kPfThreads, pf_smem_bytes<256>(), S->stream>>>(g);
     g_launches++;
     CU_TRY(cudaGetLastError());
