@@ -360,6 +360,28 @@ def test_prefill_gemm_path_page_sizes(page_size):
     st.close()
 
 
+def test_prefill_gemm_path_gqa8_wide():
+    """The prefill kernels at the LLaMA-3.1-70B attention geometry (d = 8192,
+    64 query heads over 8 KV heads: GQA group 8, so a 64-row attention CTA
+    covers 8 positions) and its 28672-wide FFN (gate/up tiles of 112 + 112
+    rows), one layer, vocabulary cut to 4096; 300-token prompt."""
+    from paper_2505_01572_b200 import Stage
+    s = replace(synth.preset("llama3.1-70b"), name="70b-1l", n_layers=1, vocab=4096)
+    w = synth.make_weights(s, seed=47, device="cuda")
+    w64 = synth.weights_to_numpy(w)
+    prompt = list(synth.make_prompt(s.vocab, 300, seed=48))
+    st = Stage(s, w, max_seq=340)
+    st.prefill(prompt)
+    window = [int(t) for t in synth.make_prompt(s.vocab, 2, seed=49)]
+    a, nxt, lg = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(lg, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
+    del w
+    torch.cuda.empty_cache()
+
+
 def test_prefill_path_rejects_unknown():
     from paper_2505_01572_b200 import abi
     s, w, st = make("toy-verifier", 5, max_seq=128)
