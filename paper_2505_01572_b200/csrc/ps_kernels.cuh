@@ -922,9 +922,9 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) voff[mt] = attn_sw(2, (lane & 7) + (lane >> 4) * 8, d_own + mt * 16 + ((lane >> 3) & 1) * 8);
   // exchange slot of (buffer b, warp w, n-tile n, this lane): xbuf + ((b * 4 + w) * NR + n) * 512 + lane * 16
-  const uint32_t xw = xbuf_u32 + (warp * NR) * 512 + lane * 16;
-  const uint32_t xr = xbuf_u32 + lane * 16;
-  constexpr uint32_t XB = 4 * NR * 512;      // one buffer
+  float4* const xw = reinterpret_cast<float4*>(xbuf) + warp * NR * 32 + lane;
+  const float4* const xr = reinterpret_cast<const float4*>(xbuf) + lane;
+  constexpr int XB = 4 * NR * 32;            // one buffer (float4s)
 #if PS_TRACE
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
   unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
@@ -943,8 +943,10 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   int c_item = it0, c_s = 0, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_mrows;
   int n_item = it0, n_s = 0, n_ns = 0, n_kbeg = 0, n_kend = 0, n_kh = 0, n_rb = 0, n_j = 0, n_mrows = 0;
   // this thread's Q^T B fragment (hi / lo) of k step kk, n-tile n: a uint2 at qslot(kk, n, hl)
-  const uint32_t qs_u32 = xbuf_u32 + kAttnQOff + lane * 8;
-  auto qslot = [&](int kk, int n, int hl) { return qs_u32 + (uint32_t)((((warp * KS + kk) * NR + n) * 2 + hl) * 256); };
+  // (plain C++ accesses: the compiler orders them against each other and may
+  // schedule them freely around the MMAs)
+  uint2* const qs = reinterpret_cast<uint2*>(xbuf + kAttnQOff) + lane;
+  auto qslot = [&](int kk, int n, int hl) { return qs + (((warp * KS + kk) * NR + n) * 2 + hl) * 32; };
   auto load_item = [&](int it, int& ns, int& kbeg, int& kend, int& kh, int& rb, int& j, int& mrows) {
     gm.item(p, it, kh, rb, j, kbeg, kend, ns);
     const int m0 = rb * gm.rb_rows;
@@ -964,8 +966,8 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
           const float2 qv = qo >= 0 ? *reinterpret_cast<const float2*>(qp + qo + d) : make_float2(0.f, 0.f);
           split_pack(qv.x * qscale, qv.y * qscale, bh[hf], bl[hf]);
         }
-        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(qslot(kk, n, 0)), "r"(bh[0]), "r"(bh[1]) : "memory");
-        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(qslot(kk, n, 1)), "r"(bl[0]), "r"(bl[1]) : "memory");
+        *qslot(kk, n, 0) = make_uint2(bh[0], bh[1]);
+        *qslot(kk, n, 1) = make_uint2(bl[0], bl[1]);
       }
     }
   };
@@ -991,9 +993,8 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
       ldsm_x4(sb + PL + koff[kk], kl4[0], kl4[1], kl4[2], kl4[3]);   // K_lo
 #pragma unroll
       for (int n = 0; n < NR; ++n) {
-        uint32_t bh0, bh1, bl0, bl1;
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(bh0), "=r"(bh1) : "r"(qslot(kk, n, 0)) : "memory");
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(bl0), "=r"(bl1) : "r"(qslot(kk, n, 1)) : "memory");
+        const uint2 qh2 = *qslot(kk, n, 0), ql2 = *qslot(kk, n, 1);
+        const uint32_t bh0 = qh2.x, bh1 = qh2.y, bl0 = ql2.x, bl1 = ql2.y;
         float* acc = a[kk % NA][n];
         mma16816(acc, kh4, bh0, bh1);
         mma16816(acc, kh4, bl0, bl1);
@@ -1006,9 +1007,9 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
       for (int n = 0; n < NR; ++n)
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[0][n][i] += a[c][n][i];
-    const uint32_t xb = xw + (u & 1) * XB;
+    float4* const xb = xw + (u & 1) * XB;
 #pragma unroll
-    for (int n = 0; n < NR; ++n) st_shared_v4(xb + n * 512, a[0][n][0], a[0][n][1], a[0][n][2], a[0][n][3]);
+    for (int n = 0; n < NR; ++n) xb[n * 32] = make_float4(a[0][n][0], a[0][n][1], a[0][n][2], a[0][n][3]);
   };
   float mrow[NR][2], lrow[NR][2];
   float oacc[MT][NR][4];
@@ -1030,13 +1031,13 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
     // ---- S^T of stage t (fixed warp order)
     float sacc[NR][4];
     {
-      const uint32_t xb = xr + (seq & 1) * XB;
+      const float4* const xb = xr + (seq & 1) * XB;
 #pragma unroll
       for (int n = 0; n < NR; ++n) {
-        float4 v = ld_shared_v4(xb + n * 512);
+        float4 v = xb[n * 32];
 #pragma unroll
         for (int w = 1; w < 4; ++w) {
-          const float4 x = ld_shared_v4(xb + (w * NR + n) * 512);
+          const float4 x = xb[(w * NR + n) * 32];
           v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
         }
         sacc[n][0] = v.x; sacc[n][1] = v.y; sacc[n][2] = v.z; sacc[n][3] = v.w;
