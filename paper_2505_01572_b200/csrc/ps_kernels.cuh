@@ -913,7 +913,7 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   const float qscale = p.scale_log2;
   const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int d_own = warp * DW;
-  const uint32_t ring_u32 = smem_u32(ring), xbuf_u32 = smem_u32(xbuf);
+  const uint32_t ring_u32 = smem_u32(ring);
   // per-lane ldmatrix offsets inside a stage: K as the A operand (key rows,
   // non-transposed), V^T as the A operand (transposed)
   uint32_t koff[KS], voff[MT];
@@ -980,12 +980,11 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
     const int buf = u % kAttnStages;
     mbar_wait(&full[buf], (u / kAttnStages) & 1);
     const uint32_t sb = ring_u32 + buf * SB;
-    constexpr int NA = 1;   // (one chain per k step, summed at the end, measured no faster)
-    float a[NA][NR][4];
+    // one accumulator chain per n-tile: k_hi q_hi, k_hi q_lo, k_lo q_hi per k
+    // step (separate chains per k step, summed at the end, measured no faster)
+    float a[NR][4];
 #pragma unroll
-    for (int c = 0; c < NA; ++c)
-#pragma unroll
-      for (int n = 0; n < NR; ++n) a[c][n][0] = a[c][n][1] = a[c][n][2] = a[c][n][3] = 0.f;
+    for (int n = 0; n < NR; ++n) a[n][0] = a[n][1] = a[n][2] = a[n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
       uint32_t kh4[4], kl4[4];
@@ -994,22 +993,14 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
 #pragma unroll
       for (int n = 0; n < NR; ++n) {
         const uint2 qh2 = *qslot(kk, n, 0), ql2 = *qslot(kk, n, 1);
-        const uint32_t bh0 = qh2.x, bh1 = qh2.y, bl0 = ql2.x, bl1 = ql2.y;
-        float* acc = a[kk % NA][n];
-        mma16816(acc, kh4, bh0, bh1);
-        mma16816(acc, kh4, bl0, bl1);
-        mma16816(acc, kl4, bh0, bh1);
+        mma16816(a[n], kh4, qh2.x, qh2.y);
+        mma16816(a[n], kh4, ql2.x, ql2.y);
+        mma16816(a[n], kl4, qh2.x, qh2.y);
       }
     }
-#pragma unroll
-    for (int c = 1; c < NA; ++c)
-#pragma unroll
-      for (int n = 0; n < NR; ++n)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[0][n][i] += a[c][n][i];
     float4* const xb = xw + (u & 1) * XB;
 #pragma unroll
-    for (int n = 0; n < NR; ++n) xb[n * 32] = make_float4(a[0][n][0], a[0][n][1], a[0][n][2], a[0][n][3]);
+    for (int n = 0; n < NR; ++n) xb[n * 32] = make_float4(a[n][0], a[n][1], a[n][2], a[n][3]);
   };
   float mrow[NR][2], lrow[NR][2];
   float oacc[MT][NR][4];
