@@ -364,9 +364,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         for (int i = et; i < NW8; i += 128) dst[i] = src[i];
       }
       const int prev_head = ph > 0 ? P.ph[ph - 1].head : 0;
-      // Wait for the whole previous phase unless this is a GEMM phase whose
-      // epilogue needs no full-row statistic (O / down: RESID, no rstd); the
-      // mainloop of every GEMM phase is gated per tile by the X loader.
+      // Wait for the whole previous phase (its outputs, and for QKV / gate-up
+      // epilogues its row statistics); for a GEMM phase this is off the
+      // critical path -- the first accumulator needs the X tiles, which the
+      // X loader issues only after the same publication.
       named_bar(1, 128);
       if (et == 0) {   // the phase's step pointers -> the smem copy (read after the next barrier)
         sph->g.step = sstep;
