@@ -56,17 +56,26 @@ struct StepIn {                    // written by the host before every forward
   int32_t R;                       // rows in this forward, 1..kRowsCap (<= kMaxRows with the lm_head)
   int32_t pos0;                    // absolute position of row 0
   int32_t w;                       // drafts in the window (rows 1..w), verify only
-  int32_t flags;                   // kFlagLogits | kFlagSynth
+  int32_t flags;                   // kFlagLogits | kFlagSynth | kFlagChainIn | kFlagChainOut
   int32_t syn_p0;                  // generated index predicted by row row0 (= n - n_prompt)
   int32_t syn_onpath;              // 1 iff the committed context is on the target stream
   int32_t row0;                    // first prediction row (rows before it are KV catch-up)
   int32_t gen;                     // forwards so far on this stage (megakernel counter target)
   int32_t gen_head;                // forwards with lm_head so far (targets of the head phases)
-  int32_t pad2[3];
+  int32_t chain_idx;               // chained draft forwards (ps_draft): this forward's slot in the chain array
+  int32_t pad2[2];
   int32_t tokens[kRowsCap];        // row tokens: [pending, d_0, ..., d_{w-1}] (or a prefill chunk)
 };
 constexpr int kFlagLogits = 1;
 constexpr int kFlagSynth = 2;
+// Chained draft forwards (ps_draft of n > 1 tokens, launched back to back with
+// no host round trip): a forward with kFlagChainOut stores its token in
+// chain[chain_idx] (bit 31: the context is still on the synthetic target
+// stream after it); one with kFlagChainIn takes its row-0 token and that
+// on-path bit from chain[chain_idx - 1] instead of the host's StepIn.
+constexpr int kFlagChainIn = 4;
+constexpr int kFlagChainOut = 8;
+constexpr int kMaxChain = 256;     // longest chain of draft forwards (one ps_draft call)
 
 struct StepOut {                   // written by argmax_run (== ps_verify_result)
   int32_t a, next, R, kv_len;      // R = -1: a row token was out of range (nothing committed)

@@ -51,6 +51,7 @@ struct MegaParams {
   unsigned long long* dbg;         // PS_TRACE builds: [G][n_ph][8] %globaltimer stamps
   int tp_n;                        // tensor-parallel group size (1: none)
   const unsigned* peer_done[8];    // every rank's phase counters (peer memory for other ranks)
+  int32_t* chain;                  // chained draft forwards' tokens (see kFlagChainIn / kFlagChainOut)
 };
 
 // Phase-wait poll back-off cap (ns; measured: 1024 +5-8%, 256 / 64 / 32 within noise).
@@ -343,6 +344,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       const int* src = reinterpret_cast<const int*>(P.step);
       int* dst = reinterpret_cast<int*>(sstep);
       for (int i = et0; i < (int)(sizeof(StepIn) / 4); i += 128) dst[i] = src[i];
+      named_bar(1, 128);
+      if (et0 == 0 && (sstep->flags & kFlagChainIn)) {   // row 0 = the previous chained forward's token
+        const int v = __ldcg(P.chain + sstep->chain_idx - 1);
+        sstep->tokens[0] = v & 0x7FFFFFFF;
+        sstep->syn_onpath = (int)(((unsigned)v) >> 31);
+      }
     }
     const StepIn* st = P.step;
     const int R = st->R;
@@ -407,7 +414,17 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
         const int nt = Q.tp.d >> 7;
         for (int u = c * 4 + (et >> 5); u < R * nt; u += G * 4) tp_reduce_unit(Q.tp, u / nt, u % nt, lane);
       } else if (kind == PH_ARGMAX) {
-        if (c == 0) argmax_run<128>(Q.am, et, (int*)scratch, 1);
+        if (c == 0) {
+          argmax_run<128>(Q.am, et, (int*)scratch, 1);
+          if (et == 0 && (sstep->flags & kFlagChainOut)) {   // (et 0 wrote out->next)
+            const int nx = Q.am.out->next;
+            const SynthParams* sp = Q.am.syn;
+            const int g = sstep->syn_p0;
+            const bool on = (sstep->flags & kFlagSynth) && sp != nullptr && sstep->syn_onpath && g >= 0 &&
+                            g < sp->len_S && nx == sp->S[g];
+            P.chain[sstep->chain_idx] = (int)((unsigned)nx | (on ? 0x80000000u : 0u));
+          }
+        }
       } else {
         const GemmParams& gp = Q.g;
         const int kbt = gp.kb_total;

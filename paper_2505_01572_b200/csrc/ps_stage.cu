@@ -132,6 +132,10 @@ struct ps_stage {
   cudaEvent_t pf_tok_ev = nullptr;      // the staging buffer's previous copy ran
   std::vector<PfGemmParams> pf_gemm;    // [L][4]: QKV, O, gate/up, down
   double sum_prefill_ms = 0;
+  // chained draft forwards (ps_draft): device tokens + pinned copy, timing events
+  int32_t* d_chain = nullptr;
+  int32_t* h_chain = nullptr;
+  cudaEvent_t chain_ev[2] = {nullptr, nullptr};
 };
 
 // rows buckets: 16 and 32 (forwards with the lm_head: verify / draft), 64 (prefill chunks)
@@ -434,7 +438,7 @@ static ps_status launch_mega(ps_stage* S, int b, bool with_head) {
   // (tables are built at create / connect time: a build here would allocate
   // after the forward's generation counters were prepared)
   if (!S->mega_ph[key]) return fail(PS_E_INVALID, "megakernel phase table %d missing", key);
-  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, S->mega_dbg, S->tp_size, {}};
+  MegaParams mp{S->mega_ph[key], S->mega_n[key], S->d_in, S->mega_done, S->mega_dbg, S->tp_size, {}, S->d_chain};
   for (int q = 0; q < S->tp_size; ++q) mp.peer_done[q] = (const unsigned*)S->peers[q];
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(S->n_ctas);
@@ -558,6 +562,10 @@ ps_status ps_stage_destroy(ps_stage* S) {
   for (void* p : pf)
     if (p) cudaFree(p);
   if (S->h_pf_tok) cudaFreeHost(S->h_pf_tok);
+  if (S->d_chain) cudaFree(S->d_chain);
+  if (S->h_chain) cudaFreeHost(S->h_chain);
+  for (auto& ev : S->chain_ev)
+    if (ev) cudaEventDestroy(ev);
   if (S->pf_tok_ev) cudaEventDestroy(S->pf_tok_ev);
   if (S->h_page_table) cudaFreeHost(S->h_page_table);
   if (S->h_in) cudaFreeHost(S->h_in);
@@ -903,6 +911,11 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->xch, 0, S->xch_bytes));
   S->mega_done = (unsigned*)S->xch;
   S->peers[S->tp_rank] = S->xch;
+  // --- chained draft forwards
+  S_TRY(cudaMalloc(&S->d_chain, kMaxChain * 4));
+  S_TRY(cudaMemset(S->d_chain, 0, kMaxChain * 4));
+  S_TRY(cudaHostAlloc(&S->h_chain, kMaxChain * 4, cudaHostAllocDefault));
+  for (auto& ev : S->chain_ev) S_TRY(cudaEventCreate(&ev));
   // --- synthetic override (disabled)
   S_TRY(cudaMalloc(&S->d_syn, sizeof(SynthParams)));
   S->h_syn = SynthParams{};
@@ -974,8 +987,12 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
 // the megakernel's cumulative phase targets) are committed only once the
 // forward is enqueued, so a failed launch leaves them consistent with the
 // device counters.
+// chain_flags / chain_idx / syn_g: chained draft forwards (ps_draft): the
+// forward's slot in the chain array and its generated index (the host's token
+// buffer does not hold the chain's earlier tokens yet).
 static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long pos0, int w, bool with_head,
-                              bool want_logits, int row0 = 0, const int32_t* dev_window = nullptr) {
+                              bool want_logits, int row0 = 0, const int32_t* dev_window = nullptr,
+                              int chain_flags = 0, int chain_idx = 0, long long syn_g = -1) {
   ps_status st;
   if (!S->tp_connected) return fail(PS_E_INVALID, "tensor-parallel stage not connected (ps_tp_connect)");
   if ((st = ensure_pages(S, pos0 + R - 1)) != PS_OK) return st;
@@ -988,7 +1005,8 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   in->R = R;
   in->pos0 = (int32_t)pos0;
   in->w = w;
-  in->flags = (want_logits ? kFlagLogits : 0);
+  in->flags = (want_logits ? kFlagLogits : 0) | chain_flags;
+  in->chain_idx = chain_idx;
   in->syn_p0 = 0;
   in->syn_onpath = 0;
   in->row0 = row0;
@@ -996,9 +1014,9 @@ static ps_status forward_rows(ps_stage* S, const int32_t* toks, int R, long long
   in->gen_head = (int32_t)gen_head;
   if (with_head && !S->S_host.empty()) {
     in->flags |= kFlagSynth;
-    const long long g = (long long)S->tokens.size() - S->n_prompt;
+    const long long g = syn_g >= 0 ? syn_g : (long long)S->tokens.size() - S->n_prompt;
     in->syn_p0 = (int32_t)g;
-    in->syn_onpath = (g >= 0 && S->onpath == g) ? 1 : 0;
+    in->syn_onpath = (g >= 0 && S->onpath == g) ? 1 : 0;   // (a kFlagChainIn forward takes it from the chain)
   }
   for (int j = 0; j < kRowsCap; ++j) in->tokens[j] = j < R ? toks[j] : 0;
   const int b = bucket_of(R);
@@ -1309,11 +1327,65 @@ ps_status ps_verify_query(ps_stage* S, int32_t* done) {
   return fail(PS_E_CUDA, "ps_verify_query: %s", cudaGetErrorString(e));
 }
 
+// n greedy steps as a chain of forwards launched back to back: forward i > 0
+// takes its row token from forward i - 1's result on the device (kFlagChainIn),
+// so the host waits once for the chain instead of once per token.  Same
+// forwards, same arithmetic and results as n single steps.
+static ps_status draft_chain(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
+  const long long n = (long long)S->tokens.size();
+  ps_status st = catch_up(S, 1);
+  if (st != PS_OK) return st;
+  const long long kv0 = S->kv_len;
+  const int row0 = (int)(n - 1 - kv0);
+  int32_t rows[kMaxRows];
+  for (int j = 0; j <= row0; ++j) rows[j] = S->tokens[kv0 + j];
+  CU_TRY(cudaEventRecord(S->chain_ev[0], S->stream));
+  for (int i = 0; i < n_steps; ++i) {
+    const long long g = n + i - S->n_prompt;
+    if (i == 0) st = forward_rows(S, rows, row0 + 1, kv0, 0, true, false, row0, nullptr, kFlagChainOut, 0, g);
+    else st = forward_rows(S, rows, 1, n - 1 + i, 0, true, false, 0, nullptr, kFlagChainIn | kFlagChainOut, i, g);
+    if (st != PS_OK) {
+      cudaStreamSynchronize(S->stream);
+      S->kv_len = 0;                     // KV state unknown: recompute on the next forward
+      free_pages_from(S, 0);
+      return st;
+    }
+  }
+  CU_TRY(cudaEventRecord(S->chain_ev[1], S->stream));
+  CU_TRY(cudaMemcpyAsync(S->h_chain, S->d_chain, (size_t)n_steps * 4, cudaMemcpyDeviceToHost, S->stream));
+  CU_TRY(cudaStreamSynchronize(S->stream));
+  {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, S->chain_ev[0], S->chain_ev[1]) == cudaSuccess) {
+      S->last_fwd_ms = ms / n_steps;
+      S->sum_fwd_ms += ms;
+      S->n_fwd += n_steps;
+    }
+    cudaGetLastError();
+  }
+  const StepOut* r = S->h_out;           // the last forward's result
+  const long long kv_end = n - 1 + n_steps;
+  if (r->R == -1 || r->kv_len != kv_end)
+    return fail(PS_E_CUDA, "corrupt chained draft result R=%d kv_len=%d (want %lld)", r->R, r->kv_len, kv_end);
+  for (int i = 0; i < n_steps; ++i) {
+    const int t = S->h_chain[i] & 0x7FFFFFFF;
+    if (t < 0 || t >= S->vocab_full) return fail(PS_E_CUDA, "corrupt chained draft token %d", t);
+    S->tokens.push_back(t);
+    out_tokens[i] = t;
+  }
+  S->kv_len = kv_end;
+  update_onpath(S);
+  return PS_OK;
+}
+
 ps_status ps_draft(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
   if (!S || (n_steps > 0 && !out_tokens)) return fail(PS_E_INVALID, "NULL argument");
   PS_NOT_INFLIGHT(S);
   if (n_steps < 0) return fail(PS_E_INVALID, "n_steps < 0");
   CU_TRY(cudaSetDevice(S->device));
+  const long long n = (long long)S->tokens.size();
+  if (n_steps > 1 && n_steps <= kMaxChain && n >= 1 && n - 1 + n_steps <= S->max_seq && S->kv_len <= n - 1)
+    return draft_chain(S, n_steps, out_tokens);
   for (int i = 0; i < n_steps; ++i) {
     int32_t a, nxt;
     ps_status st = verify_host(S, nullptr, 0, &a, &nxt, nullptr);

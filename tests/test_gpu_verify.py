@@ -132,6 +132,35 @@ def test_synthetic_override_matches_counter_generator(toy):
     st.clear_synthetic()
 
 
+def test_chained_draft_equals_single_steps(toy):
+    """ps_draft of n tokens launches the n forwards back to back, each taking
+    its row token (and the synthetic on-path bit) from the previous forward on
+    the device; the result equals n single-step drafts bit for bit -- greedy,
+    with the synthetic override (on and off the target stream), and after a
+    lazy resync (the chain's first forward carries the catch-up rows)."""
+    s, w, w64, st, prompt = toy
+    for mode in ("greedy", "synthetic"):
+        st.prefill(prompt)
+        if mode == "synthetic":
+            base = st.draft(1)
+            st.kv_rollback(len(prompt))
+            # the target stream: the greedy token first (on path), then random
+            S = base + [int(x) for x in synth.make_prompt(s.vocab, 60, seed=6)]
+            st.set_synthetic(S, len(prompt), level=0, top=1, alphas=[0.6], seed=99)
+        chained = st.draft(12)
+        st.kv_rollback(len(prompt))
+        single = [st.draft(1)[0] for _ in range(12)]
+        assert chained == single, mode
+        other = list(prompt) + single[:3] + [(single[3] + 1) % s.vocab] + single[4:7]
+        st.resync(other)
+        c2 = st.draft(5)
+        assert st.tokens() == other + c2
+        st.resync(other)
+        s2 = [st.draft(1)[0] for _ in range(5)]
+        assert c2 == s2, mode
+    st.clear_synthetic()
+
+
 @pytest.mark.parametrize("name,layers,plen,w", [
     ("llama-68m", None, 96, 8),
     ("llama3.2-1b", None, 96, 16),
