@@ -188,11 +188,12 @@ ps_status ps_resync(ps_stage* stage, const int32_t* tokens, int32_t n);
  * "Generate next token, append to O_0"), appended to O_i; the tokens are
  * written to out_tokens[0:n_steps] (host).  Equals ps_verify with w = 0,
  * repeated.  With a synthetic-alpha override set (ps_set_synthetic), the
- * emitted token is the override's on-path token.  For 2 <= n_steps <= 256 the
- * forwards are launched back to back, each taking its row token from the
+ * emitted token is the override's on-path token.  The forwards are launched
+ * back to back in chains of up to 256, each taking its row token from the
  * previous one on the device (no host round trip per token; same results as
- * n single steps); a failure inside such a chain leaves O_i unchanged and
- * the stage's KV to be recomputed by the next forward. */
+ * n single steps); a failure inside a chain leaves the tokens of the earlier
+ * chains appended, O_i otherwise unchanged, and the stage's KV to be
+ * recomputed by the next forward. */
 ps_status ps_draft(ps_stage* stage, int32_t n_steps, int32_t* out_tokens);
 
 /* Verification pass (Alg.1).  With len(O_i) = n, window[j] (host or

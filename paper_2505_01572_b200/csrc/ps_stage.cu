@@ -1384,8 +1384,20 @@ ps_status ps_draft(ps_stage* S, int32_t n_steps, int32_t* out_tokens) {
   if (n_steps < 0) return fail(PS_E_INVALID, "n_steps < 0");
   CU_TRY(cudaSetDevice(S->device));
   const long long n = (long long)S->tokens.size();
-  if (n_steps > 1 && n_steps <= kMaxChain && n >= 1 && n - 1 + n_steps <= S->max_seq && S->kv_len <= n - 1)
-    return draft_chain(S, n_steps, out_tokens);
+  if (n_steps > 1 && n >= 1 && n - 1 + n_steps <= S->max_seq && S->kv_len <= n - 1) {
+    for (int done = 0; done < n_steps;) {          // chains of up to kMaxChain forwards
+      const int c = std::min(n_steps - done, kMaxChain);
+      ps_status st = c > 1 ? draft_chain(S, c, out_tokens + done) : PS_OK;
+      if (c == 1) {
+        int32_t a, nxt;
+        st = verify_host(S, nullptr, 0, &a, &nxt, nullptr);
+        if (st == PS_OK) out_tokens[done] = nxt;
+      }
+      if (st != PS_OK) return st;
+      done += c;
+    }
+    return PS_OK;
+  }
   for (int i = 0; i < n_steps; ++i) {
     int32_t a, nxt;
     ps_status st = verify_host(S, nullptr, 0, &a, &nxt, nullptr);
