@@ -62,6 +62,35 @@ ps_status ar_step(ps_stage* const* S, int i, const ps_run_opts* o, ps_run_stats*
   return PS_OK;
 }
 
+// m AR steps of stage i in one ps_draft call (its forwards chained on the
+// device, include/pipespec.h); per-step events and stats as m ar_step calls.
+// Stages with a virtual latency (padded per step) take them one by one.
+ps_status ar_steps(ps_stage* const* S, int i, const ps_run_opts* o, ps_run_stats* stt, SyncLog& lg, int m,
+                   std::vector<int32_t>& out) {
+  if (m <= 1 || (o->virtual_ns && o->virtual_ns[i] > 0)) {
+    for (int j = 0; j < m; ++j) {
+      int32_t t;
+      ps_status st = ar_step(S, i, o, stt, lg, &t);
+      if (st != PS_OK) return st;
+      out.push_back(t);
+    }
+    return PS_OK;
+  }
+  int64_t n = 0;
+  ps_status st = ps_stage_tokens(S[i], nullptr, 0, &n);
+  if (st != PS_OK) return st;
+  const long long t0 = now_ns();
+  std::vector<int32_t> t(m);
+  if ((st = ps_draft(S[i], m, t.data())) != PS_OK) return st;
+  stt->steps[i] += m;
+  stt->busy_ns[i] += now_ns() - t0;
+  for (int j = 0; j < m; ++j) {
+    lg.add(i, i == 0 ? PS_EV_DRAFT : PS_EV_AR, n + j, 0, 0, t[j], -1, nullptr);
+    out.push_back(t[j]);
+  }
+  return PS_OK;
+}
+
 // One verify step of stage i over window d.
 ps_status verify_step(ps_stage* const* S, int i, const std::vector<int32_t>& d, const ps_run_opts* o,
                       ps_run_stats* stt, SyncLog& lg, int32_t* a, int32_t* nxt) {
@@ -91,9 +120,7 @@ ps_status produce(ps_stage* const* S, int i, const std::vector<int32_t>& ctx, in
   const int gamma = i > 0 ? opt_gamma(o, i) : 0;
   while ((int)out.size() < m) {
     if (i == 0 || gamma == 0) {
-      int32_t t;
-      if ((st = ar_step(S, i, o, stt, lg, &t)) != PS_OK) return st;
-      out.push_back(t);
+      if ((st = ar_steps(S, i, o, stt, lg, m - (int)out.size(), out)) != PS_OK) return st;
       continue;
     }
     std::vector<int32_t> cur = ctx;
@@ -188,6 +215,9 @@ extern "C" ps_status ps_pipeline_run(ps_stage* const* S, int32_t k, const int32_
     return o->eos_id >= 0 && std::find(gen.begin(), gen.end(), o->eos_id) != gen.end();
   };
   if (o->mode == PS_MODE_AR || K == 0) {
+    if (o->eos_id < 0) {                 // no early stop: one chained ps_draft
+      if ((st = ar_steps(S, K, o, stt, lg, o->max_new_tokens, gen)) != PS_OK) return st;
+    }
     while (!done()) {
       int32_t t;
       if ((st = ar_step(S, K, o, stt, lg, &t)) != PS_OK) return st;
