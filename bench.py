@@ -664,6 +664,10 @@ def main():
     drafter.set_synthetic(S, args.prompt, level=0, top=1, alphas=[args.alpha], seed=args.seed + 1234)
 
     state = {"gen": [], "pass_ctx": []}
+    # M_1's committed buffer O_1 = prompt ++ gen as one int32 array updated in
+    # place (the resync argument is a view: no per-step list building)
+    ctx = np.zeros(args.prompt + args.gen + 2 * g + 8, dtype=np.int32)
+    ctx[:args.prompt] = prompt
 
     def step(record):
         if len(state["gen"]) >= args.gen:          # job restarts from the prompt
@@ -676,8 +680,10 @@ def main():
         if record:
             state["pass_ctx"].append(args.prompt + len(state["gen"]))
         new = d[:a] + [nxt]
+        n0 = args.prompt + len(state["gen"])
+        ctx[n0:n0 + len(new)] = new
         state["gen"] += new
-        drafter.resync(prompt + state["gen"])     # rollback signal: O_0 := O_1 (lazy KV catch-up)
+        drafter.resync(ctx[:n0 + len(new)])        # rollback signal: O_0 := O_1 (lazy KV catch-up)
         return len(new)
 
     for _ in range(args.warmup):
