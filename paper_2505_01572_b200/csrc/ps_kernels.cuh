@@ -773,13 +773,19 @@ constexpr int kAttnQOff = kAttnXBufs * kAttnXBytes;
 constexpr int kAttnQBytes = 4 * 2 * kAttnMaxNR * 2 * 32 * 8;
 constexpr int kAttnXAreaBytes = kAttnQOff + kAttnQBytes;
 // n-tiles per row block.  Any choice gives the same per-row arithmetic (see
-// above), so it is picked per forward for speed: up to 2K keys, one n-tile
-// (more, lighter items: the short phase is latency-bound); beyond, as many as
-// the rows need (one pass over the keys for up to 24 rows).  Measured on the
-// 8B (scripts/_ab_attn.sh): R = 5 at 600 keys 3.855 ms with 1 n-tile vs 3.89
-// with 3; at 8K 5.94 with 3 vs 6.22 with 1; R = 17 at 8K 9.25 vs 11.8.
+// above), so it is picked per forward for speed, from a sweep of the 8B with
+// the count forced to 1 / 2 / 3 (`gpurun_out/s4q_nr.log`, 1K-16K keys, R = 3
+// .. 17): the fewest n-tiles processed (row blocks x n-tiles each), ties to 2
+// (3 n-tiles per pass run with more register pressure); a 3-n-tile window
+// (R = 5-6 at g = 4) at up to 1.5K keys as three 1-n-tile passes (more,
+// lighter items: the short attention phase is latency-bound; the bench's
+// verify pass, 600 keys: 3.855 vs 3.89 ms).
 __host__ __device__ constexpr int attn_nr(int rows, int n_keys) {
-  return (rows <= 8 || n_keys <= 2048) ? 1 : rows <= 16 ? 2 : 3;
+  const int tiles = (rows + 7) / 8;
+  if (tiles <= 1) return 1;
+  if (tiles == 2) return 2;
+  if (tiles == 3) return n_keys <= 1536 ? 1 : 3;
+  return ((tiles + 2) / 3) * 3 < ((tiles + 1) / 2) * 2 ? 3 : 2;
 }
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
