@@ -853,12 +853,28 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   S_TRY(cudaMemset(S->amax, 0, (size_t)kMaxRows * 8));
   // --- attention workspace
   // keys per attention work item: sc 64-key chunks, a per-stage constant
-  // (results must not depend on R or on the context length): one chunk up to
-  // 16K keys, then fewer, longer items (fewer partials for the combine) with
-  // >= 128 items per KV head at max_seq
+  // (results must not depend on R or on the context length).  At max_seq, a
+  // one-row-block window has kv_heads x ceil(chunks / sc) items of 4 sc ring
+  // stages on n_ctas CTAs, and every query row combines ceil(chunks / sc)
+  // partials: sc (a power of two <= 16) minimises the makespan in stages +
+  // 0.2 per partial (ties to the larger sc), fitted to the 8B with sc forced
+  // (`profiles/r02_attn_sc_sweep.log`: best at 4K keys sc 4, 8K 8, 16K 16 --
+  // what this picks; R = 5 at 8K 5.83 ms with the previous rule (sc 1) vs
+  // 5.22 with sc 8).
   {
     const int chunks = (S->max_seq + kRowsCap + kAttnChunk - 1) / kAttnChunk;
-    S->attn_sc = std::max(1, std::min(8, chunks / 128));
+    long long best = -1;
+    // up to 1.5K keys one-chunk items: a CTA's whole item (<= 4 stages) is
+    // prefetched into the ring during the QKV phase (measured at 1K keys: sc 1
+    // 0.696 of the HBM peak vs sc 2 0.648 for R = 1)
+    for (int sc = 1; sc <= (chunks <= 24 ? 1 : 16); sc *= 2) {
+      const long long items = (long long)sh.n_kv_heads * ((chunks + sc - 1) / sc);
+      const long long cost = 10 * ((items + S->n_ctas - 1) / S->n_ctas) * 4 * sc + 2 * ((chunks + sc - 1) / sc);
+      if (best < 0 || cost <= best) {
+        best = cost;
+        S->attn_sc = sc;
+      }
+    }
     S->max_chunks = (chunks + S->attn_sc - 1) / S->attn_sc;   // item partials per (head, row block)
   }
   {

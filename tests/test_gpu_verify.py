@@ -433,19 +433,21 @@ def _oracle_verify_incremental(w64, shape, x, d, chunk=512):
 
 
 def test_long_context_16k_multichunk_items():
-    """a 16.6K context with the long-context attention items
-    (sc = 4 chunks = 256 keys per work item, streamed through the 16-key TMA
-    ring with an online softmax).  The window's rows straddle an item
-    boundary (position 16640 = 65 * 256): a verify over accepted drafts equals
-    the AR steps bit-exactly, and a verify with a rejection matches the oracle."""
+    """a ~16.6K context with the long-context attention items
+    (sc > 1 64-key chunks per work item, streamed through the 16-key TMA ring
+    with an online softmax; sc is the stage's choice for max_seq 32K).  The
+    window's rows straddle an item boundary: a verify over accepted drafts
+    equals the AR steps bit-exactly, and a verify with a rejection matches the
+    oracle."""
     from paper_2505_01572_b200 import Stage
     s = replace(synth.preset("llama3.1-8b"), name="hd128-16k", n_layers=2, d_model=1024, n_heads=8,
-                n_kv_heads=2, d_ffn=1024, vocab=4096)
+                n_kv_heads=4, d_ffn=1024, vocab=4096)
     wt = synth.make_weights(s, seed=41, device="cuda")
     w64 = synth.weights_to_numpy(wt)
-    n = 65 * 256 - 2
-    st = Stage(s, wt, max_seq=32768)         # sc = 4: 256-key items
-    assert st.info()["attn_sc"] == 4
+    st = Stage(s, wt, max_seq=32768)
+    item = 64 * st.info()["attn_sc"]         # keys per work item
+    assert item >= 128
+    n = -(-16600 // item) * item - 2          # rows n-1 .. n+3 straddle the item boundary at n + 2
     prompt = list(synth.make_prompt(s.vocab, n, seed=42))
     st.prefill(prompt)
     rows = []
