@@ -83,10 +83,10 @@ struct GemmShape {
 // Stream-K partition of one GEMM over the persistent grid.  align_pct > 0:
 // if k = floor(#SMs / n_tiles) CTAs per tile keep >= align_pct% of the SMs
 // busy, use n_tiles * k CTAs: every CTA then owns one tile-aligned segment
-// and each tile exactly k partials.  Small models' phases are latency-bound,
-// where fewer partials per tile beat the lost SMs (1B draft step 0.940 ->
-// 0.919 ms at 60%); large models' are bandwidth-bound and keep >= 95% (8B:
-// QKV on 144 CTAs -0.25%; O / down on 128 CTAs would cost +1.4%).
+// and each tile exactly k partials.  Large models' phases are bandwidth-bound
+// and take it at >= 95% (8B: QKV on 144 CTAs -0.25%; O / down on 128 CTAs
+// would cost +1.4%; 80% +1.3%).  (Round 1 also aligned small models at 60%:
+// 1B 0.940 -> 0.919 ms then; with round 2's kernels pure stream-K is 1% faster.)
 static GemmShape gemm_shape(int n_tiles, int K, int num_sms, int align_pct = 0) {
   GemmShape g;
   g.n_tiles = n_tiles;

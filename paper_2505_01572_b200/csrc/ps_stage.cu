@@ -823,7 +823,10 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
   }
   // --- GEMM partitions (persistent grid = #SMs, stream-K)
   const int n = S->n_ctas;
-  const int align = d <= 2048 ? 60 : 95;       // tile-aligned partitions where they pay (gemm_shape)
+  // tile-aligned partitions where they pay (gemm_shape): d_model > 2048 only
+  // (round 2, split-bf16 operands and the keys-as-M attention: the 1B draft
+  // step 0.955 ms with >= 60% aligned partitions, 0.946 with pure stream-K)
+  const int align = d <= 2048 ? 0 : 95;
   S->gs_qkv = gemm_shape((hq + 127) / 128 + 2 * ((hkv + 127) / 128), d, n, align);
   S->gs_o = gemm_shape((d + 127) / 128, hq, n, align);
   S->gs_gu = gemm_shape((f + 63) / 64, d, n, align);
