@@ -328,6 +328,12 @@ def run_layout(args, rank, local, world):
                     if c:
                         accept[kk] = accept.get(kk, 0) + int(c)
     launches = L.ps_kernel_launch_count() - launches0
+    # per-GPU busy time over the timed generations: the stage forwards' device
+    # time (in-library CUDA events), one entry per GPU of this rank's stage
+    my_devs = devs[my_stage] if my_stage is not None else []
+    busy_local = [(int(d_), float(st_.info()["sum_fwd_ms"])) for d_, st_ in zip(my_devs, group)]
+    busy_all = [None] * world
+    dist.all_gather_object(busy_all, busy_local)
     # synchronous SD on the same GPUs: the verifier waits for gamma drafts and the
     # drafter stops gamma ahead (lookahead = max_lead = gamma), one generation
     w0 = time.perf_counter()
@@ -392,6 +398,14 @@ def run_layout(args, rank, local, world):
             "gpu_launches": int(lt[0]),
             "clocks": clk.summary(),
         }
+        busy = {}
+        for lst in busy_all:
+            for d_, ms_ in lst or []:
+                busy[d_] = busy.get(d_, 0.0) + ms_
+        line["gpu_busy"] = {"gpus_active": sum(1 for v in busy.values() if v > 0),
+                            "busy_ms_per_gpu": {str(d_): v for d_, v in sorted(busy.items())},
+                            "busy_frac_of_timed": {str(d_): v / (1e3 * dev_s) for d_, v in sorted(busy.items())},
+                            "source": "stage forwards' in-library CUDA events over the timed generations"}
         print(json.dumps(line), flush=True)
     for st_ in group:
         st_.close()
