@@ -765,13 +765,12 @@ template <int HD> __host__ __device__ constexpr int attn_stage_bytes() { return 
 // by TMA) + its full barriers; the S exchange lives in the GEMM ring's
 // activation slots (idle during an attention phase, see ps_mega.cuh)
 constexpr int attn_smem_bytes(int /*nw*/) { return kAttnStages * attn_stage_bytes<128>() + 64; }
-constexpr int kAttnXBytes = 4 * kAttnMaxNR * 32 * 16;   // S exchange buffer: [warp][n-tile][lane] float4
-constexpr int kAttnXBufs = 2;                            // double-buffered (stage t read, t + 1 written)
-// Q^T fragments of the current item, [warp][k step][n-tile][hi|lo][lane] uint2
-// (each thread reads back only its own: no barrier), after the exchange buffers
-constexpr int kAttnQOff = kAttnXBufs * kAttnXBytes;
-constexpr int kAttnQBytes = 4 * 2 * kAttnMaxNR * 2 * 32 * 8;
-constexpr int kAttnXAreaBytes = kAttnQOff + kAttnQBytes;
+constexpr int kAttnWarps = 4;               // consumer warps = item partials per item
+static_assert(kAttnStages == kAttnWarps, "warp w consumes ring slot w (stages s = w mod 4 of an item)");
+// Q^T fragments of an item, [k step][n-tile][hi|lo][lane] uint2, double-buffered
+// by item parity (written by all 4 warps, one barrier per item)
+constexpr int kAttnQBufBytes = (128 / 16) * kAttnMaxNR * 2 * 32 * 8;
+constexpr int kAttnXAreaBytes = 2 * kAttnQBufBytes;
 // n-tiles per row block.  Any choice gives the same per-row arithmetic (see
 // above), so it is picked per forward for speed, from a sweep of the 8B with
 // the count forced to 1 / 2 / 3 (`gpurun_out/s4q_nr.log`, 1K-16K keys, R = 3
@@ -783,6 +782,9 @@ constexpr int kAttnXAreaBytes = kAttnQOff + kAttnQBytes;
 __host__ __device__ constexpr int attn_nr(int rows, int n_keys) {
   const int tiles = (rows + 7) / 8;
   if (tiles <= 1) return 1;
+#ifdef PS_ATTN_NR                           // A/B builds: n-tiles forced
+  return PS_ATTN_NR < tiles ? PS_ATTN_NR : tiles;
+#endif
   if (tiles == 2) return 2;
   if (tiles == 3) return n_keys <= 1536 ? 1 : 3;
   return ((tiles + 2) / 3) * 3 < ((tiles + 1) / 2) * 2 ? 3 : 2;
@@ -848,7 +850,9 @@ struct AttnGeom {
     kh = it / (nsc * n_rb);
     kbeg = j * p.sc * kAttnChunk;
     kend = min(n_keys, (j + 1) * p.sc * kAttnChunk);
-    ns = (kend - kbeg + kAttnStep - 1) / kAttnStep;
+    // stages, padded to a multiple of kAttnWarps (only the context's last item
+    // pads: its extra stages are fully masked, exact no-ops)
+    ns = ((kend - kbeg + kAttnStep - 1) / kAttnStep + kAttnWarps - 1) / kAttnWarps * kAttnWarps;
   }
 };
 
@@ -884,7 +888,8 @@ PS_DEV void attn_producer_seek(const AttnParams& p, const AttnGeom& gm, int it_e
     gm.item(p, u.item, u.kh, rb, j, u.kbeg, kend, u.ns);
     u.s = 0;
   }
-  u.row = attn_row(p, u.kh, u.kbeg + u.s * kAttnStep);
+  // (a padded stage past the context loads the last key's page: any finite rows)
+  u.row = attn_row(p, u.kh, min(u.kbeg + u.s * kAttnStep, gm.n_keys - 1));
 }
 // TMA of ring stage `seq` (buffer seq % 4): 16 keys x all four planes, one box
 // per 64 dims.  Keys past the context are loaded too (finite: the pool is
@@ -904,21 +909,23 @@ PS_DEV void attn_issue(const AttnParams& p, uint32_t ring_u32, uint32_t full_u32
 // (noinline: ptxas allocates a called function's registers beside the
 // caller's live ones, so the megakernel keeps little live across the call)
 //
-// Software-pipelined over the CTA's stage stream: iteration t sums stage t's
-// S^T partials, computes stage t + 1's partial K Q^T (its HMMAs overlap stage
-// t's softmax), then runs stage t's online softmax and V^T P^T; one barrier
-// per iteration publishes the t + 1 partials.  Stage t + 1 may start the next
-// item: its geometry and query fragments are loaded before its K Q^T, while
-// stage t's item state is finished (partial written) after its V^T P^T.
+// Key split: warp w takes the stages s = w, w + 4, ... of every item (ring slot
+// w: items are whole multiples of 4 stages and the CTA's stream starts at slot
+// 0), over the whole head dimension, with its own online softmax state, and
+// writes its own item partial (index 4 j + w).  Which keys a warp sees depends
+// only on their absolute positions, so rows stay bit-identical for any R.  No
+// per-stage exchange or barrier: one barrier per item publishes the item's
+// Q^T fragments (each warp converts a quarter of the k steps).  S^T is
+// accumulated in two chains (even / odd k steps) added at the end.
 // NR = attn_nr(R g): n-tiles of 8 query rows per item.
 template <int HD, int NR>
 __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, uint8_t* xbuf,
                                       int tid, int cta, int ncta, uint32_t& seq) {
-  constexpr int DW = HD / 4;          // dims per warp
-  constexpr int KS = DW / 16;         // 16-dim k steps of K Q^T per warp
-  constexpr int MT = DW / 16;         // 16-dim m tiles of V^T P^T per warp
+  constexpr int KS = HD / 16;         // 16-dim k steps of K Q^T
+  constexpr int MT = HD / 16;         // 16-dim m tiles of V^T P^T
   constexpr uint32_t SB = attn_stage_bytes<HD>();
   constexpr uint32_t PL = kAttnStep * 128;   // plane stride inside a 64-dim block
+  constexpr int QB = kAttnQBufBytes / 8;     // one Q buffer (uint2s)
   const AttnGeom gm(p);
   const int it0 = gm.first(cta, ncta), it_end = gm.first(cta + 1, ncta);
   if (it0 >= it_end) return;
@@ -927,19 +934,11 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   const int ld_q = p.ld_q;
   const float qscale = p.scale_log2;
   const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-  const int d_own = warp * DW;
-  const uint32_t ring_u32 = smem_u32(ring);
-  // per-lane ldmatrix offsets inside a stage: K as the A operand (key rows,
-  // non-transposed), V^T as the A operand (transposed)
-  uint32_t koff[KS], voff[MT];
-#pragma unroll
-  for (int kk = 0; kk < KS; ++kk) koff[kk] = attn_sw(0, (lane & 7) + ((lane >> 3) & 1) * 8, d_own + kk * 16 + (lane >> 4) * 8);
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) voff[mt] = attn_sw(2, (lane & 7) + (lane >> 4) * 8, d_own + mt * 16 + ((lane >> 3) & 1) * 8);
-  // exchange slot of (buffer b, warp w, n-tile n, this lane): xbuf + ((b * 4 + w) * NR + n) * 512 + lane * 16
-  float4* const xw = reinterpret_cast<float4*>(xbuf) + warp * NR * 32 + lane;
-  const float4* const xr = reinterpret_cast<const float4*>(xbuf) + lane;
-  constexpr int XB = 4 * NR * 32;            // one buffer (float4s)
+  const uint32_t sb = smem_u32(ring) + warp * SB;       // this warp's ring slot
+  // per-lane ldmatrix rows: K as the A operand (key rows), V^T as the A operand (transposed)
+  const int kr = (lane & 7) + ((lane >> 3) & 1) * 8, kd = (lane >> 4) * 8;
+  const int vr = (lane & 7) + (lane >> 4) * 8, vd = ((lane >> 3) & 1) * 8;
+  uint2* const qs = reinterpret_cast<uint2*>(xbuf) + lane;
 #if PS_TRACE
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 0);
   unsigned long long tr_wait = 0, tr_qk = 0, tr_pv = 0, tr_t = globaltimer();
@@ -954,18 +953,13 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
   do {                   \
   } while (0)
 #endif
-  // ---- item state: cur (stage t) and nxt (stage t + 1)
-  int c_item = it0, c_s = 0, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_mrows;
-  int n_item = it0, n_s = 0, n_ns = 0, n_kbeg = 0, n_kend = 0, n_kh = 0, n_rb = 0, n_j = 0, n_mrows = 0;
-  // this thread's Q^T B fragment (hi / lo) of k step kk, n-tile n: a uint2 at qslot(kk, n, hl)
-  // (plain C++ accesses: the compiler orders them against each other and may
-  // schedule them freely around the MMAs)
-  uint2* const qs = reinterpret_cast<uint2*>(xbuf + kAttnQOff) + lane;
-  auto qslot = [&](int kk, int n, int hl) { return qs + (((warp * KS + kk) * NR + n) * 2 + hl) * 32; };
-  auto load_item = [&](int it, int& ns, int& kbeg, int& kend, int& kh, int& rb, int& j, int& mrows) {
+  for (int it = it0; it < it_end; ++it) {
+    int kh, rb, j, kbeg, kend, ns;
     gm.item(p, it, kh, rb, j, kbeg, kend, ns);
     const int m0 = rb * gm.rb_rows;
-    mrows = min(gm.rb_rows, gm.rows - m0);
+    const int mrows = min(gm.rb_rows, gm.rows - m0);
+    uint2* const qb = qs + (it & 1) * QB;
+    // ---- Q^T fragments of this item: this warp's k steps kk = warp mod 4
 #pragma unroll
     for (int n = 0; n < NR; ++n) {
       // B fragment column n-index gq = query row 8 n + gq of the block
@@ -974,52 +968,21 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
       const int qo = m < mrows ? r * ld_q + h * HD : -1;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
+        if ((kk & 3) != warp) continue;
         uint32_t bh[2], bl[2];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-          const int d = d_own + kk * 16 + tq * 2 + hf * 8;
+          const int d = kk * 16 + tq * 2 + hf * 8;
           const float2 qv = qo >= 0 ? *reinterpret_cast<const float2*>(qp + qo + d) : make_float2(0.f, 0.f);
           split_pack(qv.x * qscale, qv.y * qscale, bh[hf], bl[hf]);
         }
-        *qslot(kk, n, 0) = make_uint2(bh[0], bh[1]);
-        *qslot(kk, n, 1) = make_uint2(bl[0], bl[1]);
+        qb[((kk * NR + n) * 2 + 0) * 32] = make_uint2(bh[0], bh[1]);
+        qb[((kk * NR + n) * 2 + 1) * 32] = make_uint2(bl[0], bl[1]);
       }
     }
-  };
-  // causal limit of S^T column (row 8 n + 2 tq + e of row block rb): the row's position, within the item
-  auto qpos_of = [&](int rb, int kend, int n, int e) {
-    return min(kend - 1, pos0 + (rb * gm.rb_rows + n * 8 + tq * 2 + e) / g);
-  };
-  // partial S^T of stage `u` (ring sequence number) over this warp's dims -> exchange buffer u & 1
-  auto qk_partial = [&](uint32_t u) {
-    const int buf = u % kAttnStages;
-    mbar_wait(&full[buf], (u / kAttnStages) & 1);
-    const uint32_t sb = ring_u32 + buf * SB;
-    // one accumulator chain per n-tile: k_hi q_hi, k_hi q_lo, k_lo q_hi per k
-    // step (separate chains per k step, summed at the end, measured no faster)
-    float a[NR][4];
-#pragma unroll
-    for (int n = 0; n < NR; ++n) a[n][0] = a[n][1] = a[n][2] = a[n][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-      uint32_t kh4[4], kl4[4];
-      ldsm_x4(sb + koff[kk], kh4[0], kh4[1], kh4[2], kh4[3]);        // K_hi
-      ldsm_x4(sb + PL + koff[kk], kl4[0], kl4[1], kl4[2], kl4[3]);   // K_lo
-#pragma unroll
-      for (int n = 0; n < NR; ++n) {
-        const uint2 qh2 = *qslot(kk, n, 0), ql2 = *qslot(kk, n, 1);
-        mma16816(a[n], kh4, qh2.x, qh2.y);
-        mma16816(a[n], kh4, ql2.x, ql2.y);
-        mma16816(a[n], kl4, qh2.x, qh2.y);
-      }
-    }
-    float4* const xb = xw + (u & 1) * XB;
-#pragma unroll
-    for (int n = 0; n < NR; ++n) xb[n * 32] = make_float4(a[n][0], a[n][1], a[n][2], a[n][3]);
-  };
-  float mrow[NR][2], lrow[NR][2];
-  float oacc[MT][NR][4];
-  auto reset_state = [&]() {
+    named_bar(2, 128);
+    float mrow[NR][2], lrow[NR][2];
+    float oacc[MT][NR][4];
 #pragma unroll
     for (int n = 0; n < NR; ++n) {
       mrow[n][0] = mrow[n][1] = -INFINITY;
@@ -1027,140 +990,117 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) oacc[mt][n][0] = oacc[mt][n][1] = oacc[mt][n][2] = oacc[mt][n][3] = 0.f;
     }
-  };
-  // ---- prologue: stage 0's partial S^T
-  load_item(c_item, c_ns, c_kbeg, c_kend, c_kh, c_rb, c_j, c_mrows);
-  reset_state();
-  qk_partial(seq);
-  named_bar(2, 128);
-  while (true) {
-    // ---- S^T of stage t (fixed warp order)
-    float sacc[NR][4];
-    {
-      const float4* const xb = xr + (seq & 1) * XB;
+    // causal limit of S^T column (row 8 n + 2 tq + e of the block): the row's position, within the item
+    auto qpos_of = [&](int n, int e) { return min(kend - 1, pos0 + (m0 + n * 8 + tq * 2 + e) / g); };
+    for (int st = warp; st < ns; st += kAttnWarps) {
+      const uint32_t u = seq + st;           // ring sequence number (u % 4 == warp)
+      mbar_wait(&full[warp], (u / kAttnStages) & 1);
+      PS_ATTN_LAP(tr_wait);
+      // ---- S^T = K Q^T over all dims: chains a (even k steps) and b (odd)
+      float a[NR][4], b[NR][4];
+#pragma unroll
+      for (int n = 0; n < NR; ++n) a[n][0] = a[n][1] = a[n][2] = a[n][3] = b[n][0] = b[n][1] = b[n][2] = b[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        uint32_t kh4[4], kl4[4];
+        const uint32_t ko = attn_sw(0, kr, kk * 16 + kd);
+        ldsm_x4(sb + ko, kh4[0], kh4[1], kh4[2], kh4[3]);        // K_hi
+        ldsm_x4(sb + PL + ko, kl4[0], kl4[1], kl4[2], kl4[3]);   // K_lo
+#pragma unroll
+        for (int n = 0; n < NR; ++n) {
+          const uint2 qh2 = qb[((kk * NR + n) * 2 + 0) * 32], ql2 = qb[((kk * NR + n) * 2 + 1) * 32];
+          float* acc = (kk & 1) ? b[n] : a[n];
+          mma16816(acc, kh4, qh2.x, qh2.y);
+          mma16816(acc, kh4, ql2.x, ql2.y);
+          mma16816(acc, kl4, qh2.x, qh2.y);
+        }
+      }
+      PS_ATTN_LAP(tr_qk);
+      // ---- mask, online softmax
+      const int k0 = kbeg + st * kAttnStep;
+      float scale[NR][2];
+      uint32_t pbh[NR][2], pbl[NR][2];     // P^T as B fragments (keys 0-7 / 8-15 of the stage), hi / lo
 #pragma unroll
       for (int n = 0; n < NR; ++n) {
-        float4 v = xb[n * 32];
+        float pv[4];
 #pragma unroll
-        for (int w = 1; w < 4; ++w) {
-          const float4 x = xb[(w * NR + n) * 32];
-          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+        for (int e = 0; e < 2; ++e) {
+          // this thread's S^T entries of row 8 n + 2 tq + e: keys gq (c_e) and gq + 8 (c_{2+e})
+          float sa = a[n][e] + b[n][e], sb8 = a[n][2 + e] + b[n][2 + e];
+          const int qpos = qpos_of(n, e);
+          if (k0 + gq > qpos) sa = -INFINITY;
+          if (k0 + gq + 8 > qpos) sb8 = -INFINITY;
+          float mx = fmaxf(sa, sb8);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+          const float mn = fmaxf(mrow[n][e], mx);
+          scale[n][e] = (mrow[n][e] == -INFINITY) ? 0.f : ex2_approx(mrow[n][e] - mn);
+          mrow[n][e] = mn;
+          const float pa = (mn == -INFINITY) ? 0.f : ex2_approx(sa - mn);
+          const float pb = (mn == -INFINITY) ? 0.f : ex2_approx(sb8 - mn);
+          // this lane's share of the row sum (its two keys); the lanes' shares
+          // are added once per item (the max must be row-uniform, the sum not)
+          lrow[n][e] = lrow[n][e] * scale[n][e] + (pa + pb);
+          pv[e] = pa;
+          pv[2 + e] = pb;
         }
-        sacc[n][0] = v.x; sacc[n][1] = v.y; sacc[n][2] = v.z; sacc[n][3] = v.w;
+        uint32_t h01, l01, h23, l23;
+        split_pack(pv[0], pv[1], h01, l01);      // key gq, rows 2 tq, 2 tq + 1
+        split_pack(pv[2], pv[3], h23, l23);      // key gq + 8
+        pbh[n][0] = movm_t(h01);                 // -> row gq, keys 2 tq, 2 tq + 1 (the B layout)
+        pbh[n][1] = movm_t(h23);
+        pbl[n][0] = movm_t(l01);
+        pbl[n][1] = movm_t(l23);
       }
-    }
-    PS_ATTN_LAP(tr_wait);
-    // ---- stage t + 1: next position in the stream; its partial S^T
-    const bool more = (c_s + 1 < c_ns) || (c_item + 1 < it_end);
-    if (more) {
-      if (c_s + 1 < c_ns) {
-        n_item = c_item; n_s = c_s + 1; n_ns = c_ns; n_kbeg = c_kbeg; n_kend = c_kend; n_kh = c_kh; n_rb = c_rb;
-        n_j = c_j; n_mrows = c_mrows;
-      } else {
-        n_item = c_item + 1;
-        n_s = 0;
-        load_item(n_item, n_ns, n_kbeg, n_kend, n_kh, n_rb, n_j, n_mrows);
+      // ---- O^T = O^T * scale + V^T P^T over all dims
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t vh[4], vl[4];
+        const uint32_t vo = attn_sw(2, vr, mt * 16 + vd);
+        ldsm_x4_t(sb + vo, vh[0], vh[1], vh[2], vh[3]);          // V_hi
+        ldsm_x4_t(sb + PL + vo, vl[0], vl[1], vl[2], vl[3]);     // V_lo
+#pragma unroll
+        for (int n = 0; n < NR; ++n) {
+          oacc[mt][n][0] *= scale[n][0]; oacc[mt][n][1] *= scale[n][1];
+          oacc[mt][n][2] *= scale[n][0]; oacc[mt][n][3] *= scale[n][1];
+          mma16816(oacc[mt][n], vh, pbh[n][0], pbh[n][1]);
+          mma16816(oacc[mt][n], vl, pbh[n][0], pbh[n][1]);
+          mma16816(oacc[mt][n], vh, pbl[n][0], pbl[n][1]);
+        }
       }
-      qk_partial(seq + 1);
+      // this warp is done with the slot (K/V fragments are in registers)
+      __syncwarp();
+      if (lane == 0) mbar_arrive_n(&empty[warp], kAttnWarps);   // (the barrier counts 4 consumers)
+      PS_ATTN_LAP(tr_pv);
     }
-    PS_ATTN_LAP(tr_qk);
-    // ---- stage t: mask, online softmax, O^T (own dims) = O^T * scale + V^T P^T
-    const int k0 = c_kbeg + c_s * kAttnStep;
-    const uint32_t sb = ring_u32 + (seq % kAttnStages) * SB;
-    uint32_t vh[MT][4], vl[MT][4];
+    seq += ns;
+    // ---- this warp's item partial -> workspace [kh][4 j + warp][row][HD] (all dims)
+    const size_t base = ((size_t)kh * p.max_chunks + (size_t)j * kAttnWarps + warp) * p.rows_cap + (size_t)m0;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      ldsm_x4_t(sb + voff[mt], vh[mt][0], vh[mt][1], vh[mt][2], vh[mt][3]);                        // V_hi
-      ldsm_x4_t(sb + PL + voff[mt], vl[mt][0], vl[mt][1], vl[mt][2], vl[mt][3]);                      // V_lo
-    }
-    float scale[NR][2];
-    uint32_t pbh[NR][2], pbl[NR][2];     // P^T as B fragments (keys 0-7 / 8-15 of the stage), hi / lo
-#pragma unroll
-    for (int n = 0; n < NR; ++n) {
-      float pv[4];
+    for (int n = 0; n < NR; ++n)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        // this thread's S^T entries of row 8 n + 2 tq + e: keys gq (c_e) and gq + 8 (c_{2+e})
-        float sa = sacc[n][e], sb8 = sacc[n][2 + e];
-        const int qpos = qpos_of(c_rb, c_kend, n, e);
-        if (k0 + gq > qpos) sa = -INFINITY;
-        if (k0 + gq + 8 > qpos) sb8 = -INFINITY;
-        float mx = fmaxf(sa, sb8);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        const float mn = fmaxf(mrow[n][e], mx);
-        scale[n][e] = (mrow[n][e] == -INFINITY) ? 0.f : ex2_approx(mrow[n][e] - mn);
-        mrow[n][e] = mn;
-        const float pa = (mn == -INFINITY) ? 0.f : ex2_approx(sa - mn);
-        const float pb = (mn == -INFINITY) ? 0.f : ex2_approx(sb8 - mn);
-        // this lane's share of the row sum (its two keys); the lanes' shares
-        // are added once per item (the max must be row-uniform, the sum not)
-        lrow[n][e] = lrow[n][e] * scale[n][e] + (pa + pb);
-        pv[e] = pa;
-        pv[2 + e] = pb;
-      }
-      uint32_t h01, l01, h23, l23;
-      split_pack(pv[0], pv[1], h01, l01);      // key gq, rows 2 tq, 2 tq + 1
-      split_pack(pv[2], pv[3], h23, l23);      // key gq + 8
-      pbh[n][0] = movm_t(h01);                 // -> row gq, keys 2 tq, 2 tq + 1 (the B layout)
-      pbh[n][1] = movm_t(h23);
-      pbl[n][0] = movm_t(l01);
-      pbl[n][1] = movm_t(l23);
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int n = 0; n < NR; ++n) {
-        oacc[mt][n][0] *= scale[n][0]; oacc[mt][n][1] *= scale[n][1];
-        oacc[mt][n][2] *= scale[n][0]; oacc[mt][n][3] *= scale[n][1];
+        float ls = lrow[n][e];                // row sum over the 8 key lanes (fixed tree)
+        ls += __shfl_xor_sync(0xffffffffu, ls, 4);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 8);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 16);
+        lrow[n][e] = ls;
       }
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+    for (int n = 0; n < NR; ++n)
 #pragma unroll
-      for (int n = 0; n < NR; ++n) {
-        mma16816(oacc[mt][n], vh[mt], pbh[n][0], pbh[n][1]);
-        mma16816(oacc[mt][n], vl[mt], pbh[n][0], pbh[n][1]);
-        mma16816(oacc[mt][n], vh[mt], pbl[n][0], pbl[n][1]);
-      }
-    // this warp is done with stage t's buffer (K/V fragments are in registers)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[seq % kAttnStages]);
-    PS_ATTN_LAP(tr_pv);
-    if (c_s + 1 == c_ns) {
-      // ---- item partial -> workspace [kh][j][row][HD] (own dims; m, l by warp 0)
-      const size_t base = ((size_t)c_kh * p.max_chunks + c_j) * p.rows_cap + (size_t)c_rb * gm.rb_rows;
+      for (int e = 0; e < 2; ++e) {
+        const int m = n * 8 + tq * 2 + e;
+        if (m >= mrows) continue;           // a later row block's row (or none)
+        float* op = p.ws_o + (base + m) * HD + gq;
 #pragma unroll
-      for (int n = 0; n < NR; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          float ls = lrow[n][e];                // row sum over the 8 key lanes (fixed tree)
-          ls += __shfl_xor_sync(0xffffffffu, ls, 4);
-          ls += __shfl_xor_sync(0xffffffffu, ls, 8);
-          ls += __shfl_xor_sync(0xffffffffu, ls, 16);
-          lrow[n][e] = ls;
+        for (int mt = 0; mt < MT; ++mt) {
+          __stcg(op + mt * 16, oacc[mt][n][e]);
+          __stcg(op + mt * 16 + 8, oacc[mt][n][2 + e]);
         }
-#pragma unroll
-      for (int n = 0; n < NR; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int m = n * 8 + tq * 2 + e;
-          if (m >= c_mrows) continue;         // a later row block's row (or none)
-          float* op = p.ws_o + (base + m) * HD + d_own + gq;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            __stcg(op + mt * 16, oacc[mt][n][e]);
-            __stcg(op + mt * 16 + 8, oacc[mt][n][2 + e]);
-          }
-          if (warp == 0 && gq == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[n][e], lrow[n][e]));
-        }
-      reset_state();
-    }
-    ++seq;
-    if (!more) break;
-    c_item = n_item; c_s = n_s; c_ns = n_ns; c_kbeg = n_kbeg; c_kend = n_kend; c_kh = n_kh; c_rb = n_rb; c_j = n_j;
-    c_mrows = n_mrows;
-    named_bar(2, 128);                       // stage t + 1's partials are published
+        if (gq == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml + (base + m) * 2), make_float2(mrow[n][e], lrow[n][e]));
+      }
   }
 #if PS_TRACE
   if (tid == 0) PS_TRACE_STAMP(p.dbg, cta * 8 + 4);
@@ -1173,7 +1113,8 @@ __device__ __noinline__ void attn_run(const AttnParams& p, uint8_t* ring, uint64
 #undef PS_ATTN_LAP
 }
 
-// Combine of the item partials (next phase): one CTA per output row (kh, m),
+// Combine of the item partials (next phase; kAttnWarps per item, partial
+// 4 j + w from warp w of item j): one CTA per output row (kh, m),
 // its 4 warps take the partials c = w, w + 4, ... (a split independent of the
 // partial count, so the extra all-masked partials of a longer window add exact
 // zeros: row-bucket invariance).  Per row M = max_c m_c, L = sum_c 2^(m_c - M)
@@ -1185,7 +1126,7 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
   const int R = st->R, pos0 = st->pos0;
   const int g = p.H / p.hkv;
   const int rows = R * g;
-  const int np = ((pos0 + R + kAttnChunk - 1) / kAttnChunk + p.sc - 1) / p.sc;   // item partials
+  const int np = kAttnWarps * (((pos0 + R + kAttnChunk - 1) / kAttnChunk + p.sc - 1) / p.sc);   // item partials
   const int warp = tid >> 5, lane = tid & 31;
   constexpr int DPL = HD / 32;
   using VecT = typename std::conditional<DPL == 4, float4, float2>::type;

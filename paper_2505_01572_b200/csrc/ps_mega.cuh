@@ -75,7 +75,7 @@ struct MegaSmem {
   static constexpr int kOffKvRow = kOffRstd + RP * 4;
   static constexpr int kOffAttn = (kOffKvRow + RP * 8 + 1023) / 1024 * 1024;   // TMA 128B-swizzle dst
   // the attention's S exchange lives in the activation slots (idle in an attention phase)
-  static_assert(kMegaStages * kXBytes >= kAttnXAreaBytes, "attention S exchange + Q fragments live in the X slots");
+  static_assert(kMegaStages * kXBytes >= kAttnXAreaBytes, "attention Q fragments live in the X slots");
   static constexpr int kAttnBytes = attn_smem_bytes(4);
   static constexpr int kOffBar = kOffAttn + kAttnBytes;
   static constexpr int kOffMisc = kOffBar + (2 * kMegaStages + 4) * 8;
@@ -118,7 +118,7 @@ PS_DEV bool poll_ready(const unsigned* p, unsigned target) {
 
 // Attention K/V ring producer (one thread of the X-loader warp): this CTA's
 // stream of 16-key stages of attention phase pa, each issued once its buffer
-// is released by the 4 consumer warps.  Stages whose keys are all below pos0
+// is released by its consumer (warp w for slot w, arriving for all 4).  Stages whose keys are all below pos0
 // go out immediately; the first one reaching the window's rows waits for the
 // QKV phase (pa - 1) to be published grid-wide (its K/V rows are new).
 template <int HD>
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) mega_kernel(const __grid_cons
       if (kind == PH_EMBED) {
         for (int r = c; r < R; r += G) embed_row(Q.em, r, et);
       } else if (kind == PH_ATTN) {          // chunk partials; combined in the next phase
-        // (the S exchange uses the X slots: during an attention phase this CTA's
+        // (the Q fragments use the X slots: during an attention phase this CTA's
         // previous GEMM phase is consumed, and the next one's X tiles load only
         // after the combine phase is published)
         const int nr = attn_nr(sstep->R * (Q.a.H / Q.a.hkv), sstep->pos0 + sstep->R);

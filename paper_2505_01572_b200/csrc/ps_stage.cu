@@ -878,7 +878,10 @@ ps_status ps_stage_create(const ps_model_shape* shape, const ps_weights* w, cons
         S->attn_sc = sc;
       }
     }
-    S->max_chunks = (chunks + S->attn_sc - 1) / S->attn_sc;   // item partials per (head, row block)
+#ifdef PS_ATTN_SC                               // A/B builds: keys per item forced
+    S->attn_sc = PS_ATTN_SC;
+#endif
+    S->max_chunks = kAttnWarps * ((chunks + S->attn_sc - 1) / S->attn_sc);   // item partials per (head, row block)   // item partials per (head, row block)
   }
   {
     const int g = sh.n_heads / sh.n_kv_heads;

@@ -466,3 +466,37 @@ def test_long_context_16k_multichunk_items():
     check_logits(logits, ref["logits"])
     check_verify((a, nxt), ref, len(window))
     st.close()
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_attention_ragged_last_item(hd):
+    """Key-split attention (warp w takes the stages w mod 4 of an item and
+    writes its own partial) at a context whose last item is ragged (3 of its 4
+    stages hold keys; the padded stage is fully masked): a verify over accepted
+    drafts equals the AR steps bit-exactly, and a verify with a rejection
+    matches the oracle."""
+    from paper_2505_01572_b200 import Stage
+    s = replace(synth.preset("llama3.1-8b"), name=f"ragged-hd{hd}", n_layers=2, d_model=8 * hd, n_heads=8,
+                n_kv_heads=2, head_dim=hd, d_ffn=1024, vocab=4096)
+    wt = synth.make_weights(s, seed=51, device="cuda")
+    w64 = synth.weights_to_numpy(wt)
+    n = 713                                   # 11 full 64-key chunks + a ragged one
+    st = Stage(s, wt, max_seq=n + 64)
+    prompt = list(synth.make_prompt(s.vocab, n, seed=52))
+    st.prefill(prompt)
+    rows = []
+    for _ in range(9):
+        a, nxt, lg = st.verify([], want_logits=True)
+        rows.append(lg[0])
+    stream = st.tokens()[n:]
+    st.prefill(prompt)
+    a, nxt, logits = st.verify(stream[:8], want_logits=True)
+    assert a == 8 and nxt == stream[8]
+    assert np.array_equal(logits, np.stack(rows))
+    st.prefill(prompt)
+    window = stream[:3] + [(stream[3] + 5) % s.vocab] + stream[4:6]
+    a, nxt, logits = st.verify(window, want_logits=True)
+    ref = L.verify(w64, s, prompt, window)
+    check_logits(logits, ref["logits"])
+    check_verify((a, nxt), ref, len(window))
+    st.close()
