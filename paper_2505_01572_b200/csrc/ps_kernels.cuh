@@ -1135,6 +1135,10 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
   for (int it = cta; it < p.hkv * rows; it += ncta) {
     const int kh = it / rows, mg = it % rows;
     const size_t rbase = (size_t)kh * p.max_chunks * cstride + mg;   // partial c of this row: rbase + c * cstride
+    // this warp's first 32 partials' (m, l) go out before the M pass (they
+    // do not depend on M: one round trip for both)
+    float2 ml0 = make_float2(-INFINITY, 0.f);
+    if (warp + 4 * lane < np) ml0 = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (rbase + (warp + 4 * lane) * cstride) * 2));
     float M = -INFINITY;
     for (int c = lane; c < np; c += 32) M = fmaxf(M, __ldcg(p.ws_ml + (rbase + c * cstride) * 2));
 #pragma unroll
@@ -1148,7 +1152,7 @@ PS_DEV void attn_combine(const AttnParams& p, float* xs, int tid, int cta, int n
       const int cl = warp + 4 * (i0 + lane);
       float sc = 0.f;
       if (cl < np) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (rbase + cl * cstride) * 2));
+        const float2 ml = i0 == 0 ? ml0 : __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (rbase + cl * cstride) * 2));
         sc = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
         Lp += sc * ml.y;
       }
